@@ -1,0 +1,117 @@
+/* crac_engine.h — C-ABI of the B200 checkpoint engine (libcrac_b200.so).
+ *
+ * This is the boundary a non-C++ caller binds (ctypes / cgo / JNI; see
+ * INTEGRATION.md).  Every entry point wraps one reference C++ interface
+ * (/root/reference/proj, cited per function) with the B200 implementation
+ * behind it; handles are opaque, all sizes are bytes, `stream` < 0 means
+ * "synchronous" (std::nullopt in the reference API).
+ *
+ * Return convention: 0 on success, otherwise 1 + the cracsim::Errc code of the
+ * failure (ImageCorrupt = 14, ReplayDivergence = 13, QuiesceTimeout = 12,
+ * DeviceFault = 17, ...); crac_last_error() returns the message of the last
+ * failure on the calling thread.  Nothing here falls back to a CPU path: with
+ * no usable GPU every call that needs one returns DeviceFault.
+ */
+#ifndef CRAC_ENGINE_H
+#define CRAC_ENGINE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct crac_session crac_session_t; /* cracsim::Session */
+typedef struct crac_image crac_image_t;     /* cracsim::PinnedImage */
+
+/* Device-timed phases of the last drain/refill (cracsim::DrainStats). */
+typedef struct crac_stats {
+  double total_ms, hash_ms, pack_ms, copy_ms;
+  uint64_t hash_bytes, hash_launches, pack_launches, pack_bytes;
+  uint64_t d2h_bytes, h2d_bytes, image_bytes, dirty_chunks, total_chunks;
+  int32_t incremental;
+  int32_t reserved;
+} crac_stats_t;
+
+const char* crac_last_error(void);
+int crac_abi_version(void); /* 1 */
+
+/* Session — ref: include/cracsim/ckpt_engine.hpp:18-55 (SessionConfig, Session) */
+int crac_session_create(uint64_t seed, uint64_t arena_bytes, int mode, uint32_t quiesce_timeout_ms,
+                        crac_session_t** out);
+void crac_session_destroy(crac_session_t* s);
+int crac_session_fixed_va(crac_session_t* s); /* 1 if the arena sits at kArenaBase */
+
+/* RuntimeApi — ref: include/cracsim/shim.hpp:159-184 (the interposed calls) */
+int crac_alloc(crac_session_t* s, uint8_t kind, uint64_t size, uint64_t* id, uint64_t* address);
+int crac_free(crac_session_t* s, uint64_t id);
+int crac_stream_create(crac_session_t* s, uint64_t* id);
+int crac_stream_destroy(crac_session_t* s, uint64_t id);
+/* Kernel bodies resolve by name from the standard catalog; other names get
+ * an empty body (ref: include/cracsim/kernels.hpp:16-21). */
+int crac_register_fat_binary(crac_session_t* s, uint32_t n, const char* const* names,
+                             const uint32_t* buffer_arity, const uint32_t* scalar_arity,
+                             uint64_t* handle);
+int crac_unregister_fat_binary(crac_session_t* s, uint64_t handle);
+int crac_launch(crac_session_t* s, uint64_t stream, const char* kernel, uint32_t nbuf,
+                const uint64_t* buf_ids, const uint64_t* buf_offsets, uint32_t nscalar,
+                const uint64_t* scalars);
+int crac_copy_h2d(crac_session_t* s, uint64_t id, uint64_t offset, const void* src, uint64_t n,
+                  int64_t stream);
+int crac_copy_d2h(crac_session_t* s, void* dst, uint64_t id, uint64_t offset, uint64_t n,
+                  int64_t stream);
+int crac_copy_d2d(crac_session_t* s, uint64_t dst_id, uint64_t dst_off, uint64_t src_id,
+                  uint64_t src_off, uint64_t n, int64_t stream);
+int crac_synchronize(crac_session_t* s);
+int crac_page_read(crac_session_t* s, uint64_t id, uint64_t offset, uint64_t n, uint8_t side,
+                   void* out);
+int crac_page_write(crac_session_t* s, uint64_t id, uint64_t offset, const void* src, uint64_t n,
+                    uint8_t side);
+int crac_set_app_state(crac_session_t* s, const void* src, uint64_t n);
+
+/* Checkpoint drain — ref: src/ckpt_engine.cpp:29-61 + src/image.cpp:383-399.
+ * The image lives in `img` (page-locked, reused across calls). */
+int crac_image_create(crac_image_t** out);
+void crac_image_destroy(crac_image_t* img);
+int crac_image_view(crac_image_t* img, const uint8_t** data, uint64_t* size);
+int crac_checkpoint(crac_session_t* s, crac_image_t* img, crac_stats_t* stats);
+int crac_checkpoint_incremental(crac_session_t* s, crac_image_t* img, crac_stats_t* stats);
+/* checkpoint(Session&) -> Snapshot -> encode_image, into a malloc'd buffer
+ * released with crac_buffer_free (the reference-shaped value API). */
+int crac_checkpoint_value(crac_session_t* s, uint8_t** image, uint64_t* size);
+
+/* Restart refill — ref: src/ckpt_engine.cpp:120-171 + src/image.cpp:280-345. */
+int crac_restart(const void* image, uint64_t size, int mode, crac_session_t** out,
+                 crac_stats_t* stats);
+/* decode_image validation only — ref: src/image.cpp:401-404. */
+int crac_decode_check(const void* image, uint64_t size);
+/* summarize_image — ref: src/image.cpp:406-413; lengths/crcs: 7 each;
+ * totals: log_entries, active, payload_bytes, uvm_bytes, file_bytes. */
+int crac_summarize(const void* image, uint64_t size, uint64_t* lengths, uint32_t* crcs,
+                   uint64_t* totals);
+
+/* Introspection (tests) — ref: include/cracsim/device_core.hpp:117-140 */
+int crac_debug_dump(crac_session_t* s, char** out);
+void crac_buffer_free(void* p);
+int crac_log_size(crac_session_t* s, uint64_t* n);
+int crac_live_records(crac_session_t* s, uint64_t cap, uint64_t* ids, uint8_t* kinds,
+                      uint64_t* sizes, uint64_t* addresses, uint64_t* n);
+int crac_managed_pages(crac_session_t* s, uint64_t id, uint64_t cap, uint8_t* flags, uint64_t* n);
+int crac_read_raw(crac_session_t* s, uint64_t address, uint64_t n, void* out);
+int crac_backing_ptr(crac_session_t* s, uint64_t id, uint64_t* ptr);
+
+/* Workload fixtures (bench / tests): synthetic content (see crac_gpu.h) and
+ * the C5 epoch mutation over every live Device allocation. */
+int crac_fill_synthetic(crac_session_t* s, uint64_t id, uint64_t seed, uint8_t managed_side);
+int crac_mutate_device(crac_session_t* s, uint64_t seed, uint64_t epoch, uint64_t threshold,
+                       uint64_t* mutated_chunks);
+
+/* Kernel-level entry for parity tests: CRC of every 64 KiB (chunk_bytes)
+ * chunk of a host buffer, computed by K1 on the GPU. */
+int crac_hash_host_buffer(const void* data, uint64_t n, uint32_t chunk_bytes, uint32_t* crc_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CRAC_ENGINE_H */

@@ -1,0 +1,113 @@
+/* crac_gpu.h — C-ABI kernel layer of the B200 checkpoint drain / restart
+ * refill (sm_100a).  Plain pointers and sizes only; `stream` is a
+ * cudaStream_t passed as void* so this header needs no CUDA includes.
+ *
+ * Conventions:
+ *   - every function returns 0 or a cudaError_t value and never throws;
+ *   - buffers are caller-owned device (or UVA-visible pinned/managed)
+ *     pointers; nothing here allocates;
+ *   - work is enqueued asynchronously on `stream`; re-entrant per stream;
+ *   - one process per GPU; crac_gpu_init() once per process/device.
+ *
+ * Each kernel replaces a CPU step of the reference (/root/reference/proj):
+ *   crac_chunk_crc32     K1   crc32_of per section payload, src/image.cpp:16-26,
+ *                             used by encode_image :396 and decode_inner :301
+ *   crac_pack_records    K2a  encode_payloads / encode_uvm framing + the
+ *                             read_raw drain, src/image.cpp:53-77,
+ *                             src/ckpt_engine.cpp:38-56, device_core.cpp:442-447
+ *   crac_diff_compact /  K2b  new (incremental drain; the reference has none,
+ *   crac_gather_chunks        SPEC.md:336) — emits the same bytes as a full drain
+ *   crac_scatter_records K3   restart refill via write_raw,
+ *                             src/ckpt_engine.cpp:147-164, device_core.cpp:449-454
+ */
+#ifndef CRAC_GPU_H
+#define CRAC_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* A device-visible byte range (16-byte aligned `ptr` for the hash kernel). */
+typedef struct crac_span {
+  uint64_t ptr;
+  uint64_t len;
+} crac_span_t;
+
+/* One framed record of a section stream (ALLOC_PAYLOADS / UVM_PAGES):
+ * `frame_len` literal bytes at stream offset `out_off`, followed by `len`
+ * payload bytes that live at device-visible address `ptr`.
+ * Refill writes `ext` >= len bytes at `ptr`; bytes past `len` are zeroed
+ * (the allocator's 256-byte padding, ref: device_core.cpp:48,65). */
+typedef struct crac_record {
+  uint64_t out_off;
+  uint64_t ptr;
+  uint64_t len;
+  uint64_t ext;
+  uint32_t frame_len; /* 0..24 */
+  uint32_t reserved;
+  uint8_t frame[24];
+} crac_record_t; /* 64 bytes */
+
+/* Stream tile size used by pack/scatter: the host supplies, per tile of the
+ * window, the index of the first record overlapping it (tile_rec). */
+#define CRAC_TILE_BYTES 65536u
+
+/* Uploads the CRC tables to the current device.  Idempotent. */
+int crac_gpu_init(void);
+
+/* K1: zlib-identical CRC-32 of every `chunk_bytes` piece of every span.
+ * chunk_bytes: multiple of 512.  d_chunk_first[i] = index of span i's first
+ * chunk (exclusive prefix sum of ceil(len/chunk_bytes)), n_spans+1 entries.
+ * d_crc receives total_chunks values. */
+int crac_chunk_crc32(const crac_span_t* d_spans, const uint64_t* d_chunk_first, uint32_t n_spans,
+                     uint32_t chunk_bytes, uint64_t total_chunks, uint32_t* d_crc, void* stream);
+
+/* K2a: writes stream bytes [win_off, win_off + win_len) into d_out (16-byte
+ * aligned; win_off multiple of 16).  Records sorted by out_off; bytes not
+ * covered by any record are written as zero.  d_tile_rec[t] = first record
+ * overlapping stream tile (win_off / CRAC_TILE_BYTES + t). */
+int crac_pack_records(const crac_record_t* d_recs, uint32_t n_recs, const uint32_t* d_tile_rec,
+                      uint64_t win_off, uint64_t win_len, uint8_t* d_out, void* stream);
+
+/* K3: inverse of pack.  d_win holds stream bytes [win_off, win_off+win_len+16)
+ * (16 bytes of look-ahead past the window).  Every destination 16-byte word
+ * whose first stream byte lies in the window is written; the padding words
+ * (len..ext) of a record are zero-filled by the window holding its last
+ * payload byte (or by window 0 for len == 0). */
+int crac_scatter_records(const crac_record_t* d_recs, uint32_t n_recs,
+                         const uint32_t* d_tile_rec, const uint8_t* d_win, uint64_t win_off,
+                         uint64_t win_len, void* stream);
+
+/* K2b: dirty-chunk detection.  d_dirty_idx receives, in ascending order, the
+ * indices c with d_crc_new[c] != d_crc_prev[c]; *d_dirty_count their number.
+ * d_block_counts: scratch of ceil(n_chunks / 4096) uint32.  d_crc_prev is
+ * then overwritten with d_crc_new. */
+int crac_diff_compact(const uint32_t* d_crc_new, uint32_t* d_crc_prev, uint64_t n_chunks,
+                      uint32_t* d_block_counts, uint64_t* d_dirty_idx, uint64_t* d_dirty_count,
+                      void* stream);
+
+/* Copies dirty chunks d_dirty_idx[first .. first+count) (chunk numbering as in
+ * crac_chunk_crc32) to d_staging + k * chunk_bytes, k = 0..count-1. */
+int crac_gather_chunks(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
+                       uint32_t n_spans, uint32_t chunk_bytes, const uint64_t* d_dirty_idx,
+                       uint64_t first, uint64_t count, uint8_t* d_staging, void* stream);
+
+/* Test/bench fixtures: synthetic content and epoch mutation.
+ * Word k of allocation `id`: mix64(k + 0x1000003*id + (seed << 56)), LE. */
+int crac_fill_synth(uint8_t* d_dst, uint64_t len, uint64_t seed, uint64_t id,
+                    uint64_t word_offset, void* stream);
+
+/* Rewrites chunk c of span s iff mix64(seed ^ (epoch << 40) ^ (chunk_first[s]+c)) <
+ * threshold, with synth content of seed' = seed + epoch (ids from d_ids). */
+int crac_mutate_chunks(const crac_span_t* d_spans, const uint64_t* d_ids,
+                       const uint64_t* d_chunk_first, uint32_t n_spans, uint32_t chunk_bytes,
+                       uint64_t total_chunks, uint64_t seed, uint64_t epoch, uint64_t threshold,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CRAC_GPU_H */

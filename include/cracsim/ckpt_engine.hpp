@@ -1,0 +1,132 @@
+// cracsim B200 build — the checkpoint engine.
+//
+// Drop-in surface of the reference engine (ref: include/cracsim/ckpt_engine.hpp:16-84):
+// Session / SessionConfig / checkpoint / checkpoint_to_file / replay_log /
+// restart / restart_from_file, with the same semantics (non-destructive
+// checkpoint, replay verified address-by-address, ReplayDivergence fatal).
+//
+// B200 fast path (the timed hot path):
+//   checkpoint_image   quiesce -> K1 chunk CRCs (HBM) || pack kernel -> staging
+//                      ring -> D2H into a pinned image; host writes the small
+//                      sections and folds chunk CRCs into section CRCs.
+//                      Bytes equal encode_image(checkpoint(session)).
+//   checkpoint_incremental  same bytes; only chunks whose CRC changed since
+//                      the previous image of this session cross PCIe.
+//   restart_image      strict host parse of the framing -> log replay (same
+//                      first-fit, real backing only for allocations live at
+//                      the end) -> H2D ring -> scatter kernel -> K1 over the
+//                      refilled regions verifies the stored CRCs -> managed
+//                      residence restored with cudaMemPrefetchAsync.
+// checkpoint()/restart() on Snapshot values are adapters over these.
+#pragma once
+
+#include <chrono>
+#include <memory>
+
+#include "cracsim/image.hpp"
+
+namespace cracsim {
+
+using KernelCatalog = std::map<std::string, KernelBody, std::less<>>;
+
+struct SessionConfig {
+  uint64_t seed = 0;
+  uint64_t arena_bytes = 1ull << 24;
+  TableMode mode = TableMode::Direct;
+  std::chrono::milliseconds quiesce_timeout{30000};
+};
+
+struct DrainEngine;  // staging ring, device tables, streams (drain.cu)
+
+class Session {
+ public:
+  explicit Session(const SessionConfig& cfg);
+  ~Session();
+  Session(Session&&) noexcept;
+  Session& operator=(Session&&) noexcept;
+
+  RuntimeApi& api() { return *table_; }
+  DispatchTable& table() { return *table_; }
+  DeviceContext& device() { return *ctx_; }
+  CallLog& log() { return *log_; }
+  RegionMap& regions() { return *regions_; }
+  std::vector<uint8_t>& app_state() { return app_state_; }
+  const SessionConfig& config() const { return cfg_; }
+  DrainEngine& drain_engine();
+
+ private:
+  SessionConfig cfg_;
+  std::unique_ptr<DeviceContext> ctx_;
+  std::unique_ptr<CallLog> log_;
+  std::unique_ptr<RegionMap> regions_;
+  std::unique_ptr<DispatchTable> table_;
+  std::vector<uint8_t> app_state_;
+  std::unique_ptr<DrainEngine> drain_;
+};
+
+// Page-locked host buffer holding one image; reused across checkpoints.  The
+// drain places the image so the bulk sections start 4 KiB-aligned.
+class PinnedImage {
+ public:
+  PinnedImage() = default;
+  ~PinnedImage();
+  PinnedImage(const PinnedImage&) = delete;
+  PinnedImage& operator=(const PinnedImage&) = delete;
+  PinnedImage(PinnedImage&& o) noexcept;
+  PinnedImage& operator=(PinnedImage&& o) noexcept;
+
+  const uint8_t* data() const { return base_ + off_; }
+  uint8_t* mutable_data() { return base_ + off_; }
+  uint64_t size() const { return size_; }
+  std::span<const uint8_t> bytes() const { return {data(), size_}; }
+  // Ensures capacity for `size` bytes with (data() + align_at) % 4096 == 0.
+  void prepare(uint64_t size, uint64_t align_at);
+  void set_size(uint64_t n) { size_ = n; }
+
+ private:
+  uint8_t* base_ = nullptr;
+  uint64_t cap_ = 0;
+  uint64_t off_ = 0;
+  uint64_t size_ = 0;
+};
+
+// Device-timed phase breakdown of the last drain / refill (CUDA events on the
+// engine streams; milliseconds).
+struct DrainStats {
+  double total_ms = 0;       // first to last event of the operation
+  double hash_ms = 0;        // K1 span (all launches)
+  double pack_ms = 0;        // pack (drain) or scatter (refill) kernels, summed
+  double copy_ms = 0;        // D2H (drain) or H2D (refill) span
+  uint64_t hash_bytes = 0;   // bytes K1 read
+  uint64_t hash_launches = 0;
+  uint64_t pack_launches = 0;
+  uint64_t pack_bytes = 0;   // stream bytes packed / scattered
+  uint64_t d2h_bytes = 0;
+  uint64_t h2d_bytes = 0;
+  uint64_t image_bytes = 0;
+  uint64_t dirty_chunks = 0;
+  uint64_t total_chunks = 0;
+  bool incremental = false;
+};
+
+// ---- reference surface ----
+Snapshot checkpoint(Session& session);
+void checkpoint_to_file(Session& session, const std::filesystem::path& path, bool compress = false);
+std::map<uint64_t, uint64_t> replay_log(
+    DeviceContext& ctx, std::span<const CallLogEntry> log,
+    const std::map<uint64_t, std::vector<KernelDescriptor>>* binaries = nullptr);
+Session restart(const Snapshot& snapshot, const KernelCatalog& catalog,
+                TableMode mode = TableMode::Direct,
+                std::chrono::milliseconds quiesce_timeout = std::chrono::milliseconds{30000});
+Session restart_from_file(const std::filesystem::path& path, const KernelCatalog& catalog,
+                          TableMode mode = TableMode::Direct);
+
+// ---- B200 fast path ----
+void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats = nullptr);
+void checkpoint_incremental(Session& session, PinnedImage& image, DrainStats* stats = nullptr);
+Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catalog,
+                      TableMode mode = TableMode::Direct,
+                      std::chrono::milliseconds quiesce_timeout = std::chrono::milliseconds{30000},
+                      DrainStats* stats = nullptr);
+
+}  // namespace cracsim

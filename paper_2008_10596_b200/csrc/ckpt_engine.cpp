@@ -1,0 +1,117 @@
+// Session lifecycle, log replay, and the value-type (Snapshot) adapters over
+// the B200 drain/refill (drain.cu).
+#include <fstream>
+
+#include "drain_engine.hpp"
+#include "image_codec.hpp"
+
+namespace cracsim {
+
+Session::Session(const SessionConfig& cfg)
+    : cfg_(cfg),
+      ctx_(std::make_unique<DeviceContext>(cfg.seed, cfg.arena_bytes)),
+      log_(std::make_unique<CallLog>()),
+      regions_(std::make_unique<RegionMap>()),
+      table_(std::make_unique<DispatchTable>(*ctx_, *log_, *regions_, cfg.mode)) {}
+
+Session::~Session() {
+  drain_.reset();  // engine buffers go before the device context
+}
+Session::Session(Session&&) noexcept = default;
+Session& Session::operator=(Session&&) noexcept = default;
+
+DrainEngine& Session::drain_engine() {
+  if (!drain_) drain_ = std::make_unique<DrainEngine>(ctx_->device());
+  return *drain_;
+}
+
+// ref: ckpt_engine.cpp:29-61.  The snapshot is decoded from the image the
+// GPU drain produced, so both APIs share one hot path.
+Snapshot checkpoint(Session& session) {
+  PinnedImage img;
+  checkpoint_image(session, img);
+  std::vector<uint8_t> bytes(img.data(), img.data() + img.size());
+  return decode_image(bytes);
+}
+
+// ref: ckpt_engine.cpp:63-65 (the drain itself is the GPU path; the file is
+// written from the pinned image, compressed on request).
+void checkpoint_to_file(Session& session, const std::filesystem::path& path, bool compress) {
+  PinnedImage img;
+  checkpoint_image(session, img);
+  std::vector<uint8_t> z;
+  std::span<const uint8_t> out = img.bytes();
+  if (compress) {
+    z = compress_image(out);
+    out = z;
+  }
+  std::ofstream f(path, std::ios::binary | std::ios::trunc);
+  f.write(reinterpret_cast<const char*>(out.data()), static_cast<std::streamsize>(out.size()));
+  f.flush();
+  if (!f.good()) raise(Errc::InvalidArgument, "cannot write " + path.string());
+}
+
+// ref: ckpt_engine.cpp:67-118 — re-execute in seq order, verify every result.
+std::map<uint64_t, uint64_t> replay_log(
+    DeviceContext& ctx, std::span<const CallLogEntry> log,
+    const std::map<uint64_t, std::vector<KernelDescriptor>>* binaries) {
+  std::map<uint64_t, uint64_t> placed;
+  auto diverged = [](const CallLogEntry& e, const std::string& what) {
+    raise(Errc::ReplayDivergence, "seq " + std::to_string(e.seq) + ": " + what);
+  };
+  for (const CallLogEntry& e : log) {
+    switch (e.op) {
+      case LogOp::Alloc: {
+        const AllocationRecord rec = ctx.alloc(static_cast<AllocationKind>(e.kind), e.size);
+        if (rec.id != e.id)
+          diverged(e, "id " + std::to_string(rec.id) + " != logged " + std::to_string(e.id));
+        if (rec.address != e.address)
+          diverged(e, "address mismatch for allocation " + std::to_string(e.id));
+        placed.emplace(e.seq, rec.address);
+        break;
+      }
+      case LogOp::Free: ctx.free(e.id); break;
+      case LogOp::StreamCreate:
+        if (ctx.stream_create() != e.id) diverged(e, "stream id mismatch");
+        break;
+      case LogOp::StreamDestroy: ctx.stream_destroy(e.id); break;
+      case LogOp::RegisterBinary: {
+        // binaries unregistered before the checkpoint replay as empty
+        // placeholders so later handles line up (ref: ckpt_engine.cpp:98-110)
+        std::vector<KernelDescriptor> kernels;
+        if (binaries)
+          if (auto it = binaries->find(e.id); it != binaries->end()) kernels = it->second;
+        if (ctx.register_fat_binary(std::move(kernels)) != e.id) diverged(e, "handle mismatch");
+        break;
+      }
+      case LogOp::UnregisterBinary: ctx.unregister_fat_binary(e.id); break;
+    }
+  }
+  return placed;
+}
+
+// ref: ckpt_engine.cpp:120-171, via the GPU refill.
+Session restart(const Snapshot& snapshot, const KernelCatalog& catalog, TableMode mode,
+                std::chrono::milliseconds quiesce_timeout) {
+  for (const BinaryInfo& b : snapshot.binaries)
+    for (const KernelInfo& k : b.kernels)
+      if (!catalog.count(k.name))
+        raise(Errc::UnknownKernelBody, "no body registered for kernel '" + k.name + "'");
+  const std::vector<uint8_t> image = encode_image(snapshot);
+  try {
+    return restart_image(image, catalog, mode, quiesce_timeout);
+  } catch (const Error& e) {
+    // a snapshot that does not frame consistently is a replay mismatch here
+    // (the reference checks payload/record agreement during restart)
+    if (e.code() == Errc::ImageCorrupt) raise(Errc::ReplayDivergence, e.what());
+    throw;
+  }
+}
+
+Session restart_from_file(const std::filesystem::path& path, const KernelCatalog& catalog,
+                          TableMode mode) {
+  const std::vector<uint8_t> bytes = read_file_bytes(path);
+  return restart_image(bytes, catalog, mode);
+}
+
+}  // namespace cracsim

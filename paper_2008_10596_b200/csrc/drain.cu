@@ -1,0 +1,876 @@
+// The B200 hot path: checkpoint drain and restart refill.
+//
+// Drain  (replaces ref: src/ckpt_engine.cpp:29-61 checkpoint + src/image.cpp:383-399
+//         encode_image; the read_raw copies at ckpt_engine.cpp:49,54):
+//   host  : quiesce, small sections (META/LOG/STREAMS/APPSTATE/REGISTRY),
+//           record table of the bulk stream ALLOC_PAYLOADS||crc3||hdr4||UVM_PAGES
+//   GPU   : s_hash  K1 over every payload (64 KiB chunks) and managed page
+//           s_pack  pack kernel builds the exact stream bytes window by window
+//                   into an 8 x 16 MiB staging ring
+//           s_copy  D2H of each window into the pinned image (4 KiB aligned)
+//   host  : folds chunk CRCs with the frame CRCs into the section CRCs while
+//           the D2H drains, then patches crc3/crc4.
+// Refill (replaces ref: src/image.cpp:280-345 decode + src/ckpt_engine.cpp:120-171):
+//   host  : strict parse of the framing, replay of the log (real backing only
+//           for allocations live at the end), record table with destinations
+//   GPU   : s_copy H2D windows (+16 B look-ahead) -> ring; s_pack scatter kernel
+//           writes every destination word (padding zero-filled); K1 over the
+//           refilled regions; managed residence via cudaMemPrefetchAsync
+//   host  : fold + compare against the stored CRCs -> ImageCorrupt on mismatch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <set>
+#include <thread>
+
+#include "crc_math.hpp"
+#include "drain_engine.hpp"
+#include "image_codec.hpp"
+
+namespace cracsim {
+
+// ---------------------------------------------------------------------------
+// buffers
+// ---------------------------------------------------------------------------
+template <typename T>
+void DevArray<T>::ensure(size_t n) {
+  if (n <= cap) return;
+  release();
+  const size_t c = std::max<size_t>(n + n / 2, 64);
+  check_cuda(cudaMalloc(reinterpret_cast<void**>(&ptr), c * sizeof(T)), "cudaMalloc engine array");
+  cap = c;
+}
+template <typename T>
+void DevArray<T>::release() {
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  cap = 0;
+}
+template <typename T>
+void HostArray<T>::ensure(size_t n) {
+  if (n <= cap) return;
+  release();
+  const size_t c = std::max<size_t>(n + n / 2, 64);
+  check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&ptr), c * sizeof(T), cudaHostAllocDefault),
+             "cudaHostAlloc engine array");
+  cap = c;
+}
+template <typename T>
+void HostArray<T>::release() {
+  if (ptr) cudaFreeHost(ptr);
+  ptr = nullptr;
+  cap = 0;
+}
+
+DrainEngine::DrainEngine(int dev) : device(dev) {
+  int lo = 0, hi = 0;
+  check_cuda(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+  check_cuda(cudaStreamCreateWithPriority(&s_pack, cudaStreamNonBlocking, hi), "pack stream");
+  check_cuda(cudaStreamCreateWithPriority(&s_copy, cudaStreamNonBlocking, hi), "copy stream");
+  check_cuda(cudaStreamCreateWithPriority(&s_hash, cudaStreamNonBlocking, lo), "hash stream");
+  for (int i = 0; i < kSlots; ++i) {
+    check_cuda(cudaEventCreateWithFlags(&ev_ready[i], cudaEventDisableTiming), "event");
+    check_cuda(cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming), "event");
+    check_cuda(cudaEventCreate(&ev_p0[i]), "event");
+    check_cuda(cudaEventCreate(&ev_p1[i]), "event");
+  }
+  for (cudaEvent_t* e : {&ev_t0, &ev_t1, &ev_h0, &ev_h1, &ev_c0, &ev_c1})
+    check_cuda(cudaEventCreate(e), "event");
+  check_cuda(cudaMalloc(&d_ring, kSlots * (kWindow + 64)), "staging ring");
+  if (int rc = crac_gpu_init()) check_cuda(cudaError_t(rc), "crac_gpu_init");
+}
+
+DrainEngine::~DrainEngine() {
+  cudaDeviceSynchronize();
+  for (int i = 0; i < kSlots; ++i) {
+    cudaEventDestroy(ev_ready[i]);
+    cudaEventDestroy(ev_free[i]);
+    cudaEventDestroy(ev_p0[i]);
+    cudaEventDestroy(ev_p1[i]);
+  }
+  for (cudaEvent_t e : {ev_t0, ev_t1, ev_h0, ev_h1, ev_c0, ev_c1}) cudaEventDestroy(e);
+  cudaFree(d_ring);
+  d_recs.release();
+  d_tile_rec.release();
+  d_pay_spans.release();
+  d_page_spans.release();
+  d_pay_first.release();
+  d_page_first.release();
+  d_pay_ids.release();
+  d_pay_crc.release();
+  d_page_crc.release();
+  d_prev_crc.release();
+  d_block_counts.release();
+  d_dirty_idx.release();
+  d_dirty_count.release();
+  h_pay_crc.release();
+  h_page_crc.release();
+  h_dirty_idx.release();
+  h_count.release();
+  h_ring.release();
+  cudaStreamDestroy(s_pack);
+  cudaStreamDestroy(s_copy);
+  cudaStreamDestroy(s_hash);
+}
+
+// ---------------------------------------------------------------------------
+// pinned image
+// ---------------------------------------------------------------------------
+PinnedImage::~PinnedImage() {
+  if (base_) cudaFreeHost(base_);
+}
+PinnedImage::PinnedImage(PinnedImage&& o) noexcept
+    : base_(o.base_), cap_(o.cap_), off_(o.off_), size_(o.size_) {
+  o.base_ = nullptr;
+  o.cap_ = o.off_ = o.size_ = 0;
+}
+PinnedImage& PinnedImage::operator=(PinnedImage&& o) noexcept {
+  if (this != &o) {
+    if (base_) cudaFreeHost(base_);
+    base_ = o.base_;
+    cap_ = o.cap_;
+    off_ = o.off_;
+    size_ = o.size_;
+    o.base_ = nullptr;
+    o.cap_ = o.off_ = o.size_ = 0;
+  }
+  return *this;
+}
+
+void PinnedImage::prepare(uint64_t size, uint64_t align_at) {
+  const uint64_t need = size + 4096;
+  if (need > cap_) {
+    if (base_) cudaFreeHost(base_);
+    base_ = nullptr;
+    cap_ = 0;
+    check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&base_), need, cudaHostAllocDefault),
+               "cudaHostAlloc image");
+    cap_ = need;
+  }
+  const uint64_t b = reinterpret_cast<uint64_t>(base_);
+  off_ = (4096 - (b + align_at) % 4096) % 4096;
+  size_ = size;
+}
+
+// ---------------------------------------------------------------------------
+// CRC folding on the host
+// ---------------------------------------------------------------------------
+namespace {
+
+using namespace codec;
+
+const uint32_t* pow2_table() {
+  static const std::vector<uint32_t> t = [] {
+    std::vector<uint32_t> v(64);
+    v[0] = 0x00800000u;
+    for (int k = 1; k < 64; ++k) v[k] = crac::gf_mul(v[k - 1], v[k - 1]);
+    return v;
+  }();
+  return t.data();
+}
+
+// Multiplication by x^(8n) mod P as four byte tables (linear map).
+struct Shift {
+  uint32_t t[4][256];
+  explicit Shift(uint64_t n) {
+    const uint32_t c = crac::x8n(n, pow2_table());
+    for (int k = 0; k < 4; ++k)
+      for (uint32_t b = 0; b < 256; ++b) t[k][b] = crac::gf_mul(c, b << (8 * k));
+  }
+  uint32_t operator()(uint32_t v) const {
+    return t[0][v & 0xFF] ^ t[1][(v >> 8) & 0xFF] ^ t[2][(v >> 16) & 0xFF] ^ t[3][v >> 24];
+  }
+};
+
+const Shift& shift_for(uint64_t n) {
+  static const Shift s16(16), s4k(4096), s64k(65536);
+  return n == 16 ? s16 : n == 4096 ? s4k : s64k;
+}
+
+struct Fold {
+  uint32_t acc = 0;
+  void add(uint32_t crc, uint64_t len) {
+    if (len == 16 || len == 4096 || len == 65536)
+      acc = shift_for(len)(acc) ^ crc;
+    else
+      acc = crac::advance(acc, len, pow2_table()) ^ crc;
+  }
+};
+
+// Runs fn(0..n-1) on up to 8 host threads (image patching).
+template <typename Fn>
+void parallel_for(uint64_t n, Fn&& fn) {
+  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const uint64_t workers = std::min<uint64_t>(hw, (n + 15) / 16);
+  if (workers <= 1) {
+    for (uint64_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (uint64_t t = 0; t < workers; ++t)
+    pool.emplace_back([&, t] {
+      for (uint64_t i = n * t / workers; i < n * (t + 1) / workers; ++i) fn(i);
+    });
+  for (auto& th : pool) th.join();
+}
+
+struct StreamTimer {
+  float ms(cudaEvent_t a, cudaEvent_t b) {
+    float v = 0;
+    cudaEventElapsedTime(&v, a, b);
+    return v;
+  }
+};
+
+// Bulk-stream plan shared by drain and refill.  `dest` = device pointers of
+// the regions (drain: sources; refill: destinations).
+struct BulkItem {
+  uint64_t id = 0;
+  AllocationKind kind = AllocationKind::Device;
+  uint64_t size = 0;
+  uint64_t ptr = 0;
+  const std::vector<uint8_t>* flags = nullptr;  // managed page flags
+};
+
+void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
+  P.recs.clear();
+  P.pay_spans.clear();
+  P.page_spans.clear();
+  P.pay_first.assign(1, 0);
+  P.page_first.assign(1, 0);
+  P.pay_ids.clear();
+  P.pay_rec_off.clear();
+  P.log_sizes.clear();
+  uint64_t pos = 0, len4 = 0;
+  for (const BulkItem& it : items) {
+    P.log_sizes.push_back(it.id);
+    P.log_sizes.push_back(it.size);
+    if (it.kind == AllocationKind::Managed) {
+      len4 += 16 + 16 * page_count_for(it.size) + it.size;
+      continue;
+    }
+    crac_record_t r{};
+    r.out_off = pos;
+    r.ptr = it.ptr;
+    r.len = it.size;
+    r.ext = round_up_align(it.size);
+    r.frame_len = 16;
+    std::memcpy(r.frame, &it.id, 8);
+    std::memcpy(r.frame + 8, &it.size, 8);
+    P.recs.push_back(r);
+    P.pay_spans.push_back(crac_span_t{it.ptr, it.size});
+    P.pay_first.push_back(P.pay_first.back() + (it.size + DrainEngine::kChunk - 1) / DrainEngine::kChunk);
+    P.pay_ids.push_back(it.id);
+    P.pay_rec_off.push_back(pos + 16);
+    pos += 16 + it.size;
+  }
+  P.len3 = pos;
+  P.len4 = len4;
+  {  // crc3 placeholder + the UVM_PAGES section header, as one frame-only record
+    crac_record_t g{};
+    g.out_off = pos;
+    g.frame_len = 20;
+    const uint32_t tag = 4, zero = 0;
+    std::memcpy(g.frame + 4, &tag, 4);
+    std::memcpy(g.frame + 8, &zero, 4);
+    std::memcpy(g.frame + 12, &len4, 8);
+    P.recs.push_back(g);
+    pos += 20;
+  }
+  for (const BulkItem& it : items) {
+    if (it.kind != AllocationKind::Managed) continue;
+    const uint64_t pages = page_count_for(it.size);
+    crac_record_t h{};
+    h.out_off = pos;
+    h.frame_len = 16;
+    std::memcpy(h.frame, &it.id, 8);
+    std::memcpy(h.frame + 8, &pages, 8);
+    P.recs.push_back(h);
+    pos += 16;
+    P.page_spans.push_back(crac_span_t{it.ptr, it.size});
+    P.page_first.push_back(P.page_first.back() + pages);
+    const uint64_t padded = round_up_align(it.size);
+    for (uint64_t p = 0; p < pages; ++p) {
+      const uint64_t off = p * kPageSize;
+      const uint32_t len = uint32_t(std::min<uint64_t>(kPageSize, it.size - off));
+      const uint32_t fl = it.flags ? (*it.flags)[p] : 0;
+      crac_record_t r{};
+      r.out_off = pos;
+      r.ptr = it.ptr + off;
+      r.len = len;
+      r.ext = p + 1 == pages ? padded - off : len;
+      r.frame_len = 16;
+      std::memcpy(r.frame, &p, 8);
+      std::memcpy(r.frame + 8, &fl, 4);
+      std::memcpy(r.frame + 12, &len, 4);
+      P.recs.push_back(r);
+      pos += 16 + len;
+    }
+  }
+  P.stream_len = pos;
+  const uint64_t tiles = (pos + CRAC_TILE_BYTES - 1) / CRAC_TILE_BYTES;
+  P.tile_rec.resize(tiles);
+  uint32_t r = 0;
+  for (uint64_t t = 0; t < tiles; ++t) {
+    const uint64_t start = t * CRAC_TILE_BYTES;
+    while (r + 1 < P.recs.size() && P.recs[r + 1].out_off <= start) ++r;
+    P.tile_rec[t] = r;
+  }
+}
+
+void upload_plan(DrainEngine& E, const ImagePlan& P, cudaStream_t st) {
+  auto up = [&](auto& dev, const auto& host) {
+    if (host.empty()) return;
+    dev.ensure(host.size());
+    check_cuda(cudaMemcpyAsync(dev.ptr, host.data(), host.size() * sizeof(host[0]),
+                               cudaMemcpyHostToDevice, st),
+               "plan upload");
+  };
+  up(E.d_recs, P.recs);
+  up(E.d_tile_rec, P.tile_rec);
+  up(E.d_pay_spans, P.pay_spans);
+  up(E.d_pay_first, P.pay_first);
+  up(E.d_page_spans, P.page_spans);
+  up(E.d_page_first, P.page_first);
+  up(E.d_pay_ids, P.pay_ids);
+}
+
+// K1 over every payload and managed region; CRCs land in h_*_crc.
+void launch_hash(DrainEngine& E, const ImagePlan& P, cudaStream_t st, DrainStats* stats) {
+  const uint64_t n_pay = P.pay_first.back(), n_page = P.page_first.back();
+  E.d_pay_crc.ensure(std::max<uint64_t>(n_pay, 1));
+  E.d_page_crc.ensure(std::max<uint64_t>(n_page, 1));
+  E.h_pay_crc.ensure(std::max<uint64_t>(n_pay, 1));
+  E.h_page_crc.ensure(std::max<uint64_t>(n_page, 1));
+  check_cuda(cudaEventRecord(E.ev_h0, st), "event");
+  if (n_pay)
+    check_cuda(cudaError_t(crac_chunk_crc32(E.d_pay_spans.ptr, E.d_pay_first.ptr,
+                                            uint32_t(P.pay_spans.size()), DrainEngine::kChunk,
+                                            n_pay, E.d_pay_crc.ptr, st)),
+               "K1 payloads");
+  if (n_page)
+    check_cuda(cudaError_t(crac_chunk_crc32(E.d_page_spans.ptr, E.d_page_first.ptr,
+                                            uint32_t(P.page_spans.size()), DrainEngine::kPageChunk,
+                                            n_page, E.d_page_crc.ptr, st)),
+               "K1 pages");
+  check_cuda(cudaEventRecord(E.ev_h1, st), "event");
+  if (n_pay)
+    check_cuda(cudaMemcpyAsync(E.h_pay_crc.ptr, E.d_pay_crc.ptr, n_pay * 4, cudaMemcpyDeviceToHost, st),
+               "crc download");
+  if (n_page)
+    check_cuda(cudaMemcpyAsync(E.h_page_crc.ptr, E.d_page_crc.ptr, n_page * 4,
+                               cudaMemcpyDeviceToHost, st),
+               "crc download");
+  if (stats) {
+    stats->hash_launches += (n_pay ? 1 : 0) + (n_page ? 1 : 0);
+    for (const auto& s : P.pay_spans) stats->hash_bytes += s.len;
+    for (const auto& s : P.page_spans) stats->hash_bytes += s.len;
+  }
+}
+
+// Section CRCs from chunk CRCs + frames.  `frame_at(out_off)` returns the 16
+// frame bytes of the record at that stream offset.
+void fold_sections(const DrainEngine& E, const ImagePlan& P, uint32_t& crc3, uint32_t& crc4) {
+  Fold f3;
+  size_t span = 0;
+  for (const crac_record_t& r : P.recs) {
+    if (r.out_off >= P.len3) break;
+    f3.add(crc32_host(r.frame, 16), 16);
+    const uint64_t c0 = P.pay_first[span], c1 = P.pay_first[span + 1];
+    for (uint64_t c = c0; c < c1; ++c) {
+      const uint64_t len = std::min<uint64_t>(DrainEngine::kChunk, r.len - (c - c0) * DrainEngine::kChunk);
+      f3.add(E.h_pay_crc.ptr[c], len);
+    }
+    ++span;
+  }
+  crc3 = f3.acc;
+  Fold f4;
+  uint64_t page = 0;
+  for (const crac_record_t& r : P.recs) {
+    if (r.out_off < P.len3 + 20) continue;
+    f4.add(crc32_host(r.frame, 16), 16);
+    if (r.len) f4.add(E.h_page_crc.ptr[page++], r.len);
+  }
+  crc4 = f4.acc;
+}
+
+template <typename T>
+void put_at(uint8_t* p, T v) {
+  std::memcpy(p, &v, sizeof(T));
+}
+
+// Writes one complete small section (header, payload, crc) at `p`; returns
+// the byte count.
+uint64_t write_section(uint8_t* p, uint32_t tag, const std::vector<uint8_t>& payload) {
+  put_at<uint32_t>(p, tag);
+  put_at<uint32_t>(p + 4, 0);
+  put_at<uint64_t>(p + 8, payload.size());
+  if (!payload.empty()) std::memcpy(p + 16, payload.data(), payload.size());
+  put_at<uint32_t>(p + 16 + payload.size(), crc32_host(payload.data(), payload.size()));
+  return 20 + payload.size();
+}
+
+struct QuiesceScope {
+  DispatchTable& t;
+  QuiesceScope(DispatchTable& table, std::chrono::milliseconds to) : t(table) { t.quiesce(to); }
+  ~QuiesceScope() { t.resume(); }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// drain
+// ---------------------------------------------------------------------------
+void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
+  QuiesceScope q(session.table(), session.config().quiesce_timeout);
+  DeviceContext& ctx = session.device();
+  DrainEngine& E = session.drain_engine();
+  if (stats) *stats = DrainStats{};
+  check_cuda(cudaEventRecord(E.ev_t0, E.s_pack), "event");
+
+  const SnapshotMeta meta{ctx.seed(), ctx.arena_bytes(), kEngineVersion};
+  const std::vector<CallLogEntry> log = session.log().snapshot();
+  const std::vector<AllocationRecord> active = active_set(log);
+  const std::vector<uint8_t> sec1 = meta_bytes(meta);
+  const std::vector<uint8_t> sec2 = log_bytes(log);
+  const std::vector<uint8_t> sec5 = streams_bytes(ctx.live_stream_ids());
+  const std::vector<uint8_t>& sec6 = session.app_state();
+  const std::vector<uint8_t> sec7 = registry_bytes(ctx.registered_binaries());
+
+  // bulk plan
+  std::vector<BulkItem> items;
+  std::vector<std::vector<uint8_t>> flags;
+  flags.reserve(active.size());
+  for (const AllocationRecord& rec : active) {
+    BulkItem it{rec.id, rec.kind, rec.size, ctx.backing_ptr(rec.id), nullptr};
+    if (rec.kind == AllocationKind::Managed) {
+      const auto pages = ctx.managed_pages(rec.id);
+      std::vector<uint8_t> f(pages.size());
+      for (size_t i = 0; i < pages.size(); ++i)
+        f[i] = uint8_t((pages[i].device_resident ? 1 : 0) | (pages[i].dirty ? 2 : 0));
+      flags.push_back(std::move(f));
+      it.flags = &flags.back();
+    }
+    items.push_back(it);
+  }
+  ImagePlan& P = E.plan;
+  build_plan(items, P);
+  P.log_len = log.size();
+
+  // file layout: header | META | LOG | ALLOC hdr | stream | crc4 | STREAMS | APPSTATE | REGISTRY
+  const uint64_t s3 = 16 + (20 + sec1.size()) + (20 + sec2.size()) + 16;
+  const uint64_t total = s3 + P.stream_len + 4 + (20 + sec5.size()) + (20 + sec6.size()) +
+                         (20 + sec7.size());
+  out.prepare(total, s3);
+  P.s3 = s3;
+  P.image_bytes = total;
+  uint8_t* img = out.mutable_data();
+  std::memcpy(img, kImageMagic, 8);
+  put_at<uint32_t>(img + 8, kImageVersion);
+  put_at<uint32_t>(img + 12, kSectionCount);
+  uint64_t at = 16;
+  at += write_section(img + at, 1, sec1);
+  at += write_section(img + at, 2, sec2);
+  put_at<uint32_t>(img + at, 3);
+  put_at<uint32_t>(img + at + 4, 0);
+  put_at<uint64_t>(img + at + 8, P.len3);
+  at += 16;
+
+  const bool bulk = P.len3 + P.len4 > 0;
+  uint32_t crc3 = 0, crc4 = 0;
+  if (bulk) {
+    upload_plan(E, P, E.s_pack);
+    cudaEvent_t uploaded = E.ev_ready[0];
+    check_cuda(cudaEventRecord(uploaded, E.s_pack), "event");
+    check_cuda(cudaStreamWaitEvent(E.s_hash, uploaded, 0), "wait");
+    launch_hash(E, P, E.s_hash, stats);
+
+    const uint64_t windows = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
+    check_cuda(cudaEventRecord(E.ev_c0, E.s_pack), "event");
+    for (uint64_t w = 0; w < windows; ++w) {
+      const int slot = int(w % DrainEngine::kSlots);
+      uint8_t* buf = E.d_ring + slot * (DrainEngine::kWindow + 64);
+      const uint64_t off = w * DrainEngine::kWindow;
+      const uint64_t len = std::min(DrainEngine::kWindow, P.stream_len - off);
+      if (w >= uint64_t(DrainEngine::kSlots))
+        check_cuda(cudaStreamWaitEvent(E.s_pack, E.ev_free[slot], 0), "wait");
+      if (stats && w < uint64_t(DrainEngine::kSlots)) cudaEventRecord(E.ev_p0[slot], E.s_pack);
+      check_cuda(cudaError_t(crac_pack_records(E.d_recs.ptr, uint32_t(P.recs.size()),
+                                               E.d_tile_rec.ptr + off / CRAC_TILE_BYTES, off, len,
+                                               buf, E.s_pack)),
+                 "pack");
+      if (stats && w < uint64_t(DrainEngine::kSlots)) cudaEventRecord(E.ev_p1[slot], E.s_pack);
+      check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_pack), "event");
+      check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_ready[slot], 0), "wait");
+      check_cuda(cudaMemcpyAsync(img + s3 + off, buf, len, cudaMemcpyDeviceToHost, E.s_copy), "D2H");
+      check_cuda(cudaEventRecord(E.ev_free[slot], E.s_copy), "event");
+    }
+    check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
+    if (stats) {
+      stats->pack_launches = windows;
+      stats->pack_bytes = P.stream_len;
+      stats->d2h_bytes = P.stream_len;
+    }
+    // fold while the D2H is still draining
+    check_cuda(cudaStreamSynchronize(E.s_hash), "hash sync");
+    fold_sections(E, P, crc3, crc4);
+    // seed the incremental table with this image's payload chunk CRCs
+    const uint64_t n_pay = P.pay_first.back();
+    if (n_pay) {
+      E.d_prev_crc.ensure(n_pay);
+      check_cuda(cudaMemcpyAsync(E.d_prev_crc.ptr, E.d_pay_crc.ptr, n_pay * 4,
+                                 cudaMemcpyDeviceToDevice, E.s_hash),
+                 "seed prev crc");
+    }
+    check_cuda(cudaStreamSynchronize(E.s_copy), "copy sync");
+    check_cuda(cudaStreamSynchronize(E.s_pack), "pack sync");
+    check_cuda(cudaStreamSynchronize(E.s_hash), "hash sync");
+  } else {
+    // no bulk bytes: the stream is just crc3 (0) and the UVM_PAGES header
+    put_at<uint32_t>(img + s3, 0);
+    put_at<uint32_t>(img + s3 + 4, 4);
+    put_at<uint32_t>(img + s3 + 8, 0);
+    put_at<uint64_t>(img + s3 + 12, 0);
+  }
+  put_at<uint32_t>(img + s3 + P.len3, crc3);
+  at = s3 + P.stream_len;
+  put_at<uint32_t>(img + at, crc4);
+  at += 4;
+  at += write_section(img + at, 5, sec5);
+  at += write_section(img + at, 6, sec6);
+  at += write_section(img + at, 7, sec7);
+  if (at != total) raise(Errc::DeviceFault, "image layout mismatch");
+  P.valid = true;
+  P.tail_bytes = (20 + sec5.size()) + (20 + sec6.size()) + (20 + sec7.size());
+  E.prev_valid = P.pay_first.back() > 0;
+
+  check_cuda(cudaEventRecord(E.ev_t1, E.s_pack), "event");
+  check_cuda(cudaEventSynchronize(E.ev_t1), "event sync");
+  if (stats) {
+    StreamTimer t;
+    stats->total_ms = t.ms(E.ev_t0, E.ev_t1);
+    if (bulk) {
+      stats->hash_ms = t.ms(E.ev_h0, E.ev_h1);
+      stats->copy_ms = t.ms(E.ev_c0, E.ev_c1);
+      const uint64_t timed = std::min<uint64_t>(stats->pack_launches, DrainEngine::kSlots);
+      double sum = 0;
+      for (uint64_t i = 0; i < timed; ++i) sum += t.ms(E.ev_p0[i], E.ev_p1[i]);
+      stats->pack_ms = timed ? sum / timed * stats->pack_launches : 0;
+    }
+    stats->image_bytes = total;
+    stats->total_chunks = P.pay_first.back() + P.page_first.back();
+    stats->dirty_chunks = stats->total_chunks;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// refill
+// ---------------------------------------------------------------------------
+Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catalog, TableMode mode,
+                      std::chrono::milliseconds quiesce_timeout, DrainStats* stats) {
+  if (stats) *stats = DrainStats{};
+  std::vector<uint8_t> storage;
+  const std::span<const uint8_t> raw = unwrap(image, storage, nullptr);
+  ParsedImage p = parse_image(raw, /*verify_bulk=*/false);
+
+  SessionConfig cfg;
+  cfg.seed = p.meta.seed;
+  cfg.arena_bytes = p.meta.arena_bytes;
+  cfg.mode = mode;
+  cfg.quiesce_timeout = quiesce_timeout;
+  Session session(cfg);
+  DeviceContext& ctx = session.device();
+  DrainEngine& E = session.drain_engine();
+  check_cuda(cudaEventRecord(E.ev_t0, E.s_pack), "event");
+
+  std::map<uint64_t, std::vector<KernelDescriptor>> binaries;
+  for (const BinaryInfo& b : p.binaries) {
+    std::vector<KernelDescriptor> ks;
+    for (const KernelInfo& k : b.kernels) {
+      auto it = catalog.find(k.name);
+      if (it == catalog.end())
+        raise(Errc::UnknownKernelBody, "no body registered for kernel '" + k.name + "'");
+      ks.push_back(KernelDescriptor{k.name, k.buffer_arity, k.scalar_arity, it->second});
+    }
+    binaries.emplace(b.handle, std::move(ks));
+  }
+
+  std::set<uint64_t> live;
+  for (const AllocationRecord& r : p.facts.active) live.insert(r.id);
+  ctx.begin_replay(std::move(live));
+  try {
+    replay_log(ctx, p.log, &binaries);
+  } catch (...) {
+    ctx.end_replay();
+    throw;
+  }
+  ctx.end_replay();
+  if (ctx.live_stream_ids() != p.streams)
+    raise(Errc::ReplayDivergence, "live streams after replay do not match the snapshot");
+
+  // destinations of every framed record, in image order
+  std::vector<BulkItem> items;
+  size_t pi = 0, mi = 0;
+  for (const AllocationRecord& rec : p.facts.active) {
+    const auto replayed = ctx.find_record(rec.id);
+    if (!replayed || replayed->size != rec.size || replayed->kind != rec.kind)
+      raise(Errc::ReplayDivergence,
+            "record " + std::to_string(rec.id) + " does not match a replayed allocation");
+    BulkItem it{rec.id, rec.kind, rec.size, ctx.backing_ptr(rec.id), nullptr};
+    if (rec.kind == AllocationKind::Managed) it.flags = &p.managed[mi++].flags;
+    else ++pi;
+    items.push_back(it);
+  }
+  ImagePlan& P = E.plan;
+  build_plan(items, P);
+  P.log_len = p.log.size();
+  const uint64_t s3 = p.sec[2].payload_off;
+  if (P.len3 != p.sec[2].length || P.len4 != p.sec[3].length ||
+      s3 + P.stream_len != p.sec[3].payload_off + p.sec[3].length)
+    raise(Errc::ImageCorrupt, "bulk sections do not match the log's active set");
+
+  if (P.stream_len > 20) {
+    upload_plan(E, P, E.s_pack);
+    check_cuda(cudaEventRecord(E.ev_ready[0], E.s_pack), "event");
+    check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_ready[0], 0), "wait");
+    const uint64_t windows = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
+    check_cuda(cudaEventRecord(E.ev_c0, E.s_copy), "event");
+    for (uint64_t w = 0; w < windows; ++w) {
+      const int slot = int(w % DrainEngine::kSlots);
+      uint8_t* buf = E.d_ring + slot * (DrainEngine::kWindow + 64);
+      const uint64_t off = w * DrainEngine::kWindow;
+      const uint64_t len = std::min(DrainEngine::kWindow, P.stream_len - off);
+      const uint64_t with_ahead = std::min(len + 16, P.stream_len - off);
+      if (w >= uint64_t(DrainEngine::kSlots))
+        check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_free[slot], 0), "wait");
+      check_cuda(cudaMemcpyAsync(buf, raw.data() + s3 + off, with_ahead, cudaMemcpyHostToDevice,
+                                 E.s_copy),
+                 "H2D");
+      check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_copy), "event");
+      check_cuda(cudaStreamWaitEvent(E.s_pack, E.ev_ready[slot], 0), "wait");
+      if (stats && w < uint64_t(DrainEngine::kSlots)) cudaEventRecord(E.ev_p0[slot], E.s_pack);
+      check_cuda(cudaError_t(crac_scatter_records(E.d_recs.ptr, uint32_t(P.recs.size()),
+                                                  E.d_tile_rec.ptr + off / CRAC_TILE_BYTES, buf,
+                                                  off, len, E.s_pack)),
+                 "scatter");
+      if (stats && w < uint64_t(DrainEngine::kSlots)) cudaEventRecord(E.ev_p1[slot], E.s_pack);
+      check_cuda(cudaEventRecord(E.ev_free[slot], E.s_pack), "event");
+    }
+    check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
+    if (stats) {
+      stats->pack_launches = windows;
+      stats->pack_bytes = P.stream_len;
+      stats->h2d_bytes = P.stream_len;
+    }
+    // verify: K1 over the refilled regions, folded with the image's frames
+    launch_hash(E, P, E.s_pack, stats);
+    check_cuda(cudaStreamSynchronize(E.s_pack), "refill sync");
+    uint32_t crc3 = 0, crc4 = 0;
+    fold_sections(E, P, crc3, crc4);
+    if (crc3 != p.sec[2].crc) raise(Errc::ImageCorrupt, "crc mismatch in ALLOC_PAYLOADS");
+    if (crc4 != p.sec[3].crc) raise(Errc::ImageCorrupt, "crc mismatch in UVM_PAGES");
+    const uint64_t n_pay = P.pay_first.back();
+    if (n_pay) {
+      E.d_prev_crc.ensure(n_pay);
+      check_cuda(cudaMemcpyAsync(E.d_prev_crc.ptr, E.d_pay_crc.ptr, n_pay * 4,
+                                 cudaMemcpyDeviceToDevice, E.s_pack),
+                 "seed prev crc");
+    }
+  } else if (p.sec[2].crc != 0 || p.sec[3].crc != 0) {
+    raise(Errc::ImageCorrupt, "crc mismatch in empty bulk section");
+  }
+  // managed residence and flags
+  mi = 0;
+  for (const AllocationRecord& rec : p.facts.active)
+    if (rec.kind == AllocationKind::Managed) ctx.restore_managed(rec.id, p.managed[mi++].flags, E.s_pack);
+  check_cuda(cudaEventRecord(E.ev_t1, E.s_pack), "event");
+  check_cuda(cudaEventSynchronize(E.ev_t1), "event sync");
+  E.prev_valid = false;  // no pinned image of this session exists yet
+  P.valid = false;
+
+  session.log().reset(std::move(p.log));
+  session.app_state() = std::move(p.app_state);
+  if (stats) {
+    StreamTimer t;
+    stats->total_ms = t.ms(E.ev_t0, E.ev_t1);
+    if (P.stream_len > 20) {
+      stats->hash_ms = t.ms(E.ev_h0, E.ev_h1);
+      stats->copy_ms = t.ms(E.ev_c0, E.ev_c1);
+      const uint64_t timed = std::min<uint64_t>(stats->pack_launches, DrainEngine::kSlots);
+      double sum = 0;
+      for (uint64_t i = 0; i < timed; ++i) sum += t.ms(E.ev_p0[i], E.ev_p1[i]);
+      stats->pack_ms = timed ? sum / timed * stats->pack_launches : 0;
+    }
+    stats->image_bytes = raw.size();
+    stats->total_chunks = P.pay_first.back() + P.page_first.back();
+  }
+  return session;
+}
+
+// ---------------------------------------------------------------------------
+// incremental drain
+// ---------------------------------------------------------------------------
+namespace {
+
+// Incremental drain body; runs with the dispatch gate held.
+void incremental_locked(Session& session, PinnedImage& image, DrainStats* stats) {
+  DrainEngine& E = session.drain_engine();
+  const ImagePlan& P = E.plan;
+  DeviceContext& ctx = session.device();
+  if (stats) {
+    *stats = DrainStats{};
+    stats->incremental = true;
+  }
+  check_cuda(cudaEventRecord(E.ev_t0, E.s_pack), "event");
+  uint8_t* img = image.mutable_data();
+  const uint64_t s3 = P.s3;
+
+  // 1. hash everything (K1), 2. diff against the previous image (K2b)
+  launch_hash(E, P, E.s_pack, stats);
+  const uint64_t n = P.pay_first.back();
+  E.d_block_counts.ensure((n + 4095) / 4096 + 1);
+  E.d_dirty_idx.ensure(std::max<uint64_t>(n, 1));
+  E.d_dirty_count.ensure(1);
+  E.h_count.ensure(1);
+  check_cuda(cudaError_t(crac_diff_compact(E.d_pay_crc.ptr, E.d_prev_crc.ptr, n,
+                                           E.d_block_counts.ptr, E.d_dirty_idx.ptr,
+                                           E.d_dirty_count.ptr, E.s_pack)),
+             "diff");
+  check_cuda(cudaMemcpyAsync(E.h_count.ptr, E.d_dirty_count.ptr, 8, cudaMemcpyDeviceToHost, E.s_pack),
+             "count");
+  check_cuda(cudaStreamSynchronize(E.s_pack), "diff sync");
+  const uint64_t dirty = E.h_count.ptr[0];
+  E.h_dirty_idx.ensure(std::max<uint64_t>(dirty, 1));
+  if (dirty)
+    check_cuda(cudaMemcpyAsync(E.h_dirty_idx.ptr, E.d_dirty_idx.ptr, dirty * 8,
+                               cudaMemcpyDeviceToHost, E.s_hash),
+               "dirty idx");
+
+  // 3. gather dirty chunks into the device ring, D2H each window as one
+  //    contiguous copy into a pinned host ring, patch the image from there
+  const uint64_t per_win = DrainEngine::kWindow / DrainEngine::kChunk;
+  const uint64_t windows = (dirty + per_win - 1) / per_win;
+  E.h_ring.ensure(DrainEngine::kSlots * DrainEngine::kWindow);
+  if (windows) check_cuda(cudaStreamSynchronize(E.s_hash), "dirty idx sync");
+  check_cuda(cudaEventRecord(E.ev_c0, E.s_pack), "event");
+  auto patch = [&](uint64_t w) {  // host side of window w (its D2H has completed)
+    const int slot = int(w % DrainEngine::kSlots);
+    const uint8_t* hbuf = E.h_ring.ptr + slot * DrainEngine::kWindow;
+    const uint64_t first = w * per_win, count = std::min(per_win, dirty - first);
+    parallel_for(count, [&](uint64_t k) {
+      const uint64_t c = E.h_dirty_idx.ptr[first + k];
+      const size_t s = size_t(std::upper_bound(P.pay_first.begin(), P.pay_first.end(), c) -
+                              P.pay_first.begin() - 1);
+      const uint64_t off = (c - P.pay_first[s]) * DrainEngine::kChunk;
+      const uint64_t len = std::min<uint64_t>(DrainEngine::kChunk, P.pay_spans[s].len - off);
+      std::memcpy(img + s3 + P.pay_rec_off[s] + off, hbuf + k * DrainEngine::kChunk, len);
+    });
+  };
+  for (uint64_t w = 0; w < windows; ++w) {
+    const int slot = int(w % DrainEngine::kSlots);
+    uint8_t* buf = E.d_ring + slot * (DrainEngine::kWindow + 64);
+    const uint64_t first = w * per_win, count = std::min(per_win, dirty - first);
+    if (w >= uint64_t(DrainEngine::kSlots)) {
+      // slot reuse: its previous window must be copied out and patched
+      check_cuda(cudaEventSynchronize(E.ev_free[slot]), "slot sync");
+      patch(w - DrainEngine::kSlots);
+    }
+    check_cuda(cudaError_t(crac_gather_chunks(E.d_pay_spans.ptr, E.d_pay_first.ptr,
+                                              uint32_t(P.pay_spans.size()), DrainEngine::kChunk,
+                                              E.d_dirty_idx.ptr, first, count, buf, E.s_pack)),
+               "gather");
+    check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_pack), "event");
+    check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_ready[slot], 0), "wait");
+    check_cuda(cudaMemcpyAsync(E.h_ring.ptr + slot * DrainEngine::kWindow, buf,
+                               count * DrainEngine::kChunk, cudaMemcpyDeviceToHost, E.s_copy),
+               "D2H dirty");
+    check_cuda(cudaEventRecord(E.ev_free[slot], E.s_copy), "event");
+    if (stats) {
+      stats->d2h_bytes += count * DrainEngine::kChunk;
+      stats->pack_launches += 1;
+      stats->pack_bytes += count * DrainEngine::kChunk;
+    }
+  }
+  check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
+  for (uint64_t w = windows > uint64_t(DrainEngine::kSlots) ? windows - DrainEngine::kSlots : 0;
+       w < windows; ++w) {
+    check_cuda(cudaEventSynchronize(E.ev_free[w % DrainEngine::kSlots]), "slot sync");
+    patch(w);
+  }
+  // managed pages are never part of an incremental plan (checked above)
+  uint32_t crc3 = 0, crc4 = 0;
+  fold_sections(E, P, crc3, crc4);
+  put_at<uint32_t>(img + s3 + P.len3, crc3);
+  put_at<uint32_t>(img + s3 + P.stream_len, crc4);
+
+  // small sections can change without a layout change (app_state content,
+  // registry is tied to the log): rewrite the tail sections
+  const std::vector<uint8_t> sec5 = streams_bytes(ctx.live_stream_ids());
+  const std::vector<uint8_t>& sec6 = session.app_state();
+  const std::vector<uint8_t> sec7 = registry_bytes(ctx.registered_binaries());
+  uint64_t at = s3 + P.stream_len + 4;
+  at += write_section(img + at, 5, sec5);
+  at += write_section(img + at, 6, sec6);
+  at += write_section(img + at, 7, sec7);
+
+  check_cuda(cudaEventRecord(E.ev_t1, E.s_pack), "event");
+  check_cuda(cudaEventSynchronize(E.ev_t1), "event sync");
+  if (stats) {
+    StreamTimer t;
+    stats->total_ms = t.ms(E.ev_t0, E.ev_t1);
+    stats->hash_ms = t.ms(E.ev_h0, E.ev_h1);
+    stats->copy_ms = windows ? t.ms(E.ev_c0, E.ev_c1) : 0;
+    stats->image_bytes = P.image_bytes;
+    stats->dirty_chunks = dirty;
+    stats->total_chunks = n;
+  }
+}
+
+}  // namespace
+
+namespace {
+
+uint64_t tail_bytes(Session& session) {
+  DeviceContext& ctx = session.device();
+  return (20 + 8 * ctx.live_stream_ids().size()) + (20 + session.app_state().size()) +
+         (20 + registry_bytes(ctx.registered_binaries()).size());
+}
+
+}  // namespace
+
+void checkpoint_incremental(Session& session, PinnedImage& image, DrainStats* stats) {
+  // Emits exactly the bytes of a full drain.  Only valid while the layout of
+  // the previous image of this session is unchanged (same log, same bulk
+  // records, no managed allocations, same tail size) and `image` still holds
+  // those bytes; otherwise this is a full drain.
+  DrainEngine& E = session.drain_engine();
+  const ImagePlan& P = E.plan;
+  auto layout_unchanged = [&] {
+    if (!P.valid || !E.prev_valid || image.size() != P.image_bytes ||
+        session.log().size() != P.log_len || tail_bytes(session) != P.tail_bytes)
+      return false;
+    std::vector<uint64_t> sig;
+    for (const auto& r : active_set(session.log().snapshot())) {
+      if (r.kind == AllocationKind::Managed) return false;
+      sig.push_back(r.id);
+      sig.push_back(r.size);
+    }
+    return sig == P.log_sizes;
+  };
+  if (!layout_unchanged()) {
+    checkpoint_image(session, image, stats);
+    return;
+  }
+  bool raced = false;
+  {
+    QuiesceScope q(session.table(), session.config().quiesce_timeout);
+    // re-check under the gate: the log cannot move now
+    raced = !layout_unchanged();
+    if (!raced) incremental_locked(session, image, stats);
+  }
+  if (raced) checkpoint_image(session, image, stats);
+}
+
+}  // namespace cracsim

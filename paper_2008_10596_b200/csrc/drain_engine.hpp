@@ -1,0 +1,91 @@
+// Per-session state of the B200 drain/refill pipeline (internal).
+//
+// HBM layout owned here (allocated once, grown geometrically, reused by every
+// checkpoint so no timed step allocates):
+//   ring      kSlots x (window + 64) bytes  staging for the section stream
+//   recs      crac_record_t per framed record of ALLOC_PAYLOADS + UVM_PAGES
+//   tile_rec  u32 per 64 KiB stream tile: first record overlapping it
+//   spans/first/crc  K1 inputs/outputs: payload spans (64 KiB chunks) and
+//             managed spans (4 KiB chunks = one CRC per page)
+//   prev_crc / dirty_idx / block_counts   incremental state (K2b)
+#pragma once
+
+#include <cuda_runtime_api.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "crac_gpu.h"
+#include "cracsim/ckpt_engine.hpp"
+
+namespace cracsim {
+
+template <typename T>
+struct DevArray {
+  T* ptr = nullptr;
+  size_t cap = 0;  // elements
+  void ensure(size_t n);
+  void release();
+};
+
+template <typename T>
+struct HostArray {  // pinned
+  T* ptr = nullptr;
+  size_t cap = 0;
+  void ensure(size_t n);
+  void release();
+};
+
+// Layout of the last image this session drained (enables incremental drains).
+struct ImagePlan {
+  uint64_t image_bytes = 0;
+  uint64_t s3 = 0;          // file offset of the ALLOC_PAYLOADS payload (= stream start)
+  uint64_t len3 = 0, len4 = 0;
+  uint64_t stream_len = 0;  // len3 + 20 + len4
+  std::vector<crac_record_t> recs;
+  std::vector<uint32_t> tile_rec;
+  std::vector<crac_span_t> pay_spans, page_spans;
+  std::vector<uint64_t> pay_first, page_first;
+  std::vector<uint64_t> pay_ids;      // allocation id per payload span
+  std::vector<uint64_t> pay_rec_off;  // stream offset of each payload's first byte
+  std::vector<uint64_t> log_sizes;    // signature: (id, size) of every bulk record
+  uint64_t log_len = 0;
+  uint64_t tail_bytes = 0;  // STREAMS + APPSTATE + KERNEL_REGISTRY, framed
+  bool valid = false;
+};
+
+struct DrainEngine {
+  static constexpr int kSlots = 8;
+  static constexpr uint64_t kWindow = 16ull << 20;  // multiple of CRAC_TILE_BYTES
+  static constexpr uint32_t kChunk = 65536;         // payload hash chunk
+  static constexpr uint32_t kPageChunk = 4096;      // managed hash chunk (= page)
+
+  int device = 0;
+  cudaStream_t s_pack = nullptr, s_copy = nullptr, s_hash = nullptr;
+  cudaEvent_t ev_ready[kSlots] = {}, ev_free[kSlots] = {};
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr, ev_h0 = nullptr, ev_h1 = nullptr;
+  cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr;
+  cudaEvent_t ev_p0[kSlots] = {}, ev_p1[kSlots] = {};
+  uint8_t* d_ring = nullptr;
+
+  DevArray<crac_record_t> d_recs;
+  DevArray<uint32_t> d_tile_rec;
+  DevArray<crac_span_t> d_pay_spans, d_page_spans;
+  DevArray<uint64_t> d_pay_first, d_page_first, d_pay_ids;
+  DevArray<uint32_t> d_pay_crc, d_page_crc, d_prev_crc, d_block_counts;
+  DevArray<uint64_t> d_dirty_idx, d_dirty_count;
+  HostArray<uint32_t> h_pay_crc, h_page_crc;
+  HostArray<uint64_t> h_dirty_idx;
+  HostArray<uint64_t> h_count;
+  HostArray<uint8_t> h_ring;  // kSlots x kWindow pinned landing zone (incremental)
+
+  ImagePlan plan;
+  bool prev_valid = false;  // d_prev_crc holds the chunk CRCs of `plan`'s image
+
+  explicit DrainEngine(int dev);
+  ~DrainEngine();
+  DrainEngine(const DrainEngine&) = delete;
+  DrainEngine& operator=(const DrainEngine&) = delete;
+};
+
+}  // namespace cracsim

@@ -1,0 +1,673 @@
+// sm_100a kernels of the checkpoint drain / restart refill.  C-ABI: crac_gpu.h.
+//
+// K1  k1_chunk_crc      zlib-identical CRC-32 per region-relative chunk
+// K2a k_pack_records    framed section stream (ALLOC_PAYLOADS / UVM_PAGES) -> staging
+// K3  k_scatter_records staging -> regions (restart refill)
+// K2b k_diff_count / k_diff_write / k_gather   incremental dirty-chunk drain
+//     k_fill_synth / k_mutate                  synthetic workload fixtures
+//
+// K1 design (HBM-bound target):
+//   * one warp per chunk, rows of 512 B: lane i owns 16-byte word i of every
+//     row, so every LDG.128 is fully coalesced (4 sectors per 512 B);
+//   * each lane runs the CRC register over its column with slicing-by-4
+//     lookups.  The 496-byte gap to its next word is folded into the tables
+//     used for the 4th step of each word (group B = A^496 o group A), so the
+//     whole chunk costs exactly one table lookup per byte;
+//   * lane columns are combined with x^(128*(31-i)) mod P and a shuffle-XOR
+//     reduction; the affine part K(n) finishes the zlib value;
+//   * tables live in shared memory half-replicated (16 copies) and the two
+//     half-warps always read different tables of a 256-byte row, so every
+//     LDS is bank-conflict-free by construction; the PRMT instruction forms
+//     each lookup address (byte << 8 | table/replica offset) in one ALU op.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+#include <vector>
+
+#include "crac_gpu.h"
+#include "crc_math.hpp"
+
+namespace {
+
+constexpr int kK1Threads = 512;
+constexpr int kK1Warps = kK1Threads / 32;
+constexpr uint32_t kTabWords = 2 * 256 * 64;  // 2 groups x 256 rows x 64 words = 128 KiB
+constexpr uint32_t kTabBytes = kTabWords * 4;
+constexpr uint32_t kGroupB = 256 * 64 * 4;    // byte offset of group B
+constexpr uint32_t kRowGap = 496;             // bytes between a lane's words
+
+__device__ uint32_t g_tab[kTabWords];  // smem image of the lookup tables
+__device__ uint32_t g_t0[256];         // plain byte table
+__device__ uint32_t g_xp16[33];        // x^(128 k) mod P, k = 0..32
+__device__ uint32_t g_xpt[512];        // x^(8 t) mod P, t = 0..511
+__device__ uint32_t g_pow2[64];        // x^(8 * 2^k) mod P
+
+// ---------------------------------------------------------------------------
+// host: table construction
+// ---------------------------------------------------------------------------
+struct HostTables {
+  std::vector<uint32_t> tab, t0, xp16, xpt, pow2;
+};
+
+HostTables build_tables() {
+  HostTables h;
+  h.t0.resize(256);
+  for (uint32_t b = 0; b < 256; ++b) {
+    uint32_t c = b;
+    for (int k = 0; k < 8; ++k) c = (c & 1) ? (c >> 1) ^ crac::kCrcPoly : c >> 1;
+    h.t0[b] = c;
+  }
+  h.pow2.resize(64);
+  h.pow2[0] = 0x00800000u;  // x^8
+  for (int k = 1; k < 64; ++k) h.pow2[k] = crac::gf_mul(h.pow2[k - 1], h.pow2[k - 1]);
+  // position tables: byte p of a 4-byte step is followed by (3 - p) bytes
+  uint32_t pos[4][256];
+  for (int p = 0; p < 4; ++p)
+    for (uint32_t b = 0; b < 256; ++b) pos[p][b] = crac::advance(h.t0[b], 3 - p, h.pow2.data());
+  const uint32_t gap = crac::x8n(kRowGap, h.pow2.data());
+  h.tab.assign(kTabWords, 0);
+  for (int g = 0; g < 2; ++g)
+    for (uint32_t b = 0; b < 256; ++b)
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t v = g == 0 ? pos[t][b] : crac::gf_mul(gap, pos[t][b]);
+        for (int r = 0; r < 16; ++r) h.tab[g * 256 * 64 + b * 64 + t * 16 + r] = v;
+      }
+  h.xp16.resize(33);
+  for (int k = 0; k <= 32; ++k) h.xp16[k] = crac::x8n(16ull * k, h.pow2.data());
+  h.xpt.resize(512);
+  for (int t = 0; t < 512; ++t) h.xpt[t] = crac::x8n(t, h.pow2.data());
+  return h;
+}
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// Per-lane lookup addressing: lookup j of a step reads table t_j = (j + half)
+// & 3 (the table of byte position t_j) at replica (lane & 15).
+struct LaneLut {
+  uint32_t base;    // shared address of the table image
+  uint32_t lr[4];   // byte 0: t_j << 6 | replica << 2; bytes 1..3 zero
+  uint32_t sel[4];  // PRMT selector: (x.byte t_j << 8) | lr.byte0
+};
+
+__device__ __forceinline__ LaneLut make_lut(uint32_t smem_base, uint32_t lane) {
+  LaneLut l;
+  l.base = smem_base;
+  const uint32_t half = lane >> 4, rep = lane & 15;
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t t = (j + half) & 3;
+    l.lr[j] = (t << 6) | (rep << 2);
+    l.sel[j] = 4u | (t << 4) | (5u << 8) | (5u << 12);
+  }
+  return l;
+}
+
+// One slicing-by-4 step: returns sum_p table_p[x.byte p] of table group g.
+template <uint32_t kGroup>
+__device__ __forceinline__ uint32_t step4(const LaneLut& l, uint32_t x) {
+  const uint32_t a0 = lds32(l.base + kGroup + prmt(x, l.lr[0], l.sel[0]));
+  const uint32_t a1 = lds32(l.base + kGroup + prmt(x, l.lr[1], l.sel[1]));
+  const uint32_t a2 = lds32(l.base + kGroup + prmt(x, l.lr[2], l.sel[2]));
+  const uint32_t a3 = lds32(l.base + kGroup + prmt(x, l.lr[3], l.sel[3]));
+  return (a0 ^ a1) ^ (a2 ^ a3);
+}
+
+// Runs the CRC register over one 16-byte word; the final step uses group B
+// (which also advances past the 496-byte gap) unless this is the last row.
+template <bool kGap>
+__device__ __forceinline__ uint32_t word16(const LaneLut& l, uint32_t s, uint4 w) {
+  s = step4<0>(l, s ^ w.x);
+  s = step4<0>(l, s ^ w.y);
+  s = step4<0>(l, s ^ w.z);
+  return step4<kGap ? kGroupB : 0>(l, s ^ w.w);
+}
+
+__device__ __forceinline__ uint32_t warp_xor(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v ^= __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ uint32_t find_span(const uint64_t* chunk_first, uint32_t n_spans,
+                                              uint64_t c) {
+  uint32_t lo = 0, hi = n_spans;  // invariant: chunk_first[lo] <= c < chunk_first[hi]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(chunk_first + mid) <= c) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------------------
+// K1
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kK1Threads, 1)
+    k1_chunk_crc(const crac_span_t* __restrict__ spans, const uint64_t* __restrict__ chunk_first,
+                 uint32_t n_spans, uint32_t chunk_bytes, uint64_t total_chunks,
+                 uint32_t* __restrict__ out, uint32_t k_full) {
+  extern __shared__ __align__(16) uint32_t s_tab[];
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(g_tab);
+    uint4* dst = reinterpret_cast<uint4*>(s_tab);
+    for (uint32_t i = threadIdx.x; i < kTabWords / 4; i += kK1Threads) dst[i] = src[i];
+  }
+  __syncthreads();
+
+  const uint32_t lane = threadIdx.x & 31;
+  const LaneLut lut = make_lut(static_cast<uint32_t>(__cvta_generic_to_shared(s_tab)), lane);
+  const uint64_t gw = blockIdx.x * uint64_t(kK1Warps) + (threadIdx.x >> 5);
+  const uint64_t tw = gridDim.x * uint64_t(kK1Warps);
+  const uint64_t c_begin = total_chunks * gw / tw, c_end = total_chunks * (gw + 1) / tw;
+  if (c_begin >= c_end) return;
+
+  uint32_t s = find_span(chunk_first, n_spans, c_begin);
+  uint64_t s_next = __ldg(chunk_first + s + 1);
+  for (uint64_t c = c_begin; c < c_end; ++c) {
+    while (c >= s_next) {
+      ++s;
+      s_next = __ldg(chunk_first + s + 1);
+    }
+    const crac_span_t sp = spans[s];
+    const uint64_t off = (c - __ldg(chunk_first + s)) * chunk_bytes;
+    const uint64_t rem_len = sp.len - off;
+    const uint32_t len = rem_len < chunk_bytes ? uint32_t(rem_len) : chunk_bytes;
+    const uint8_t* base = reinterpret_cast<const uint8_t*>(sp.ptr + off);
+    const uint32_t rows = len >> 9;
+
+    // ---- main body: rows of 512 B, 4-row double-buffered loads ----
+    uint32_t acc = 0;
+    const uint8_t* p = base + lane * 16;
+    uint32_t r = 0;
+    if (rows >= 4) {
+      uint4 cur0 = ldg_stream(p), cur1 = ldg_stream(p + 512), cur2 = ldg_stream(p + 1024),
+            cur3 = ldg_stream(p + 1536);
+      for (; r + 8 <= rows; r += 4) {
+        const uint8_t* q = p + (r + 4) * 512;
+        const uint4 n0 = ldg_stream(q), n1 = ldg_stream(q + 512), n2 = ldg_stream(q + 1024),
+                    n3 = ldg_stream(q + 1536);
+        acc = word16<true>(lut, acc, cur0);
+        acc = word16<true>(lut, acc, cur1);
+        acc = word16<true>(lut, acc, cur2);
+        acc = word16<true>(lut, acc, cur3);
+        cur0 = n0; cur1 = n1; cur2 = n2; cur3 = n3;
+      }
+      acc = word16<true>(lut, acc, cur0);
+      acc = word16<true>(lut, acc, cur1);
+      acc = word16<true>(lut, acc, cur2);
+      if (r + 4 == rows) {
+        acc = word16<false>(lut, acc, cur3);
+      } else {
+        acc = word16<true>(lut, acc, cur3);
+      }
+      r += 4;
+    }
+    for (; r < rows; ++r) {
+      const uint4 w = ldg_stream(p + r * 512);
+      acc = (r + 1 == rows) ? word16<false>(lut, acc, w) : word16<true>(lut, acc, w);
+    }
+    uint32_t L = rows ? warp_xor(crac::gf_mul(g_xp16[31 - lane], acc)) : 0u;
+
+    // ---- tail (< 512 B): whole words per lane, then bytes on lane 0 ----
+    const uint32_t t = len & 511;
+    if (t) {
+      const uint32_t nt = t >> 4;
+      uint32_t part = 0;
+      if (lane < nt) {
+        const uint4 w = *reinterpret_cast<const uint4*>(base + rows * 512 + lane * 16);
+        part = crac::gf_mul(g_xp16[nt - 1 - lane], word16<false>(lut, 0u, w));
+      }
+      uint32_t lt = warp_xor(part);
+      if (lane == 0) {
+        const uint8_t* tb = base + rows * 512 + nt * 16;
+        for (uint32_t i = 0; i < (t & 15); ++i) lt = (lt >> 8) ^ g_t0[(lt ^ tb[i]) & 0xFFu];
+        L = crac::gf_mul(g_xpt[t], L) ^ lt;
+      }
+    }
+    if (lane == 0) out[c] = L ^ (len == chunk_bytes ? k_full : crac::crc_affine(len, g_pow2));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// byte-shift helper: the 16 bytes starting at byte d (0..15) of (a || b)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 shift16(uint4 a, uint4 b, uint32_t d) {
+  uint32_t x0, x1, x2, x3, x4;
+  switch (d >> 2) {
+    case 0: x0 = a.x; x1 = a.y; x2 = a.z; x3 = a.w; x4 = b.x; break;
+    case 1: x0 = a.y; x1 = a.z; x2 = a.w; x3 = b.x; x4 = b.y; break;
+    case 2: x0 = a.z; x1 = a.w; x2 = b.x; x3 = b.y; x4 = b.z; break;
+    default: x0 = a.w; x1 = b.x; x2 = b.y; x3 = b.z; x4 = b.w; break;
+  }
+  const uint32_t sh = (d & 3) * 8;
+  uint4 r;
+  r.x = __funnelshift_r(x0, x1, sh);
+  r.y = __funnelshift_r(x1, x2, sh);
+  r.z = __funnelshift_r(x2, x3, sh);
+  r.w = __funnelshift_r(x3, x4, sh);
+  return r;
+}
+
+__device__ __forceinline__ uint4 load_shifted(const uint8_t* p) {
+  const uint64_t a = reinterpret_cast<uint64_t>(p);
+  const uint4* q = reinterpret_cast<const uint4*>(a & ~uint64_t(15));
+  const uint32_t d = uint32_t(a & 15);
+  const uint4 lo = q[0];
+  if (d == 0) return lo;
+  return shift16(lo, q[1], d);
+}
+
+__device__ __forceinline__ void set_byte(uint4& v, uint32_t i, uint32_t b) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+  const uint32_t sh = (i & 3) * 8;
+  w[i >> 2] = (w[i >> 2] & ~(0xFFu << sh)) | (b << sh);
+}
+
+constexpr int kPackThreads = 256;
+constexpr uint32_t kSubTile = 512;
+
+// Byte at stream position x, walking the record cursor forward from r.
+__device__ __forceinline__ uint32_t stream_byte(const crac_record_t* recs, uint32_t n,
+                                                uint32_t& r, uint64_t x) {
+  while (r + 1 < n && __ldg(&recs[r + 1].out_off) <= x) ++r;
+  const crac_record_t& R = recs[r];
+  if (x < R.out_off) return 0;
+  const uint64_t rel = x - R.out_off;
+  if (rel < R.frame_len) return R.frame[rel];
+  const uint64_t pl = rel - R.frame_len;
+  if (pl < R.len) return reinterpret_cast<const uint8_t*>(R.ptr)[pl];
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// K2a: pack
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kPackThreads)
+    k_pack_records(const crac_record_t* __restrict__ recs, uint32_t n,
+                   const uint32_t* __restrict__ tile_rec, uint64_t win_off, uint64_t win_len,
+                   uint8_t* __restrict__ dst) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t tile0 = win_off + uint64_t(blockIdx.x) * CRAC_TILE_BYTES;
+  const uint64_t win_end = win_off + win_len;
+  uint32_t rec = tile_rec[blockIdx.x];
+  for (uint32_t st = warp; st < CRAC_TILE_BYTES / kSubTile; st += kPackThreads / 32) {
+    const uint64_t o = tile0 + uint64_t(st) * kSubTile;
+    if (o >= win_end) break;
+    while (rec + 1 < n && __ldg(&recs[rec + 1].out_off) <= o) ++rec;
+    const uint64_t x = o + lane * 16;
+    uint4* out = reinterpret_cast<uint4*>(dst + (x - win_off));
+    const crac_record_t& R = recs[rec];
+    const uint64_t P = R.out_off + R.frame_len;
+    if (o >= P && o + kSubTile <= P + R.len) {
+      // whole sub-tile inside one payload: aligned stores, shifted loads
+      if (x < win_end) *out = load_shifted(reinterpret_cast<const uint8_t*>(R.ptr) + (x - P));
+    } else if (x < win_end) {
+      uint32_t r = rec;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      for (uint32_t i = 0; i < 16; ++i) set_byte(v, i, stream_byte(recs, n, r, x + i));
+      *out = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: scatter
+// ---------------------------------------------------------------------------
+// Destination word of record R whose first stream byte lies in [x, x + 16):
+// returns its index or UINT64_MAX.
+__device__ __forceinline__ uint64_t dest_word_at(const crac_record_t& R, uint64_t x) {
+  const uint64_t P = R.out_off + R.frame_len;
+  if (R.len == 0) return ~0ull;
+  const uint64_t d = x <= P ? 0 : (x - P + 15) >> 4;
+  const uint64_t f = P + 16 * d;
+  if (f >= x + 16 || 16 * d >= R.len) return ~0ull;
+  return d;
+}
+
+__global__ void __launch_bounds__(kPackThreads)
+    k_scatter_records(const crac_record_t* __restrict__ recs, uint32_t n,
+                      const uint32_t* __restrict__ tile_rec, const uint8_t* __restrict__ win,
+                      uint64_t win_off, uint64_t win_len) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t tile0 = win_off + uint64_t(blockIdx.x) * CRAC_TILE_BYTES;
+  const uint64_t win_end = win_off + win_len;
+  uint32_t rec = tile_rec[blockIdx.x];
+  for (uint32_t st = warp; st < CRAC_TILE_BYTES / kSubTile; st += kPackThreads / 32) {
+    const uint64_t o = tile0 + uint64_t(st) * kSubTile;
+    if (o >= win_end) break;
+    while (rec + 1 < n && __ldg(&recs[rec + 1].out_off) <= o) ++rec;
+    const uint64_t x = o + lane * 16;
+    const crac_record_t& R = recs[rec];
+    const uint64_t P = R.out_off + R.frame_len;
+    if (o >= P && o + kSubTile + 16 <= P + R.len) {
+      // fast path: every lane owns one full data word of R
+      const uint64_t d = (x - P + 15) >> 4;
+      const uint64_t f = P + 16 * d;
+      *reinterpret_cast<uint4*>(R.ptr + 16 * d) = load_shifted(win + (f - win_off));
+      continue;
+    }
+    if (x >= win_end) continue;
+    // slow path: the record owning a destination word that starts in [x, x+16)
+    uint32_t r = rec;
+    while (r + 1 < n && __ldg(&recs[r + 1].out_off) <= x + 15) ++r;
+    uint64_t d = dest_word_at(recs[r], x);
+    if (d == ~0ull && r > 0) {
+      --r;
+      d = dest_word_at(recs[r], x);
+    }
+    if (d == ~0ull) continue;
+    const crac_record_t& Q = recs[r];
+    const uint64_t Pq = Q.out_off + Q.frame_len;
+    const uint64_t f = Pq + 16 * d;
+    uint4 v = load_shifted(win + (f - win_off));
+    const uint64_t valid = Q.len - 16 * d;  // >= 1
+    if (valid < 16) {
+      for (uint32_t i = uint32_t(valid); i < 16; ++i) set_byte(v, i, 0);
+    }
+    uint4* dstw = reinterpret_cast<uint4*>(Q.ptr) + d;
+    *dstw = v;
+    if (16 * (d + 1) >= Q.len) {  // last data word: zero the padding words
+      const uint4 z = make_uint4(0, 0, 0, 0);
+      for (uint64_t e = d + 1; 16 * e < Q.ext; ++e) dstw[e - d] = z;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2b: dirty detection + compaction + gather
+// ---------------------------------------------------------------------------
+constexpr int kDiffThreads = 256;
+constexpr uint32_t kDiffPerThread = 16;
+constexpr uint32_t kDiffPerBlock = kDiffThreads * kDiffPerThread;  // 4096
+
+__global__ void __launch_bounds__(kDiffThreads)
+    k_diff_count(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, uint64_t n,
+                 uint32_t* __restrict__ block_counts) {
+  const uint64_t i0 = uint64_t(blockIdx.x) * kDiffPerBlock + threadIdx.x * kDiffPerThread;
+  uint32_t cnt = 0;
+  for (uint32_t k = 0; k < kDiffPerThread; ++k) {
+    const uint64_t i = i0 + k;
+    if (i < n && a[i] != b[i]) ++cnt;
+  }
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
+  __shared__ uint32_t ws[kDiffThreads / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < kDiffThreads / 32; ++w) t += ws[w];
+    block_counts[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kDiffThreads)
+    k_diff_write(const uint32_t* __restrict__ a, uint32_t* __restrict__ b, uint64_t n,
+                 const uint32_t* __restrict__ block_counts, uint64_t* __restrict__ idx,
+                 uint64_t* __restrict__ count) {
+  __shared__ uint64_t s_base;
+  __shared__ uint32_t s_warp[kDiffThreads / 32];
+  // block offset = sum of the counts of all preceding blocks
+  uint64_t part = 0;
+  for (uint32_t k = threadIdx.x; k < blockIdx.x; k += kDiffThreads) part += block_counts[k];
+  for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, o);
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_base), part);
+
+  const uint64_t i0 = uint64_t(blockIdx.x) * kDiffPerBlock + threadIdx.x * kDiffPerThread;
+  uint32_t mask = 0;
+  for (uint32_t k = 0; k < kDiffPerThread; ++k) {
+    const uint64_t i = i0 + k;
+    if (i < n && a[i] != b[i]) mask |= 1u << k;
+  }
+  const uint32_t mine = __popc(mask);
+  // exclusive scan of `mine` across the block
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = mine;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  uint32_t before = 0;
+  for (uint32_t w = 0; w < warp; ++w) before += s_warp[w];
+  uint64_t pos = s_base + before + incl - mine;
+  for (uint32_t k = 0; k < kDiffPerThread; ++k)
+    if (mask & (1u << k)) idx[pos++] = i0 + k;
+  if (blockIdx.x + 1 == gridDim.x && threadIdx.x == kDiffThreads - 1) *count = pos;
+  __syncthreads();
+  for (uint32_t k = 0; k < kDiffPerThread; ++k) {
+    const uint64_t i = i0 + k;
+    if (i < n) b[i] = a[i];
+  }
+}
+
+constexpr int kGatherThreads = 256;
+
+__global__ void __launch_bounds__(kGatherThreads)
+    k_gather(const crac_span_t* __restrict__ spans, const uint64_t* __restrict__ chunk_first,
+             uint32_t n_spans, uint32_t chunk_bytes, const uint64_t* __restrict__ dirty,
+             uint64_t first, uint64_t count, uint8_t* __restrict__ staging) {
+  for (uint64_t k = blockIdx.x; k < count; k += gridDim.x) {
+    const uint64_t c = dirty[first + k];
+    const uint32_t s = find_span(chunk_first, n_spans, c);
+    const crac_span_t sp = spans[s];
+    const uint64_t off = (c - chunk_first[s]) * chunk_bytes;
+    const uint64_t len = min(uint64_t(chunk_bytes), sp.len - off);
+    const uint4* src = reinterpret_cast<const uint4*>(sp.ptr + off);
+    uint4* dst = reinterpret_cast<uint4*>(staging + k * chunk_bytes);
+    const uint64_t words = (len + 15) >> 4;
+    for (uint64_t w = threadIdx.x; w < words; w += kGatherThreads) dst[w] = ldg_stream(src + w);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fixtures
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t crac_mix64(uint64_t x) {  // common.hpp:55-60
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ uint64_t synth_word(uint64_t seed, uint64_t id, uint64_t k) {
+  return crac_mix64(k + 0x1000003ull * id + (seed << 56));
+}
+
+__global__ void k_fill_synth(uint8_t* __restrict__ dst, uint64_t len, uint64_t seed, uint64_t id,
+                             uint64_t word_offset) {
+  const uint64_t words = len / 8;
+  const uint64_t pairs = words / 2;
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < pairs;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t w0 = synth_word(seed, id, word_offset + 2 * i);
+    const uint64_t w1 = synth_word(seed, id, word_offset + 2 * i + 1);
+    d4[i] = make_uint4(uint32_t(w0), uint32_t(w0 >> 32), uint32_t(w1), uint32_t(w1 >> 32));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (uint64_t k = 2 * pairs; k * 8 < len; ++k) {
+      const uint64_t w = synth_word(seed, id, word_offset + k);
+      for (uint32_t b = 0; b < 8 && k * 8 + b < len; ++b) dst[k * 8 + b] = uint8_t(w >> (8 * b));
+    }
+  }
+}
+
+__global__ void k_mutate(const crac_span_t* __restrict__ spans, const uint64_t* __restrict__ ids,
+                         const uint64_t* __restrict__ chunk_first, uint32_t n_spans,
+                         uint32_t chunk_bytes, uint64_t total_chunks, uint64_t seed,
+                         uint64_t epoch, uint64_t threshold) {
+  for (uint64_t c = blockIdx.x; c < total_chunks; c += gridDim.x) {
+    if (crac_mix64(seed ^ (epoch << 40) ^ c) >= threshold) continue;
+    const uint32_t s = find_span(chunk_first, n_spans, c);
+    const crac_span_t sp = spans[s];
+    const uint64_t off = (c - chunk_first[s]) * chunk_bytes;
+    const uint64_t len = min(uint64_t(chunk_bytes), sp.len - off);
+    uint8_t* dst = reinterpret_cast<uint8_t*>(sp.ptr + off);
+    const uint64_t words = len / 8;
+    for (uint64_t k = threadIdx.x; k < words; k += blockDim.x) {
+      const uint64_t w = synth_word(seed + epoch, ids[s], off / 8 + k);
+      reinterpret_cast<uint64_t*>(dst)[k] = w;
+    }
+    if (threadIdx.x == 0)
+      for (uint64_t b = words * 8; b < len; ++b)
+        dst[b] = uint8_t(synth_word(seed + epoch, ids[s], off / 8 + words) >> (8 * (b - words * 8)));
+  }
+}
+
+std::once_flag g_init_once;
+int g_init_rc = 0;
+uint32_t g_k_full_cache_bytes = 0;
+uint32_t g_k_full_cache = 0;
+std::mutex g_kfull_mu;
+
+int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+uint32_t k_full_for(uint32_t chunk_bytes) {
+  std::lock_guard<std::mutex> lk(g_kfull_mu);
+  if (g_k_full_cache_bytes != chunk_bytes) {
+    g_k_full_cache = crac::crc_affine(chunk_bytes);
+    g_k_full_cache_bytes = chunk_bytes;
+  }
+  return g_k_full_cache;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int crac_gpu_init(void) {
+  std::call_once(g_init_once, [] {
+    const HostTables h = build_tables();
+    cudaError_t e = cudaMemcpyToSymbol(g_tab, h.tab.data(), kTabBytes);
+    if (!e) e = cudaMemcpyToSymbol(g_t0, h.t0.data(), 256 * 4);
+    if (!e) e = cudaMemcpyToSymbol(g_xp16, h.xp16.data(), 33 * 4);
+    if (!e) e = cudaMemcpyToSymbol(g_xpt, h.xpt.data(), 512 * 4);
+    if (!e) e = cudaMemcpyToSymbol(g_pow2, h.pow2.data(), 64 * 4);
+    if (!e) e = cudaFuncSetAttribute(k1_chunk_crc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kTabBytes));
+    g_init_rc = int(e);
+  });
+  return g_init_rc;
+}
+
+int crac_chunk_crc32(const crac_span_t* d_spans, const uint64_t* d_chunk_first, uint32_t n_spans,
+                     uint32_t chunk_bytes, uint64_t total_chunks, uint32_t* d_crc, void* stream) {
+  if (total_chunks == 0) return 0;
+  if (chunk_bytes == 0 || chunk_bytes % 512) return int(cudaErrorInvalidValue);
+  if (int rc = crac_gpu_init()) return rc;
+  const uint64_t warps_needed = total_chunks;
+  uint64_t blocks = (warps_needed + kK1Warps - 1) / kK1Warps;
+  if (blocks > uint64_t(sm_count())) blocks = sm_count();
+  k1_chunk_crc<<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
+      d_spans, d_chunk_first, n_spans, chunk_bytes, total_chunks, d_crc, k_full_for(chunk_bytes));
+  return int(cudaGetLastError());
+}
+
+int crac_pack_records(const crac_record_t* d_recs, uint32_t n_recs, const uint32_t* d_tile_rec,
+                      uint64_t win_off, uint64_t win_len, uint8_t* d_out, void* stream) {
+  if (win_len == 0 || n_recs == 0) return 0;
+  if (win_off % CRAC_TILE_BYTES) return int(cudaErrorInvalidValue);
+  const uint64_t tiles = (win_len + CRAC_TILE_BYTES - 1) / CRAC_TILE_BYTES;
+  k_pack_records<<<unsigned(tiles), kPackThreads, 0, cudaStream_t(stream)>>>(
+      d_recs, n_recs, d_tile_rec, win_off, win_len, d_out);
+  return int(cudaGetLastError());
+}
+
+int crac_scatter_records(const crac_record_t* d_recs, uint32_t n_recs,
+                         const uint32_t* d_tile_rec, const uint8_t* d_win, uint64_t win_off,
+                         uint64_t win_len, void* stream) {
+  if (win_len == 0 || n_recs == 0) return 0;
+  if (win_off % CRAC_TILE_BYTES) return int(cudaErrorInvalidValue);
+  const uint64_t tiles = (win_len + CRAC_TILE_BYTES - 1) / CRAC_TILE_BYTES;
+  k_scatter_records<<<unsigned(tiles), kPackThreads, 0, cudaStream_t(stream)>>>(
+      d_recs, n_recs, d_tile_rec, d_win, win_off, win_len);
+  return int(cudaGetLastError());
+}
+
+int crac_diff_compact(const uint32_t* d_crc_new, uint32_t* d_crc_prev, uint64_t n_chunks,
+                      uint32_t* d_block_counts, uint64_t* d_dirty_idx, uint64_t* d_dirty_count,
+                      void* stream) {
+  cudaStream_t st = cudaStream_t(stream);
+  if (n_chunks == 0) return int(cudaMemsetAsync(d_dirty_count, 0, 8, st));
+  const uint64_t blocks = (n_chunks + kDiffPerBlock - 1) / kDiffPerBlock;
+  k_diff_count<<<unsigned(blocks), kDiffThreads, 0, st>>>(d_crc_new, d_crc_prev, n_chunks,
+                                                          d_block_counts);
+  k_diff_write<<<unsigned(blocks), kDiffThreads, 0, st>>>(d_crc_new, d_crc_prev, n_chunks,
+                                                          d_block_counts, d_dirty_idx,
+                                                          d_dirty_count);
+  return int(cudaGetLastError());
+}
+
+int crac_gather_chunks(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
+                       uint32_t n_spans, uint32_t chunk_bytes, const uint64_t* d_dirty_idx,
+                       uint64_t first, uint64_t count, uint8_t* d_staging, void* stream) {
+  if (count == 0) return 0;
+  if (chunk_bytes % 16) return int(cudaErrorInvalidValue);
+  uint64_t blocks = count;
+  if (blocks > uint64_t(sm_count()) * 16) blocks = uint64_t(sm_count()) * 16;
+  k_gather<<<unsigned(blocks), kGatherThreads, 0, cudaStream_t(stream)>>>(
+      d_spans, d_chunk_first, n_spans, chunk_bytes, d_dirty_idx, first, count, d_staging);
+  return int(cudaGetLastError());
+}
+
+int crac_fill_synth(uint8_t* d_dst, uint64_t len, uint64_t seed, uint64_t id,
+                    uint64_t word_offset, void* stream) {
+  if (len == 0) return 0;
+  if (reinterpret_cast<uint64_t>(d_dst) % 16) return int(cudaErrorInvalidValue);
+  uint64_t blocks = (len / 16 + 255) / 256;
+  if (blocks > uint64_t(sm_count()) * 8) blocks = uint64_t(sm_count()) * 8;
+  if (blocks == 0) blocks = 1;
+  k_fill_synth<<<unsigned(blocks), 256, 0, cudaStream_t(stream)>>>(d_dst, len, seed, id,
+                                                                   word_offset);
+  return int(cudaGetLastError());
+}
+
+int crac_mutate_chunks(const crac_span_t* d_spans, const uint64_t* d_ids,
+                       const uint64_t* d_chunk_first, uint32_t n_spans, uint32_t chunk_bytes,
+                       uint64_t total_chunks, uint64_t seed, uint64_t epoch, uint64_t threshold,
+                       void* stream) {
+  if (total_chunks == 0) return 0;
+  uint64_t blocks = total_chunks;
+  if (blocks > uint64_t(sm_count()) * 32) blocks = uint64_t(sm_count()) * 32;
+  k_mutate<<<unsigned(blocks), 256, 0, cudaStream_t(stream)>>>(
+      d_spans, d_ids, d_chunk_first, n_spans, chunk_bytes, total_chunks, seed, epoch, threshold);
+  return int(cudaGetLastError());
+}
+
+}  // extern "C"

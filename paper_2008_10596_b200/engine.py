@@ -1,0 +1,392 @@
+"""Python host mirror of the reference engine API over the C-ABI (crac_engine.h).
+
+Names follow the reference (ref: /root/reference/proj/include/cracsim/
+ckpt_engine.hpp, shim.hpp, image.hpp): ``Session`` with the interposed
+``RuntimeApi`` calls, ``checkpoint`` / ``restart`` / ``decode_image`` /
+``summarize_image``.  Errors surface as ``CracError`` carrying the reference
+``Errc`` name.  There is no CPU fallback: if ``libcrac_b200.so`` is missing or
+the GPU is unusable every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Iterable, Optional, Sequence
+
+LIB_PATH = Path(__file__).resolve().parent / "libcrac_b200.so"
+
+DEVICE, PINNED, MANAGED = 1, 2, 3
+HOST_SIDE, DEVICE_SIDE = 0, 1
+DIRECT, PROXY = 0, 1
+
+ERRC = ["InvalidArgument", "OutOfArena", "DoubleFree", "UnknownId", "StreamLimitExceeded",
+        "BusyStream", "UnregisteredKernel", "DuplicateKernelId", "OutOfRange", "NotManaged",
+        "HalfConflict", "QuiesceTimeout", "ReplayDivergence", "ImageCorrupt",
+        "UnknownKernelBody", "DivisionByZero", "DeviceFault"]
+
+
+class CracError(RuntimeError):
+    def __init__(self, rc: int, message: str):
+        self.rc = rc
+        self.errc = ERRC[rc - 1] if 1 <= rc <= len(ERRC) else "Unknown"
+        super().__init__(f"{self.errc}: {message}")
+
+
+class Stats(C.Structure):
+    _fields_ = [("total_ms", C.c_double), ("hash_ms", C.c_double), ("pack_ms", C.c_double),
+                ("copy_ms", C.c_double), ("hash_bytes", C.c_uint64), ("hash_launches", C.c_uint64),
+                ("pack_launches", C.c_uint64), ("pack_bytes", C.c_uint64),
+                ("d2h_bytes", C.c_uint64), ("h2d_bytes", C.c_uint64),
+                ("image_bytes", C.c_uint64), ("dirty_chunks", C.c_uint64),
+                ("total_chunks", C.c_uint64), ("incremental", C.c_int32),
+                ("reserved", C.c_int32)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
+_LIB: Optional[C.CDLL] = None
+
+# name -> (restype, argtypes)
+_U64, _U32, _U8, _I64, _P = C.c_uint64, C.c_uint32, C.c_uint8, C.c_int64, C.c_void_p
+_PU64, _PU32, _PU8 = C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), C.POINTER(C.c_uint8)
+_SIGS = {
+    "crac_last_error": (C.c_char_p, []),
+    "crac_abi_version": (C.c_int, []),
+    "crac_session_create": (C.c_int, [_U64, _U64, C.c_int, _U32, C.POINTER(_P)]),
+    "crac_session_destroy": (None, [_P]),
+    "crac_session_fixed_va": (C.c_int, [_P]),
+    "crac_alloc": (C.c_int, [_P, _U8, _U64, _PU64, _PU64]),
+    "crac_free": (C.c_int, [_P, _U64]),
+    "crac_stream_create": (C.c_int, [_P, _PU64]),
+    "crac_stream_destroy": (C.c_int, [_P, _U64]),
+    "crac_register_fat_binary": (C.c_int, [_P, _U32, C.POINTER(C.c_char_p), _PU32, _PU32, _PU64]),
+    "crac_unregister_fat_binary": (C.c_int, [_P, _U64]),
+    "crac_launch": (C.c_int, [_P, _U64, C.c_char_p, _U32, _PU64, _PU64, _U32, _PU64]),
+    "crac_copy_h2d": (C.c_int, [_P, _U64, _U64, _P, _U64, _I64]),
+    "crac_copy_d2h": (C.c_int, [_P, _P, _U64, _U64, _U64, _I64]),
+    "crac_copy_d2d": (C.c_int, [_P, _U64, _U64, _U64, _U64, _U64, _I64]),
+    "crac_synchronize": (C.c_int, [_P]),
+    "crac_page_read": (C.c_int, [_P, _U64, _U64, _U64, _U8, _P]),
+    "crac_page_write": (C.c_int, [_P, _U64, _U64, _P, _U64, _U8]),
+    "crac_set_app_state": (C.c_int, [_P, _P, _U64]),
+    "crac_image_create": (C.c_int, [C.POINTER(_P)]),
+    "crac_image_destroy": (None, [_P]),
+    "crac_image_view": (C.c_int, [_P, C.POINTER(_P), _PU64]),
+    "crac_checkpoint": (C.c_int, [_P, _P, C.POINTER(Stats)]),
+    "crac_checkpoint_incremental": (C.c_int, [_P, _P, C.POINTER(Stats)]),
+    "crac_checkpoint_value": (C.c_int, [_P, C.POINTER(_P), _PU64]),
+    "crac_restart": (C.c_int, [_P, _U64, C.c_int, C.POINTER(_P), C.POINTER(Stats)]),
+    "crac_decode_check": (C.c_int, [_P, _U64]),
+    "crac_summarize": (C.c_int, [_P, _U64, _PU64, _PU32, _PU64]),
+    "crac_debug_dump": (C.c_int, [_P, C.POINTER(C.c_char_p)]),
+    "crac_buffer_free": (None, [_P]),
+    "crac_log_size": (C.c_int, [_P, _PU64]),
+    "crac_live_records": (C.c_int, [_P, _U64, _PU64, _PU8, _PU64, _PU64, _PU64]),
+    "crac_managed_pages": (C.c_int, [_P, _U64, _U64, _PU8, _PU64]),
+    "crac_read_raw": (C.c_int, [_P, _U64, _U64, _P]),
+    "crac_backing_ptr": (C.c_int, [_P, _U64, _PU64]),
+    "crac_fill_synthetic": (C.c_int, [_P, _U64, _U64, _U8]),
+    "crac_mutate_device": (C.c_int, [_P, _U64, _U64, _U64, _PU64]),
+    "crac_hash_host_buffer": (C.c_int, [_P, _U64, _U32, _PU32]),
+    # kernel-level C-ABI (crac_gpu.h)
+    "crac_gpu_init": (C.c_int, []),
+    "crac_chunk_crc32": (C.c_int, [_P, _P, _U32, _U32, _U64, _P, _P]),
+    "crac_pack_records": (C.c_int, [_P, _U32, _P, _U64, _U64, _P, _P]),
+    "crac_scatter_records": (C.c_int, [_P, _U32, _P, _P, _U64, _U64, _P]),
+    "crac_diff_compact": (C.c_int, [_P, _P, _U64, _P, _P, _P, _P]),
+    "crac_gather_chunks": (C.c_int, [_P, _P, _U32, _U32, _P, _U64, _U64, _P, _P]),
+    "crac_fill_synth": (C.c_int, [_P, _U64, _U64, _U64, _U64, _P]),
+    "crac_mutate_chunks": (C.c_int, [_P, _P, _P, _U32, _U32, _U64, _U64, _U64, _U64, _P]),
+}
+
+
+def exported_symbols() -> list[str]:
+    return sorted(_SIGS)
+
+
+def lib() -> C.CDLL:
+    """Loads the in-tree CUDA library; raises loudly if it is absent."""
+    global _LIB
+    if _LIB is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2008_10596_b200.build` "
+                               "(there is no CPU fallback)")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise CracError(rc, lib().crac_last_error().decode(errors="replace"))
+
+
+def _buf(data) -> tuple[C.c_void_p, int, object]:
+    """(pointer, length, keepalive) for bytes / bytearray / memoryview / numpy."""
+    mv = memoryview(data).cast("B")
+    if mv.readonly:
+        keep = C.create_string_buffer(bytes(mv), len(mv)) if len(mv) else C.create_string_buffer(1)
+        return C.cast(keep, C.c_void_p), len(mv), keep
+    arr = (C.c_char * len(mv)).from_buffer(mv) if len(mv) else C.create_string_buffer(1)
+    return C.cast(arr, C.c_void_p), len(mv), arr
+
+
+def _opt_stream(stream: Optional[int]) -> int:
+    return -1 if stream is None else int(stream)
+
+
+class Image:
+    """Page-locked image buffer (cracsim::PinnedImage), reused across checkpoints."""
+
+    def __init__(self):
+        h = C.c_void_p()
+        _check(lib().crac_image_create(C.byref(h)))
+        self._h = h
+
+    def view(self) -> memoryview:
+        p, n = C.c_void_p(), C.c_uint64()
+        _check(lib().crac_image_view(self._h, C.byref(p), C.byref(n)))
+        if n.value == 0:
+            return memoryview(b"")
+        return memoryview((C.c_char * n.value).from_address(p.value)).cast("B")
+
+    def address(self) -> tuple[int, int]:
+        p, n = C.c_void_p(), C.c_uint64()
+        _check(lib().crac_image_view(self._h, C.byref(p), C.byref(n)))
+        return p.value or 0, n.value
+
+    def tobytes(self) -> bytes:
+        return bytes(self.view())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().crac_image_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class LiveRecord:
+    id: int
+    kind: int
+    size: int
+    address: int
+
+
+class Session:
+    """ref: cracsim::Session + RuntimeApi (ckpt_engine.hpp:29-55, shim.hpp:159-184)."""
+
+    def __init__(self, seed: int = 0, arena_bytes: int = 1 << 24, mode: int = DIRECT,
+                 quiesce_timeout_ms: int = 30000, _handle: Optional[C.c_void_p] = None):
+        if _handle is None:
+            h = C.c_void_p()
+            _check(lib().crac_session_create(seed, arena_bytes, mode, quiesce_timeout_ms, C.byref(h)))
+            _handle = h
+        self._h = _handle
+
+    # ---- RuntimeApi ----
+    def alloc(self, kind: int, size: int) -> tuple[int, int]:
+        i, a = C.c_uint64(), C.c_uint64()
+        _check(lib().crac_alloc(self._h, kind, size, C.byref(i), C.byref(a)))
+        return i.value, a.value
+
+    def free(self, alloc_id: int) -> None:
+        _check(lib().crac_free(self._h, alloc_id))
+
+    def stream_create(self) -> int:
+        i = C.c_uint64()
+        _check(lib().crac_stream_create(self._h, C.byref(i)))
+        return i.value
+
+    def stream_destroy(self, stream: int) -> None:
+        _check(lib().crac_stream_destroy(self._h, stream))
+
+    def register_fat_binary(self, kernels: Sequence[tuple[str, int, int]]) -> int:
+        n = len(kernels)
+        names = (C.c_char_p * max(n, 1))(*[k[0].encode() for k in kernels])
+        ba = (C.c_uint32 * max(n, 1))(*[k[1] for k in kernels])
+        sa = (C.c_uint32 * max(n, 1))(*[k[2] for k in kernels])
+        h = C.c_uint64()
+        _check(lib().crac_register_fat_binary(self._h, n, names, ba, sa, C.byref(h)))
+        return h.value
+
+    def unregister_fat_binary(self, handle: int) -> None:
+        _check(lib().crac_unregister_fat_binary(self._h, handle))
+
+    def launch(self, stream: int, kernel: str, buffers: Iterable[tuple[int, int]] = (),
+               scalars: Iterable[int] = ()) -> None:
+        b = list(buffers)
+        s = list(scalars)
+        ids = (C.c_uint64 * max(len(b), 1))(*[x[0] for x in b])
+        offs = (C.c_uint64 * max(len(b), 1))(*[x[1] for x in b])
+        sc = (C.c_uint64 * max(len(s), 1))(*[x & (2**64 - 1) for x in s])
+        _check(lib().crac_launch(self._h, stream, kernel.encode(), len(b), ids, offs, len(s), sc))
+
+    def copy_h2d(self, alloc_id: int, offset: int, data, stream: Optional[int] = None) -> None:
+        p, n, keep = _buf(data)
+        _check(lib().crac_copy_h2d(self._h, alloc_id, offset, p, n, _opt_stream(stream)))
+
+    def copy_d2h(self, alloc_id: int, offset: int, n: int, stream: Optional[int] = None) -> bytes:
+        out = C.create_string_buffer(max(n, 1))
+        _check(lib().crac_copy_d2h(self._h, out, alloc_id, offset, n, _opt_stream(stream)))
+        return out.raw[:n]
+
+    def copy_d2d(self, dst: tuple[int, int], src: tuple[int, int], n: int,
+                 stream: Optional[int] = None) -> None:
+        _check(lib().crac_copy_d2d(self._h, dst[0], dst[1], src[0], src[1], n, _opt_stream(stream)))
+
+    def synchronize(self) -> None:
+        _check(lib().crac_synchronize(self._h))
+
+    def page_read(self, alloc_id: int, offset: int, n: int, side: int) -> bytes:
+        out = C.create_string_buffer(max(n, 1))
+        _check(lib().crac_page_read(self._h, alloc_id, offset, n, side, out))
+        return out.raw[:n]
+
+    def page_write(self, alloc_id: int, offset: int, data, side: int) -> None:
+        p, n, keep = _buf(data)
+        _check(lib().crac_page_write(self._h, alloc_id, offset, p, n, side))
+
+    def set_app_state(self, data) -> None:
+        p, n, keep = _buf(data)
+        _check(lib().crac_set_app_state(self._h, p, n))
+
+    # ---- engine ----
+    def checkpoint(self, image: Optional[Image] = None) -> tuple[bytes, dict]:
+        """checkpoint_image: returns (image bytes, device-timed stats)."""
+        img = image or Image()
+        st = Stats()
+        _check(lib().crac_checkpoint(self._h, img._h, C.byref(st)))
+        return img.tobytes(), st.as_dict()
+
+    def checkpoint_into(self, image: Image, incremental: bool = False) -> dict:
+        st = Stats()
+        fn = lib().crac_checkpoint_incremental if incremental else lib().crac_checkpoint
+        _check(fn(self._h, image._h, C.byref(st)))
+        return st.as_dict()
+
+    def checkpoint_value(self) -> bytes:
+        """encode_image(checkpoint(session)) through the value-type adapter."""
+        p, n = C.c_void_p(), C.c_uint64()
+        _check(lib().crac_checkpoint_value(self._h, C.byref(p), C.byref(n)))
+        try:
+            return C.string_at(p, n.value)
+        finally:
+            lib().crac_buffer_free(p)
+
+    # ---- introspection / fixtures ----
+    @property
+    def fixed_va(self) -> bool:
+        return bool(lib().crac_session_fixed_va(self._h))
+
+    def debug_dump(self) -> str:
+        p = C.c_char_p()
+        _check(lib().crac_debug_dump(self._h, C.byref(p)))
+        s = p.value.decode()
+        lib().crac_buffer_free(C.cast(p, C.c_void_p))
+        return s
+
+    def log_size(self) -> int:
+        n = C.c_uint64()
+        _check(lib().crac_log_size(self._h, C.byref(n)))
+        return n.value
+
+    def live_records(self) -> list[LiveRecord]:
+        n = C.c_uint64()
+        _check(lib().crac_live_records(self._h, 0, None, None, None, None, C.byref(n)))
+        k = n.value
+        ids, kinds = (C.c_uint64 * max(k, 1))(), (C.c_uint8 * max(k, 1))()
+        sizes, addrs = (C.c_uint64 * max(k, 1))(), (C.c_uint64 * max(k, 1))()
+        _check(lib().crac_live_records(self._h, k, ids, kinds, sizes, addrs, C.byref(n)))
+        return [LiveRecord(ids[i], kinds[i], sizes[i], addrs[i]) for i in range(k)]
+
+    def managed_pages(self, alloc_id: int) -> list[int]:
+        n = C.c_uint64()
+        _check(lib().crac_managed_pages(self._h, alloc_id, 0, None, C.byref(n)))
+        flags = (C.c_uint8 * max(n.value, 1))()
+        _check(lib().crac_managed_pages(self._h, alloc_id, n.value, flags, C.byref(n)))
+        return list(flags[: n.value])
+
+    def read_raw(self, address: int, n: int) -> bytes:
+        out = C.create_string_buffer(max(n, 1))
+        _check(lib().crac_read_raw(self._h, address, n, out))
+        return out.raw[:n]
+
+    def backing_ptr(self, alloc_id: int) -> int:
+        p = C.c_uint64()
+        _check(lib().crac_backing_ptr(self._h, alloc_id, C.byref(p)))
+        return p.value
+
+    def fill_synthetic(self, alloc_id: int, seed: int, side: int = DEVICE_SIDE) -> None:
+        _check(lib().crac_fill_synthetic(self._h, alloc_id, seed, side))
+
+    def mutate(self, seed: int, epoch: int, threshold: int) -> int:
+        n = C.c_uint64()
+        _check(lib().crac_mutate_device(self._h, seed, epoch, threshold, C.byref(n)))
+        return n.value
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().crac_session_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def restart(image, mode: int = DIRECT) -> tuple[Session, dict]:
+    """restart_image: strict parse + replay + GPU refill + CRC verify."""
+    p, n, keep = _buf(image)
+    h, st = C.c_void_p(), Stats()
+    _check(lib().crac_restart(p, n, mode, C.byref(h), C.byref(st)))
+    return Session(_handle=h), st.as_dict()
+
+
+def restart_from_address(addr: int, n: int, mode: int = DIRECT) -> tuple[Session, dict]:
+    """Zero-copy restart from an image already in (pinned) host memory."""
+    h, st = C.c_void_p(), Stats()
+    _check(lib().crac_restart(C.c_void_p(addr), n, mode, C.byref(h), C.byref(st)))
+    return Session(_handle=h), st.as_dict()
+
+
+def decode_check(image) -> None:
+    p, n, keep = _buf(image)
+    _check(lib().crac_decode_check(p, n))
+
+
+def summarize_image(image) -> dict:
+    p, n, keep = _buf(image)
+    lengths, crcs, totals = (C.c_uint64 * 7)(), (C.c_uint32 * 7)(), (C.c_uint64 * 5)()
+    _check(lib().crac_summarize(p, n, lengths, crcs, totals))
+    return {"lengths": list(lengths), "crcs": list(crcs), "log_entries": totals[0],
+            "active_allocations": totals[1], "payload_bytes": totals[2],
+            "uvm_page_bytes": totals[3], "file_bytes": totals[4]}
+
+
+def hash_chunks(data, chunk_bytes: int = 65536) -> list[int]:
+    """K1 on the GPU over a host buffer: CRC-32 of every chunk."""
+    p, n, keep = _buf(data)
+    k = (n + chunk_bytes - 1) // chunk_bytes
+    out = (C.c_uint32 * max(k, 1))()
+    _check(lib().crac_hash_host_buffer(p, n, chunk_bytes, out))
+    return list(out[:k])

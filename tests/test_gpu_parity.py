@@ -1,0 +1,283 @@
+"""GPU tier: the B200 drain/refill against the oracle, through the C-ABI.
+
+Bar: bit-exact.  Every image the GPU path emits must equal, byte for byte,
+the image the unmodified reference library emits for the same call sequence
+(live, via oracle/_ref, and frozen in tests/golden); every restart must
+reproduce the state; every corruption must be refused with ImageCorrupt.
+"""
+import os
+import random
+import struct
+import zlib
+
+import pytest
+
+import workloads
+from oracle import image_oracle as io
+from oracle import ref
+
+pytestmark = pytest.mark.gpu
+
+
+# ---------------------------------------------------------------------------
+# K1 (chunk CRC) against the restated zlib CRC
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n", [1, 15, 16, 17, 511, 512, 513, 4095, 4096, 4097, 65535, 65536,
+                               65537, 65536 * 3 + 1234, 1 << 20])
+@pytest.mark.parametrize("chunk", [512, 4096, 65536])
+def test_k1_chunk_crc_matches_oracle(eng, n, chunk):
+    data = os.urandom(n)
+    got = eng.hash_chunks(data, chunk)
+    want = ref.chunk_crc32(data, chunk)
+    assert got == want
+    assert want == [zlib.crc32(data[i:i + chunk]) for i in range(0, n, chunk)]
+
+
+def test_k1_known_answer(eng):
+    assert eng.hash_chunks(b"123456789", 512) == [0xCBF43926]
+    zeros = bytes(65536)
+    assert eng.hash_chunks(zeros) == [zlib.crc32(zeros)]
+
+
+# ---------------------------------------------------------------------------
+# drain parity: GPU image == reference image
+# ---------------------------------------------------------------------------
+def test_empty_session_is_188_bytes(eng, golden):
+    _, images = golden
+    s = eng.Session(seed=0, arena_bytes=1 << 24)
+    img, stats = s.checkpoint()
+    assert img == images["empty"]
+    assert stats["image_bytes"] == 188
+
+
+def test_small_session_matches_golden_and_live_reference(eng, golden):
+    _, images = golden
+    s = eng.Session(seed=3, arena_bytes=1 << 22)
+    workloads.drive_small(s, seed=1)
+    img, stats = s.checkpoint()
+    assert img == images["small_session"]
+    r = ref.RefSession(seed=3, arena_bytes=1 << 22)
+    workloads.drive_small(r, seed=1)
+    assert img == r.checkpoint()[0]
+    assert stats["hash_launches"] >= 1 and stats["pack_launches"] >= 1
+    # the value-type adapter (checkpoint -> Snapshot -> encode_image) agrees
+    assert s.checkpoint_value() == img
+
+
+def test_c1_mini_matches_golden(eng, golden):
+    _, images = golden
+    s = eng.Session(seed=1, arena_bytes=1 << 24)
+    workloads.build_regions(s, 8, lambda r: 100 * 1024 - r % 3 * 17, seed=1)
+    assert s.checkpoint()[0] == images["c1_mini"]
+
+
+def test_random_sequence_matches_golden(eng, golden):
+    _, images = golden
+    s = eng.Session(seed=7, arena_bytes=1 << 20)
+    workloads.drive_random(s, seed=42, ops=300, arena=1 << 20)
+    assert s.checkpoint()[0] == images["random_300"]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_sessions_match_reference(eng, seed):
+    s = eng.Session(seed=seed, arena_bytes=1 << 21)
+    r = ref.RefSession(seed=seed, arena_bytes=1 << 21)
+    for api in (s, r):
+        workloads.drive_random(api, seed=1000 + seed, ops=400, arena=1 << 21)
+        api.set_app_state(bytes([seed]) * (seed * 7))
+    assert s.checkpoint()[0] == r.checkpoint()[0]
+
+
+def test_checkpoint_is_non_destructive_and_repeatable(eng):
+    s = eng.Session(seed=2, arena_bytes=1 << 22)
+    workloads.drive_small(s, seed=5)
+    a = s.checkpoint()[0]
+    b = s.checkpoint()[0]
+    assert a == b
+    # the session keeps working and the log continues
+    i, addr = s.alloc(workloads.DEVICE, 2048)
+    r = ref.RefSession(seed=2, arena_bytes=1 << 22)
+    workloads.drive_small(r, seed=5)
+    r.checkpoint()
+    assert (i, addr) == r.alloc(workloads.DEVICE, 2048)
+
+
+def test_c1_shape_odd_sizes_matches_reference(eng):
+    # odd region sizes (4 MiB - r%3) stress the misaligned framing
+    n, size = 24, lambda r: (1 << 20) - r % 3
+    s = eng.Session(seed=1, arena_bytes=32 << 20)
+    r = ref.RefSession(seed=1, arena_bytes=32 << 20)
+    for api in (s, r):
+        workloads.build_regions(api, n, size, seed=1)
+    img, stats = s.checkpoint()
+    assert img == r.checkpoint()[0]
+    assert stats["d2h_bytes"] == sum(16 + size(k) for k in range(n)) + 20
+
+
+def test_queued_work_is_drained_before_capture(eng):
+    # test_ckpt_engine.cpp:332-349
+    s = eng.Session(seed=0, arena_bytes=1 << 20)
+    s.register_fat_binary(workloads.STD_KERNELS)
+    st = s.stream_create()
+    i, _ = s.alloc(workloads.DEVICE, 1024)
+    s.launch(st, "fill8", [(i, 0)], [9, 1024])
+    s.launch(st, "add8", [(i, 0)], [1, 1024])
+    img = s.checkpoint()[0]
+    snap = io.decode_image(img)
+    assert snap.payloads == [(i, bytes([10]) * 1024)]
+
+
+# ---------------------------------------------------------------------------
+# refill
+# ---------------------------------------------------------------------------
+def _state(api):
+    recs = api.live_records()
+    out = []
+    for rec in recs:
+        rid, kind, size, addr = (rec.id, rec.kind, rec.size, rec.address) if hasattr(rec, "id") else rec
+        entry = [rid, kind, size, addr, api.read_raw(addr, size)]
+        if kind == workloads.MANAGED:
+            entry.append(api.managed_pages(rid))
+        out.append(entry)
+    return out
+
+
+def test_restart_round_trip_is_lossless(eng):
+    s = eng.Session(seed=4, arena_bytes=1 << 22)
+    workloads.drive_small(s, seed=2)
+    first, _ = s.checkpoint()
+    r, stats = eng.restart(first)
+    assert _state(r) == _state(s)
+    second, _ = r.checkpoint()
+    assert second == first  # test_ckpt_engine.cpp:212-224
+    assert stats["h2d_bytes"] > 0 and stats["hash_launches"] >= 1
+    # ids / stream ids continue past the old ceiling
+    assert r.stream_create() == s.stream_create()
+    assert r.alloc(workloads.DEVICE, 64) == s.alloc(workloads.DEVICE, 64)
+
+
+def test_restart_from_reference_images(eng, golden):
+    _, images = golden
+    for name in ("small_session", "c1_mini", "random_300", "empty"):
+        r, _ = eng.restart(images[name])
+        assert r.checkpoint()[0] == images[name]
+        live = ref.ref_restart(images[name])[0]
+        assert _state(r) == _state(live)
+
+
+def test_reference_restarts_from_gpu_images(eng):
+    s = eng.Session(seed=9, arena_bytes=1 << 22)
+    workloads.drive_small(s, seed=3)
+    img, _ = s.checkpoint()
+    rs, _ = ref.ref_restart(img)
+    assert rs.checkpoint()[0] == img
+
+
+def test_restart_of_restart_is_lossless(eng, golden):
+    _, images = golden
+    img = images["random_300"]
+    for _ in range(3):
+        r, _ = eng.restart(img)
+        img2 = r.checkpoint()[0]
+        assert img2 == img
+        img = img2
+
+
+def test_bulk_corruption_is_caught_by_the_gpu_verify(eng, golden):
+    _, images = golden
+    img = bytearray(images["c1_mini"])
+    summ = ref.ref_summarize(bytes(img))
+    s3 = 16 + (20 + 24) + (20 + summ["lengths"][1]) + 16
+    rnd = random.Random(1)
+    for _ in range(24):
+        # flip a payload (not frame) bit deep inside ALLOC_PAYLOADS
+        pos = s3 + 16 + rnd.randrange(100 * 1024 - 64)
+        bit = 1 << rnd.randrange(8)
+        img[pos] ^= bit
+        with pytest.raises(eng.CracError) as e:
+            eng.restart(bytes(img))
+        assert e.value.errc == "ImageCorrupt"
+        img[pos] ^= bit
+    eng.restart(bytes(img))  # restored image is accepted
+
+
+def test_every_bit_flip_of_small_image_refused_by_restart(eng, golden):
+    _, images = golden
+    img = bytearray(images["small_session"])
+    rnd = random.Random(3)
+    for _ in range(64):
+        bit = rnd.randrange(len(img) * 8)
+        img[bit // 8] ^= 1 << (bit % 8)
+        with pytest.raises(eng.CracError) as e:
+            eng.restart(bytes(img))
+        assert e.value.errc == "ImageCorrupt"
+        img[bit // 8] ^= 1 << (bit % 8)
+
+
+def test_tampered_log_address_is_replay_divergence(eng, golden):
+    _, images = golden
+    snap = io.decode_image(images["small_session"])
+    # second Alloc record: shift its address by one alignment unit (test_ckpt_engine.cpp:132-141)
+    k = [i for i, e in enumerate(snap.log) if e[1] == 1][1]
+    seq, op, kind, size, ident, addr = snap.log[k]
+    snap.log[k] = (seq, op, kind, size, ident, addr + 256)
+    bad = io.encode_image(snap)
+    with pytest.raises(eng.CracError) as e:
+        eng.restart(bad)
+    assert e.value.errc in ("ReplayDivergence", "ImageCorrupt")
+    with pytest.raises(ref.RefError) as e2:
+        ref.ref_restart(bad)
+    assert e.value.errc == e2.value.errc
+
+
+def test_unknown_kernel_body_refused(eng, golden):
+    _, images = golden
+    with pytest.raises(eng.CracError) as e:
+        eng.restart(images["rich"])  # "scale"/"probe" are not in the standard catalog
+    assert e.value.errc == "UnknownKernelBody"
+
+
+def test_managed_residence_restored(eng):
+    s = eng.Session(seed=1, arena_bytes=1 << 22)
+    m, _ = s.alloc(workloads.MANAGED, 6 * 4096 + 10)
+    s.page_write(m, 0, workloads.patterned(6 * 4096 + 10, 1), workloads.HOST_SIDE)
+    s.page_read(m, 2 * 4096, 3 * 4096, workloads.DEVICE_SIDE)
+    flags = s.managed_pages(m)
+    assert flags == [2, 2, 3, 3, 3, 2, 2]
+    img, _ = s.checkpoint()
+    r, _ = eng.restart(img)
+    assert r.managed_pages(m) == flags
+    assert r.page_read(m, 0, 6 * 4096 + 10, workloads.HOST_SIDE) == workloads.patterned(6 * 4096 + 10, 1)
+
+
+# ---------------------------------------------------------------------------
+# incremental drain (new behaviour: must emit exactly the full image)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("pct", [0, 1, 25, 100])
+def test_incremental_equals_full(eng, pct):
+    s = eng.Session(seed=1, arena_bytes=64 << 20)
+    workloads.build_regions(s, 12, lambda r: (4 << 20) - r * 4096 - (r % 2) * 100, seed=3)
+    image = eng.Image()
+    st0 = s.checkpoint_into(image)
+    assert not st0["incremental"]
+    threshold = (2**64 - 1) * pct // 100
+    for epoch in range(1, 3):
+        mutated = s.mutate(seed=3, epoch=epoch, threshold=threshold)
+        st = s.checkpoint_into(image, incremental=True)
+        assert st["incremental"]
+        inc = image.tobytes()
+        full = s.checkpoint()[0]
+        assert inc == full
+        assert st["dirty_chunks"] == mutated
+
+
+def test_incremental_falls_back_when_layout_changes(eng):
+    s = eng.Session(seed=1, arena_bytes=16 << 20)
+    workloads.build_regions(s, 4, lambda r: 1 << 20, seed=1)
+    image = eng.Image()
+    s.checkpoint_into(image)
+    i, _ = s.alloc(workloads.DEVICE, 12345)
+    s.fill_synthetic(i, 5)
+    st = s.checkpoint_into(image, incremental=True)
+    assert not st["incremental"]
+    assert image.tobytes() == s.checkpoint()[0]
