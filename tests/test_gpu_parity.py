@@ -42,6 +42,13 @@ def test_k1_known_answer(eng):
 # ---------------------------------------------------------------------------
 # drain parity: GPU image == reference image
 # ---------------------------------------------------------------------------
+def test_arena_sits_at_the_reference_base(eng):
+    s = eng.Session(seed=0, arena_bytes=1 << 20)
+    assert s.fixed_va  # logged addresses are the device pointers
+    i, addr = s.alloc(workloads.DEVICE, 100)
+    assert addr == 0x0D00_0000_0000 == s.backing_ptr(i)
+
+
 def test_empty_session_is_188_bytes(eng, golden):
     _, images = golden
     s = eng.Session(seed=0, arena_bytes=1 << 24)
@@ -158,7 +165,7 @@ def test_restart_round_trip_is_lossless(eng):
 
 def test_restart_from_reference_images(eng, golden):
     _, images = golden
-    for name in ("small_session", "c1_mini", "random_300", "empty"):
+    for name in ("small_session", "c1_mini", "empty"):
         r, _ = eng.restart(images[name])
         assert r.checkpoint()[0] == images[name]
         live = ref.ref_restart(images[name])[0]
@@ -175,7 +182,7 @@ def test_reference_restarts_from_gpu_images(eng):
 
 def test_restart_of_restart_is_lossless(eng, golden):
     _, images = golden
-    img = images["random_300"]
+    img = images["small_session"]
     for _ in range(3):
         r, _ = eng.restart(img)
         img2 = r.checkpoint()[0]
@@ -232,9 +239,14 @@ def test_tampered_log_address_is_replay_divergence(eng, golden):
 
 def test_unknown_kernel_body_refused(eng, golden):
     _, images = golden
-    with pytest.raises(eng.CracError) as e:
-        eng.restart(images["rich"])  # "scale"/"probe" are not in the standard catalog
-    assert e.value.errc == "UnknownKernelBody"
+    # "scale"/"probe" and the random gen_k* kernels are not in the standard catalog
+    for name in ("rich", "random_300"):
+        with pytest.raises(eng.CracError) as e:
+            eng.restart(images[name])
+        assert e.value.errc == "UnknownKernelBody"
+        with pytest.raises(ref.RefError) as e2:
+            ref.ref_restart(images[name])
+        assert e2.value.errc == "UnknownKernelBody"
 
 
 def test_managed_residence_restored(eng):
