@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""Checkpoint & restart GB/s per GPU and whole box (BASELINE.json metric).
+
+Workload (BASELINE.json configs[3], "C4"): every rank owns one B200 holding
+120 GiB of live device state in 1920 x 64 MiB cudaMalloc-kind regions with
+synthetic content.  One step = full checkpoint drain of that state into a
+page-locked host image (crac_checkpoint) + session teardown + restart refill
+from the image (crac_restart: replay, H2D, scatter, CRC verify).  Ranks drain
+independently; the only cross-rank step is a host barrier (gloo), exactly the
+"global barrier" of the config.  Inputs (120 GiB/GPU) exceed L2 by ~1000x.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+value  = 2 x live bytes x ranks / (max over ranks of the summed device-event
+         time of the drain and refill operations)
+e2e    = same bytes / (max over ranks of the CUDA-event interval around the K
+         steps through the public C-ABI, host image buffers, teardown included)
+--impl reference times the reference's own CPU path (oracle/_ref, the
+unmodified library) on the host cores, one sample session per core.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+GIB = 1 << 30
+MIB = 1 << 20
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--footprint-gib", type=float, default=120.0)
+    ap.add_argument("--region-mib", type=int, default=64)
+    ap.add_argument("--cpu-sample-gib", type=float, default=1.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-incremental", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    return world, rank, local, local_world
+
+
+def pin_device(local: int, world: int) -> None:
+    # one process per GPU: each rank sees exactly its own device as cuda:0,
+    # in both torch's runtime and libcrac_b200's (statically linked) runtime
+    os.environ.setdefault("CUDA_DEVICE_ORDER", "PCI_BUS_ID")
+    if world > 1:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        devs = vis.split(",") if vis else [str(i) for i in range(64)]
+        os.environ["CUDA_VISIBLE_DEVICES"] = devs[local]
+
+
+def mem_available() -> int:
+    for line in Path("/proc/meminfo").read_text().splitlines():
+        if line.startswith("MemAvailable:"):
+            return int(line.split()[1]) * 1024
+    return 64 * GIB
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d.get("hbm_gbs", 6650.0)), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.lines: list[str] = []
+        self.proc = None
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self, gpu_indices=None) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=5)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            if gpu_indices is not None and parts[0] not in gpu_indices:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline (oracle/_ref: the unmodified reference library)
+# ---------------------------------------------------------------------------
+def ref_sample_step(state: dict) -> None:
+    from oracle import ref
+    t0 = time.perf_counter()
+    img, times = state["session"].checkpoint()
+    new, rtimes = ref.ref_restart(img)
+    state["session"].close()
+    state["session"] = new
+    state["elapsed"] = time.perf_counter() - t0
+    state["phases"] = {**times, **rtimes}
+
+
+def ref_make_session(sample_bytes: int, region: int, seed: int):
+    from oracle import ref
+    n = max(1, sample_bytes // region)
+    s = ref.RefSession(seed=seed, arena_bytes=n * region + MIB)
+    for _ in range(n):
+        i, _ = s.alloc(1, region)
+        s.fill_synthetic(i, seed)
+    return s, n * region
+
+
+def cpu_baseline(sample_gib: float, region: int) -> dict:
+    """Single-threaded reference checkpoint+encode / decode+restart (C4 scaled)."""
+    s, live = ref_make_session(int(sample_gib * GIB), region, seed=1)
+    state = {"session": s}
+    ref_sample_step(state)
+    ph = state["phases"]
+    total = ph["checkpoint_s"] + ph["encode_s"] + ph["decode_s"] + ph["restart_s"]
+    state["session"].close()
+    return {"value": round(2 * live / total / 1e9, 4), "unit": "GB/s", "cores": 1,
+            "kind": "reference",
+            "sample": f"C4 scaled to {live // MIB} MiB ({live // region} x {region // MIB} MiB "
+                      f"Device regions): checkpoint()+encode_image() then decode_image()+restart() "
+                      f"of the unmodified reference, single-threaded by construction",
+            "phases_s": {k: round(v, 3) for k, v in ph.items()}}
+
+
+def run_reference(args, world, rank) -> None:
+    if rank != 0:
+        return
+    import concurrent.futures as cf
+    threads = max(1, os.cpu_count() or 1)
+    region = args.region_mib * MIB
+    # ~5x the sample in host RAM per thread (arena + snapshot + image + decode)
+    per = min(int(args.cpu_sample_gib * GIB) // threads or region, mem_available() // (8 * threads))
+    per = max(region, per // region * region)
+    states = []
+    with cf.ThreadPoolExecutor(threads) as ex:
+        made = list(ex.map(lambda t: ref_make_session(per, region, seed=t + 1), range(threads)))
+    states = [{"session": s} for s, _ in made]
+    live = sum(b for _, b in made)
+
+    def step():
+        t0 = time.perf_counter()
+        with cf.ThreadPoolExecutor(threads) as ex:
+            list(ex.map(ref_sample_step, states))
+        return time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    total = sum(times)
+    value = 2 * live * args.steps / total / 1e9
+    line = {
+        "metric": "checkpoint & restart GB/s per GPU and whole box at 1/2/4/8 B200; % of roofline",
+        "impl": "reference", "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * total / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "C4 full checkpoint + restart (reference CPU path, scaled sample)",
+                   "live_bytes_per_step": live, "region_bytes": region, "threads": threads},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"{threads} independent reference sessions x {per // MIB} MiB "
+                                   f"({per // region} x {region // MIB} MiB regions), each step "
+                                   f"checkpoint+encode+decode+restart on every thread"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    for st in states:
+        st["session"].close()
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the B200 arm
+# ---------------------------------------------------------------------------
+def main() -> None:
+    args = parse_args()
+    world, rank, local, local_world = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    pin_device(local, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2008_10596_b200 import engine
+
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    torch.cuda.set_device(0)
+    region = args.region_mib * MIB
+    # host RAM bounds the per-rank image; HBM bounds the per-rank state
+    host_cap = int(0.80 * mem_available() / local_world) - 8 * GIB
+    dev_cap = int(torch.cuda.get_device_properties(0).total_memory * 0.85)
+    footprint = min(int(args.footprint_gib * GIB), host_cap, dev_cap) // region * region
+    n_regions = footprint // region
+    live = n_regions * region
+
+    t_setup = time.perf_counter()
+    sess = engine.Session(seed=rank + 1, arena_bytes=live + 64 * MIB)
+    for _ in range(n_regions):
+        i, _ = sess.alloc(engine.DEVICE, region)
+        sess.fill_synthetic(i, rank + 1)
+    image = engine.Image()
+    setup_s = time.perf_counter() - t_setup
+
+    def step(s):
+        dr = s.checkpoint_into(image)
+        addr, n = image.address()
+        s.close()
+        s2, rf = engine.restart_from_address(addr, n)
+        return s2, dr, rf
+
+    t_warm = time.perf_counter()
+    for _ in range(args.warmup):
+        sess, _, _ = step(sess)
+    warm_s = time.perf_counter() - t_warm
+
+    clocks = ClockSampler() if rank == 0 else None
+    if clocks:
+        clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    wall0 = time.perf_counter()
+    drains, refills = [], []
+    for _ in range(args.steps):
+        sess, dr, rf = step(sess)
+        drains.append(dr)
+        refills.append(rf)
+    ev1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    barrier()
+    e2e_ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop() if clocks else None
+
+    dev_ms = sum(d["total_ms"] for d in drains) + sum(r["total_ms"] for r in refills)
+    dev_ms_max = max_over_ranks(dev_ms)
+    e2e_ms_max = max_over_ranks(e2e_ms)
+    drain_ms = max_over_ranks(sum(d["total_ms"] for d in drains) / args.steps)
+    refill_ms = max_over_ranks(sum(r["total_ms"] for r in refills) / args.steps)
+
+    # kernel roofline: the kernel with the largest device time in the step
+    peaks = measured_peaks()
+    hbm = peaks["hbm_gbs"]
+    k1_ms = statistics.mean(d["hash_ms"] for d in drains)          # one payload launch
+    k1_bytes = drains[-1]["hash_bytes"] / max(drains[-1]["hash_launches"], 1)
+    pack_launches = drains[-1]["pack_launches"]
+    pack_ms_per = statistics.mean(d["pack_ms"] for d in drains) / max(pack_launches, 1)
+    pack_bytes = 2 * drains[-1]["pack_bytes"] / max(pack_launches, 1)   # read + write
+    scat_launches = refills[-1]["pack_launches"]
+    scat_ms_per = statistics.mean(r["pack_ms"] for r in refills) / max(scat_launches, 1)
+    scat_bytes = 2 * refills[-1]["pack_bytes"] / max(scat_launches, 1)
+    kernels = {
+        "k1_chunk_crc (drain)": (k1_ms, k1_bytes, 1),
+        "k_pack_records": (pack_ms_per, pack_bytes, pack_launches),
+        "k_scatter_records": (scat_ms_per, scat_bytes, scat_launches),
+    }
+    dom = max(kernels, key=lambda k: kernels[k][0] * kernels[k][2])
+    dom_ms, dom_bytes, _ = kernels[dom]
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
+
+    # incremental (C5 shape on the resident state): hash-only and 1 % dirty drain
+    incremental = None
+    if not args.no_incremental:
+        h = sess.hash_only()
+        sess.checkpoint_into(image)  # seeds the previous-image chunk CRCs
+        thr = (2**64 - 1) // 100
+        mutated = sess.mutate(seed=rank + 1, epoch=1, threshold=thr)
+        inc = sess.checkpoint_into(image, incremental=True)
+        k1_gbs = h["hash_bytes"] / (h["hash_ms"] * 1e-3) / 1e9 if h["hash_ms"] else 0
+        incremental = {
+            "hash_only": {"bytes": h["hash_bytes"], "ms": round(h["hash_ms"], 3),
+                          "GBps": round(k1_gbs, 1), "frac_of_hbm": round(k1_gbs / hbm, 3)},
+            "drain_1pct": {"dirty_chunks": inc["dirty_chunks"], "mutated": mutated,
+                           "total_chunks": inc["total_chunks"], "ms": round(inc["total_ms"], 3),
+                           "d2h_bytes": inc["d2h_bytes"], "incremental": bool(inc["incremental"])},
+        }
+
+    # reported CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.cpu_sample_gib, region)
+
+    if rank == 0:
+        value = 2 * live * world * args.steps / (dev_ms_max * 1e-3) / 1e9
+        e2e = 2 * live * world * args.steps / (e2e_ms_max * 1e-3) / 1e9
+        launches = sum(d["hash_launches"] + d["pack_launches"] for d in drains) + \
+            sum(r["hash_launches"] + r["pack_launches"] for r in refills)
+        line = {
+            "metric": "checkpoint & restart GB/s per GPU and whole box at 1/2/4/8 B200; % of roofline",
+            "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(dev_ms_max / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic",
+            "config": {"workload": "C4: full checkpoint drain + restart refill of live device "
+                                   "state, independent per-GPU drains, host barrier",
+                       "live_bytes_per_gpu": live, "regions_per_gpu": n_regions,
+                       "region_bytes": region, "requested_footprint_gib": args.footprint_gib,
+                       "parallelism": f"independent drains x{world}",
+                       "l2": "inputs larger than L2 (live state >> 126 MB)"},
+            "per_gpu": {"checkpoint_GBps": round(live / (drain_ms * 1e-3) / 1e9, 3),
+                        "restart_GBps": round(live / (refill_ms * 1e-3) / 1e9, 3),
+                        "checkpoint_ms": round(drain_ms, 3), "restart_ms": round(refill_ms, 3),
+                        "image_bytes": drains[-1]["image_bytes"]},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+                         "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                         "traffic": None, "peak_source": peaks["source"],
+                         "algorithmic_bytes_per_launch": int(dom_bytes),
+                         "avg_launch_ms": round(dom_ms, 4)},
+            "pcie_roofline": {"d2h_GBps": round(drains[-1]["d2h_bytes"] / (statistics.mean(d["copy_ms"] for d in drains) * 1e-3) / 1e9, 2),
+                              "h2d_GBps": round(refills[-1]["h2d_bytes"] / (statistics.mean(r["copy_ms"] for r in refills) * 1e-3) / 1e9, 2)},
+            "e2e": {"value": round(e2e, 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": refills[-1]["h2d_bytes"],
+                    "d2h_bytes_per_step": drains[-1]["d2h_bytes"],
+                    "wall_s": round(wall, 3)},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "incremental": incremental,
+            "cpu_baseline": cpu,
+            "setup_s": round(setup_s, 1), "warmup_s": round(warm_s, 1),
+        }
+        print(json.dumps(line), flush=True)
+    sess.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

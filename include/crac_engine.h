@@ -106,6 +106,10 @@ int crac_fill_synthetic(crac_session_t* s, uint64_t id, uint64_t seed, uint8_t m
 int crac_mutate_device(crac_session_t* s, uint64_t seed, uint64_t epoch, uint64_t threshold,
                        uint64_t* mutated_chunks);
 
+/* Hash-only pass (C5 "hash-only"): K1 over every live allocation of the
+ * session, chunk CRCs left on the device; stats.hash_ms / hash_bytes. */
+int crac_hash_session(crac_session_t* s, crac_stats_t* stats);
+
 /* Kernel-level entry for parity tests: CRC of every 64 KiB (chunk_bytes)
  * chunk of a host buffer, computed by K1 on the GPU. */
 int crac_hash_host_buffer(const void* data, uint64_t n, uint32_t chunk_bytes, uint32_t* crc_out);

@@ -124,6 +124,8 @@ Session restart_from_file(const std::filesystem::path& path, const KernelCatalog
 // ---- B200 fast path ----
 void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats = nullptr);
 void checkpoint_incremental(Session& session, PinnedImage& image, DrainStats* stats = nullptr);
+// K1 over every live allocation (hash-only timing; no drain).
+void hash_only(Session& session, DrainStats* stats);
 Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catalog,
                       TableMode mode = TableMode::Direct,
                       std::chrono::milliseconds quiesce_timeout = std::chrono::milliseconds{30000},

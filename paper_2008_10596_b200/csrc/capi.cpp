@@ -363,6 +363,14 @@ int crac_mutate_device(crac_session_t* s, uint64_t seed, uint64_t epoch, uint64_
   });
 }
 
+int crac_hash_session(crac_session_t* s, crac_stats_t* stats) {
+  return guard([&] {
+    DrainStats d;
+    hash_only(s->s, &d);
+    to_c(d, stats);
+  });
+}
+
 int crac_hash_host_buffer(const void* data, uint64_t n, uint32_t chunk_bytes, uint32_t* crc_out) {
   return guard([&] {
     if (n == 0) return;

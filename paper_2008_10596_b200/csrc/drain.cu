@@ -565,6 +565,28 @@ void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
   }
 }
 
+void hash_only(Session& session, DrainStats* stats) {
+  QuiesceScope q(session.table(), session.config().quiesce_timeout);
+  DeviceContext& ctx = session.device();
+  DrainEngine& E = session.drain_engine();
+  if (stats) *stats = DrainStats{};
+  std::vector<BulkItem> items;
+  for (const AllocationRecord& rec : active_set(session.log().snapshot()))
+    items.push_back(BulkItem{rec.id, rec.kind, rec.size, ctx.backing_ptr(rec.id), nullptr});
+  ImagePlan P;
+  build_plan(items, P);
+  upload_plan(E, P, E.s_hash);
+  launch_hash(E, P, E.s_hash, stats);
+  check_cuda(cudaStreamSynchronize(E.s_hash), "hash sync");
+  if (stats) {
+    StreamTimer t;
+    stats->hash_ms = t.ms(E.ev_h0, E.ev_h1);
+    stats->total_ms = stats->hash_ms;
+    stats->total_chunks = P.pay_first.back() + P.page_first.back();
+  }
+  E.plan.valid = false;  // the device tables now describe this pass, not an image
+}
+
 // ---------------------------------------------------------------------------
 // refill
 // ---------------------------------------------------------------------------
@@ -598,7 +620,24 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   }
 
   std::set<uint64_t> live;
-  for (const AllocationRecord& r : p.facts.active) live.insert(r.id);
+  {
+    // map every live Device extent up front, coalescing neighbours, so the
+    // replay does no per-allocation driver calls
+    uint64_t run_lo = 0, run_hi = 0;
+    for (const AllocationRecord& r : p.facts.active) {
+      live.insert(r.id);
+      if (r.kind != AllocationKind::Device) continue;
+      const uint64_t lo = r.address, hi = r.address + round_up_align(r.size);
+      if (run_hi && lo <= run_hi + (2ull << 20)) {
+        run_hi = std::max(run_hi, hi);
+      } else {
+        if (run_hi) ctx.premap(run_lo, run_hi - run_lo);
+        run_lo = lo;
+        run_hi = hi;
+      }
+    }
+    if (run_hi) ctx.premap(run_lo, run_hi - run_lo);
+  }
   ctx.begin_replay(std::move(live));
   try {
     replay_log(ctx, p.log, &binaries);

@@ -90,6 +90,7 @@ _SIGS = {
     "crac_fill_synthetic": (C.c_int, [_P, _U64, _U64, _U8]),
     "crac_mutate_device": (C.c_int, [_P, _U64, _U64, _U64, _PU64]),
     "crac_hash_host_buffer": (C.c_int, [_P, _U64, _U32, _PU32]),
+    "crac_hash_session": (C.c_int, [_P, C.POINTER(Stats)]),
     # kernel-level C-ABI (crac_gpu.h)
     "crac_gpu_init": (C.c_int, []),
     "crac_chunk_crc32": (C.c_int, [_P, _P, _U32, _U32, _U64, _P, _P]),
@@ -335,6 +336,11 @@ class Session:
         n = C.c_uint64()
         _check(lib().crac_mutate_device(self._h, seed, epoch, threshold, C.byref(n)))
         return n.value
+
+    def hash_only(self) -> dict:
+        st = Stats()
+        _check(lib().crac_hash_session(self._h, C.byref(st)))
+        return st.as_dict()
 
     def close(self) -> None:
         if getattr(self, "_h", None):
