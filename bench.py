@@ -142,6 +142,39 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+class HostGroup:
+    """The only cross-rank exchange of the path: a host barrier marking the
+    consistent global checkpoint, plus the max-over-ranks of the timings
+    (gloo on CPU tensors; no data-path collective exists)."""
+
+    def __init__(self, world: int, rank: int):
+        self.world = world
+        if world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29511")
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def barrier(self) -> None:
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self) -> None:
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------------------
 # reference arm / cpu baseline (oracle/_ref: the unmodified reference library)
 # ---------------------------------------------------------------------------
@@ -244,20 +277,8 @@ def main() -> None:
     import torch.distributed as dist
     from paper_2008_10596_b200 import engine
 
-    if world > 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("gloo", rank=rank, world_size=world)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    group = HostGroup(world, rank)
+    barrier, max_over_ranks = group.barrier, group.max
 
     torch.cuda.set_device(0)
     region = args.region_mib * MIB
@@ -396,8 +417,7 @@ def main() -> None:
         }
         print(json.dumps(line), flush=True)
     sess.close()
-    if world > 1:
-        dist.destroy_process_group()
+    group.close()
 
 
 if __name__ == "__main__":

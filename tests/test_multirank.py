@@ -1,0 +1,58 @@
+"""CPU tier: the N>1 host logic of bench.py on gloo, world_size 2.
+
+The path has no data-path collective (independent per-GPU drains); the only
+exchange is the host barrier and the max-over-ranks timing, tested here.
+"""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank: int, world: int, port: int, q) -> None:
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import bench
+    g = bench.HostGroup(world, rank)
+    g.barrier()
+    m = g.max(float(10 + rank * 5))
+    # per-rank device pinning: each rank sees only its LOCAL_RANK device
+    os.environ.pop("CUDA_VISIBLE_DEVICES", None)
+    bench.pin_device(rank, world)
+    q.put((rank, m, os.environ["CUDA_VISIBLE_DEVICES"]))
+    g.close()
+
+
+def test_host_barrier_and_max_over_ranks():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    got = sorted(q.get(timeout=5) for _ in range(2))
+    assert got == [(0, 15.0, "0"), (1, 15.0, "1")]
+
+
+def test_reference_arm_nonzero_ranks_exit_without_work(capsys):
+    import bench
+
+    class A:
+        impl = "reference"
+        steps = 1
+        warmup = 0
+        region_mib = 64
+        cpu_sample_gib = 0.0625
+
+    bench.run_reference(A, world=2, rank=1)
+    assert capsys.readouterr().out == ""
