@@ -64,6 +64,21 @@ int crac_gpu_init(void);
 int crac_chunk_crc32(const crac_span_t* d_spans, const uint64_t* d_chunk_first, uint32_t n_spans,
                      uint32_t chunk_bytes, uint64_t total_chunks, uint32_t* d_crc, void* stream);
 
+/* K1 over the absolute chunk range [c_lo, c_hi) of the same span table,
+ * writing d_crc[c]; at most max_ctas CTAs (0 = one per SM) so the kernel can
+ * leave SMs to work running beside it. */
+int crac_chunk_crc32_range(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
+                           uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
+                           uint32_t* d_crc, uint32_t max_ctas, void* stream);
+
+/* Incremental drain straight to the host image: dirty chunk k (index
+ * d_dirty_idx[first + k]) of payload span s is written by the SMs to
+ * host_image + d_dst_off[s] + chunk offset (pinned, UVA-mapped memory). */
+int crac_gather_chunks_to_host(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
+                               uint32_t n_spans, uint32_t chunk_bytes,
+                               const uint64_t* d_dirty_idx, uint64_t first, uint64_t count,
+                               const uint64_t* d_dst_off, uint8_t* host_image, void* stream);
+
 /* K2a: writes stream bytes [win_off, win_off + win_len) into d_out (16-byte
  * aligned; win_off multiple of 16).  Records sorted by out_off; bytes not
  * covered by any record are written as zero.  d_tile_rec[t] = first record

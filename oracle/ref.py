@@ -143,9 +143,9 @@ def chunk_crc32_ptr(addr: int, n: int, chunk: int, out_addr: int, threads: int) 
                                     threads)
 
 
-def synth_bytes(seed: int, alloc_id: int, size: int) -> bytes:
+def synth_bytes(seed: int, alloc_id: int, size: int, word_offset: int = 0) -> bytes:
     out = C.create_string_buffer(max(size, 1))
-    oracle_lib().oracle_synth_bytes(seed, alloc_id, 0, size, out)
+    oracle_lib().oracle_synth_bytes(seed, alloc_id, word_offset, size, out)
     return out.raw[:size]
 
 

@@ -15,13 +15,13 @@ Session::Session(const SessionConfig& cfg)
       table_(std::make_unique<DispatchTable>(*ctx_, *log_, *regions_, cfg.mode)) {}
 
 Session::~Session() {
-  drain_.reset();  // engine buffers go before the device context
+  release_engine(std::move(drain_));  // pooled for the next session on this device
 }
 Session::Session(Session&&) noexcept = default;
 Session& Session::operator=(Session&&) noexcept = default;
 
 DrainEngine& Session::drain_engine() {
-  if (!drain_) drain_ = std::make_unique<DrainEngine>(ctx_->device());
+  if (!drain_) drain_ = acquire_engine(ctx_->device());
   return *drain_;
 }
 

@@ -4,32 +4,69 @@
 //         encode_image; the read_raw copies at ckpt_engine.cpp:49,54):
 //   host  : quiesce, small sections (META/LOG/STREAMS/APPSTATE/REGISTRY),
 //           record table of the bulk stream ALLOC_PAYLOADS||crc3||hdr4||UVM_PAGES
-//   GPU   : s_hash  K1 over every payload (64 KiB chunks) and managed page
+//   GPU   : s_hash  K1 over every payload (64 KiB chunks) and managed page,
+//                   on all but kPackSMs SMs so the pack never waits for it
 //           s_pack  pack kernel builds the exact stream bytes window by window
-//                   into an 8 x 16 MiB staging ring
+//                   into an 8 x 16 MiB staging ring (about L2-sized)
 //           s_copy  D2H of each window into the pinned image (4 KiB aligned)
 //   host  : folds chunk CRCs with the frame CRCs into the section CRCs while
 //           the D2H drains, then patches crc3/crc4.
 // Refill (replaces ref: src/image.cpp:280-345 decode + src/ckpt_engine.cpp:120-171):
 //   host  : strict parse of the framing, replay of the log (real backing only
-//           for allocations live at the end), record table with destinations
+//           for allocations live at the end, pre-mapped in coalesced runs)
 //   GPU   : s_copy H2D windows (+16 B look-ahead) -> ring; s_pack scatter kernel
-//           writes every destination word (padding zero-filled); K1 over the
-//           refilled regions; managed residence via cudaMemPrefetchAsync
+//           writes every destination word (padding zero-filled), then K1
+//           re-hashes each region as soon as its last window has landed;
+//           managed residence via cudaMemPrefetchAsync
 //   host  : fold + compare against the stored CRCs -> ImageCorrupt on mismatch.
+// Incremental drain (new; the reference has none):
+//   K1 -> diff against the previous image's chunk CRCs -> ordered compaction
+//   -> the SMs write every dirty chunk straight into the pinned image.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <set>
 #include <thread>
+
+#include <sys/mman.h>
 
 #include "crc_math.hpp"
 #include "drain_engine.hpp"
 #include "image_codec.hpp"
 
 namespace cracsim {
+
+// ---------------------------------------------------------------------------
+// tracing
+// ---------------------------------------------------------------------------
+namespace {
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+bool trace_on() {
+  static const bool on = std::getenv("CRAC_TRACE") != nullptr;
+  return on;
+}
+}  // namespace
+
+PhaseTrace::PhaseTrace(const char* name) : op(name), t0(now_ms()), last(t0), on(trace_on()) {}
+void PhaseTrace::mark(const char* phase) {
+  if (!on) return;
+  const double t = now_ms();
+  std::fprintf(stderr, "[crac] %s %-14s %9.3f ms\n", op, phase, t - last);
+  last = t;
+}
+PhaseTrace::~PhaseTrace() {
+  if (on) std::fprintf(stderr, "[crac] %s %-14s %9.3f ms\n", op, "TOTAL", now_ms() - t0);
+}
 
 // ---------------------------------------------------------------------------
 // buffers
@@ -73,11 +110,10 @@ DrainEngine::DrainEngine(int dev) : device(dev) {
   for (int i = 0; i < kSlots; ++i) {
     check_cuda(cudaEventCreateWithFlags(&ev_ready[i], cudaEventDisableTiming), "event");
     check_cuda(cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming), "event");
-    check_cuda(cudaEventCreate(&ev_p0[i]), "event");
-    check_cuda(cudaEventCreate(&ev_p1[i]), "event");
   }
   for (cudaEvent_t* e : {&ev_t0, &ev_t1, &ev_h0, &ev_h1, &ev_c0, &ev_c1})
     check_cuda(cudaEventCreate(e), "event");
+  check_cuda(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev), "sm count");
   check_cuda(cudaMalloc(&d_ring, kSlots * (kWindow + 64)), "staging ring");
   if (int rc = crac_gpu_init()) check_cuda(cudaError_t(rc), "crac_gpu_init");
 }
@@ -87,9 +123,9 @@ DrainEngine::~DrainEngine() {
   for (int i = 0; i < kSlots; ++i) {
     cudaEventDestroy(ev_ready[i]);
     cudaEventDestroy(ev_free[i]);
-    cudaEventDestroy(ev_p0[i]);
-    cudaEventDestroy(ev_p1[i]);
   }
+  for (cudaEvent_t e : ev_w0) cudaEventDestroy(e);
+  for (cudaEvent_t e : ev_w1) cudaEventDestroy(e);
   for (cudaEvent_t e : {ev_t0, ev_t1, ev_h0, ev_h1, ev_c0, ev_c1}) cudaEventDestroy(e);
   cudaFree(d_ring);
   d_recs.release();
@@ -98,7 +134,7 @@ DrainEngine::~DrainEngine() {
   d_page_spans.release();
   d_pay_first.release();
   d_page_first.release();
-  d_pay_ids.release();
+  d_pay_dst.release();
   d_pay_crc.release();
   d_page_crc.release();
   d_prev_crc.release();
@@ -107,20 +143,95 @@ DrainEngine::~DrainEngine() {
   d_dirty_count.release();
   h_pay_crc.release();
   h_page_crc.release();
-  h_dirty_idx.release();
   h_count.release();
-  h_ring.release();
+  h_dirty_idx.release();
   cudaStreamDestroy(s_pack);
   cudaStreamDestroy(s_copy);
   cudaStreamDestroy(s_hash);
 }
 
+void DrainEngine::ensure_window_events(size_t n) {
+  while (ev_w0.size() < n) {
+    cudaEvent_t a, b;
+    check_cuda(cudaEventCreate(&a), "event");
+    check_cuda(cudaEventCreate(&b), "event");
+    ev_w0.push_back(a);
+    ev_w1.push_back(b);
+  }
+}
+
+// Engines (streams, events, staging ring, device tables) outlive sessions:
+// a restart reuses the engine of the session it replaces, so no timed step
+// pays for cudaMalloc / stream creation.  Deliberately never freed at exit.
+namespace {
+std::mutex g_pool_mu;
+std::vector<DrainEngine*>* g_pool = new std::vector<DrainEngine*>();
+}  // namespace
+
+std::unique_ptr<DrainEngine> acquire_engine(int device) {
+  {
+    std::lock_guard lk(g_pool_mu);
+    for (auto it = g_pool->begin(); it != g_pool->end(); ++it)
+      if ((*it)->device == device) {
+        DrainEngine* e = *it;
+        g_pool->erase(it);
+        return std::unique_ptr<DrainEngine>(e);
+      }
+  }
+  return std::make_unique<DrainEngine>(device);
+}
+
+void release_engine(std::unique_ptr<DrainEngine> e) {
+  if (!e) return;
+  if (cudaStreamSynchronize(e->s_pack) != cudaSuccess ||
+      cudaStreamSynchronize(e->s_copy) != cudaSuccess ||
+      cudaStreamSynchronize(e->s_hash) != cudaSuccess)
+    return;  // a broken engine is dropped (and leaked), never pooled
+  e->plan = ImagePlan{};
+  e->prev_valid = false;
+  e->dst_for_image = 0;
+  std::lock_guard lk(g_pool_mu);
+  if (g_pool->size() < 4) g_pool->push_back(e.release());
+}
+
 // ---------------------------------------------------------------------------
 // pinned image
 // ---------------------------------------------------------------------------
-PinnedImage::~PinnedImage() {
-  if (base_) cudaFreeHost(base_);
+// Page-locked host memory for images.  cudaHostAlloc faults and pins 4 KiB
+// pages one by one (~2.3 GB/s measured on the B200 box); instead map
+// anonymous memory with transparent huge pages, first-touch it from all
+// cores, then register it with the driver (~28 GB/s measured, and the same
+// 55.9 GB/s D2H into it).
+namespace {
+uint8_t* pinned_alloc(uint64_t bytes) {
+  void* m = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE,
+                 -1, 0);
+  if (m == MAP_FAILED) raise(Errc::DeviceFault, "mmap of the image buffer failed");
+  madvise(m, bytes, MADV_HUGEPAGE);
+  const unsigned threads = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < threads; ++t)
+    pool.emplace_back([=] {
+      const uint64_t a = bytes * t / threads / 4096 * 4096, b = bytes * (t + 1) / threads;
+      for (uint64_t o = a; o < b; o += 4096) static_cast<volatile uint8_t*>(m)[o] = 0;
+    });
+  for (auto& th : pool) th.join();
+  const cudaError_t e = cudaHostRegister(m, bytes, cudaHostRegisterDefault);
+  if (e != cudaSuccess) {
+    munmap(m, bytes);
+    check_cuda(e, "cudaHostRegister image");
+  }
+  return static_cast<uint8_t*>(m);
 }
+
+void pinned_free(uint8_t* p, uint64_t bytes) {
+  if (!p) return;
+  cudaHostUnregister(p);
+  munmap(p, bytes);
+}
+}  // namespace
+
+PinnedImage::~PinnedImage() { pinned_free(base_, cap_); }
 PinnedImage::PinnedImage(PinnedImage&& o) noexcept
     : base_(o.base_), cap_(o.cap_), off_(o.off_), size_(o.size_) {
   o.base_ = nullptr;
@@ -128,7 +239,7 @@ PinnedImage::PinnedImage(PinnedImage&& o) noexcept
 }
 PinnedImage& PinnedImage::operator=(PinnedImage&& o) noexcept {
   if (this != &o) {
-    if (base_) cudaFreeHost(base_);
+    pinned_free(base_, cap_);
     base_ = o.base_;
     cap_ = o.cap_;
     off_ = o.off_;
@@ -140,13 +251,12 @@ PinnedImage& PinnedImage::operator=(PinnedImage&& o) noexcept {
 }
 
 void PinnedImage::prepare(uint64_t size, uint64_t align_at) {
-  const uint64_t need = size + 4096;
+  const uint64_t need = (size + 4096 + (2ull << 20) - 1) / (2ull << 20) * (2ull << 20);
   if (need > cap_) {
-    if (base_) cudaFreeHost(base_);
+    pinned_free(base_, cap_);
     base_ = nullptr;
     cap_ = 0;
-    check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&base_), need, cudaHostAllocDefault),
-               "cudaHostAlloc image");
+    base_ = pinned_alloc(need);
     cap_ = need;
   }
   const uint64_t b = reinterpret_cast<uint64_t>(base_);
@@ -171,7 +281,7 @@ const uint32_t* pow2_table() {
   return t.data();
 }
 
-// Multiplication by x^(8n) mod P as four byte tables (linear map).
+// Multiplication by x^(8n) mod P as four byte tables (a linear map).
 struct Shift {
   uint32_t t[4][256];
   explicit Shift(uint64_t n) {
@@ -199,33 +309,24 @@ struct Fold {
   }
 };
 
-// Runs fn(0..n-1) on up to 8 host threads (image patching).
-template <typename Fn>
-void parallel_for(uint64_t n, Fn&& fn) {
-  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
-  const uint64_t workers = std::min<uint64_t>(hw, (n + 15) / 16);
-  if (workers <= 1) {
-    for (uint64_t i = 0; i < n; ++i) fn(i);
-    return;
-  }
-  std::vector<std::thread> pool;
-  for (uint64_t t = 0; t < workers; ++t)
-    pool.emplace_back([&, t] {
-      for (uint64_t i = n * t / workers; i < n * (t + 1) / workers; ++i) fn(i);
-    });
-  for (auto& th : pool) th.join();
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float v = 0;
+  cudaEventElapsedTime(&v, a, b);
+  return v;
 }
 
-struct StreamTimer {
-  float ms(cudaEvent_t a, cudaEvent_t b) {
-    float v = 0;
-    cudaEventElapsedTime(&v, a, b);
-    return v;
-  }
-};
+// Median duration of the first n window kernels (robust to the windows that
+// ran beside K1 at the start of a drain).
+double median_window_ms(DrainEngine& E, size_t n) {
+  std::vector<float> v;
+  for (size_t i = 0; i < n; ++i) v.push_back(elapsed(E.ev_w0[i], E.ev_w1[i]));
+  if (v.empty()) return 0;
+  std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
+  return v[v.size() / 2];
+}
 
-// Bulk-stream plan shared by drain and refill.  `dest` = device pointers of
-// the regions (drain: sources; refill: destinations).
+// Bulk-stream plan shared by drain and refill.  `ptr` = device-visible
+// address of the region (drain: source; refill: destination).
 struct BulkItem {
   uint64_t id = 0;
   AllocationKind kind = AllocationKind::Device;
@@ -240,7 +341,6 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
   P.page_spans.clear();
   P.pay_first.assign(1, 0);
   P.page_first.assign(1, 0);
-  P.pay_ids.clear();
   P.pay_rec_off.clear();
   P.log_sizes.clear();
   uint64_t pos = 0, len4 = 0;
@@ -261,8 +361,8 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
     std::memcpy(r.frame + 8, &it.size, 8);
     P.recs.push_back(r);
     P.pay_spans.push_back(crac_span_t{it.ptr, it.size});
-    P.pay_first.push_back(P.pay_first.back() + (it.size + DrainEngine::kChunk - 1) / DrainEngine::kChunk);
-    P.pay_ids.push_back(it.id);
+    P.pay_first.push_back(P.pay_first.back() +
+                          (it.size + DrainEngine::kChunk - 1) / DrainEngine::kChunk);
     P.pay_rec_off.push_back(pos + 16);
     pos += 16 + it.size;
   }
@@ -320,42 +420,47 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
   }
 }
 
-void upload_plan(DrainEngine& E, const ImagePlan& P, cudaStream_t st) {
-  auto up = [&](auto& dev, const auto& host) {
-    if (host.empty()) return;
-    dev.ensure(host.size());
-    check_cuda(cudaMemcpyAsync(dev.ptr, host.data(), host.size() * sizeof(host[0]),
-                               cudaMemcpyHostToDevice, st),
-               "plan upload");
-  };
-  up(E.d_recs, P.recs);
-  up(E.d_tile_rec, P.tile_rec);
-  up(E.d_pay_spans, P.pay_spans);
-  up(E.d_pay_first, P.pay_first);
-  up(E.d_page_spans, P.page_spans);
-  up(E.d_page_first, P.page_first);
-  up(E.d_pay_ids, P.pay_ids);
+template <typename D, typename H>
+void upload(D& dev, const H& host, cudaStream_t st) {
+  if (host.empty()) return;
+  dev.ensure(host.size());
+  check_cuda(cudaMemcpyAsync(dev.ptr, host.data(), host.size() * sizeof(host[0]),
+                             cudaMemcpyHostToDevice, st),
+             "plan upload");
 }
 
-// K1 over every payload and managed region; CRCs land in h_*_crc.
-void launch_hash(DrainEngine& E, const ImagePlan& P, cudaStream_t st, DrainStats* stats) {
+void upload_plan(DrainEngine& E, const ImagePlan& P, cudaStream_t st) {
+  upload(E.d_recs, P.recs, st);
+  upload(E.d_tile_rec, P.tile_rec, st);
+  upload(E.d_pay_spans, P.pay_spans, st);
+  upload(E.d_pay_first, P.pay_first, st);
+  upload(E.d_page_spans, P.page_spans, st);
+  upload(E.d_page_first, P.page_first, st);
   const uint64_t n_pay = P.pay_first.back(), n_page = P.page_first.back();
   E.d_pay_crc.ensure(std::max<uint64_t>(n_pay, 1));
   E.d_page_crc.ensure(std::max<uint64_t>(n_page, 1));
   E.h_pay_crc.ensure(std::max<uint64_t>(n_pay, 1));
   E.h_page_crc.ensure(std::max<uint64_t>(n_page, 1));
-  check_cuda(cudaEventRecord(E.ev_h0, st), "event");
-  if (n_pay)
-    check_cuda(cudaError_t(crac_chunk_crc32(E.d_pay_spans.ptr, E.d_pay_first.ptr,
-                                            uint32_t(P.pay_spans.size()), DrainEngine::kChunk,
-                                            n_pay, E.d_pay_crc.ptr, st)),
-               "K1 payloads");
-  if (n_page)
-    check_cuda(cudaError_t(crac_chunk_crc32(E.d_page_spans.ptr, E.d_page_first.ptr,
-                                            uint32_t(P.page_spans.size()), DrainEngine::kPageChunk,
-                                            n_page, E.d_page_crc.ptr, st)),
-               "K1 pages");
-  check_cuda(cudaEventRecord(E.ev_h1, st), "event");
+}
+
+void hash_payloads(DrainEngine& E, const ImagePlan& P, uint64_t c_lo, uint64_t c_hi,
+                   uint32_t max_ctas, cudaStream_t st) {
+  check_cuda(cudaError_t(crac_chunk_crc32_range(E.d_pay_spans.ptr, E.d_pay_first.ptr,
+                                                uint32_t(P.pay_spans.size()), DrainEngine::kChunk,
+                                                c_lo, c_hi, E.d_pay_crc.ptr, max_ctas, st)),
+             "K1 payloads");
+}
+
+void hash_pages(DrainEngine& E, const ImagePlan& P, uint32_t max_ctas, cudaStream_t st) {
+  check_cuda(cudaError_t(crac_chunk_crc32_range(E.d_page_spans.ptr, E.d_page_first.ptr,
+                                                uint32_t(P.page_spans.size()),
+                                                DrainEngine::kPageChunk, 0, P.page_first.back(),
+                                                E.d_page_crc.ptr, max_ctas, st)),
+             "K1 pages");
+}
+
+void download_crcs(DrainEngine& E, const ImagePlan& P, cudaStream_t st) {
+  const uint64_t n_pay = P.pay_first.back(), n_page = P.page_first.back();
   if (n_pay)
     check_cuda(cudaMemcpyAsync(E.h_pay_crc.ptr, E.d_pay_crc.ptr, n_pay * 4, cudaMemcpyDeviceToHost, st),
                "crc download");
@@ -363,15 +468,24 @@ void launch_hash(DrainEngine& E, const ImagePlan& P, cudaStream_t st, DrainStats
     check_cuda(cudaMemcpyAsync(E.h_page_crc.ptr, E.d_page_crc.ptr, n_page * 4,
                                cudaMemcpyDeviceToHost, st),
                "crc download");
-  if (stats) {
-    stats->hash_launches += (n_pay ? 1 : 0) + (n_page ? 1 : 0);
-    for (const auto& s : P.pay_spans) stats->hash_bytes += s.len;
-    for (const auto& s : P.page_spans) stats->hash_bytes += s.len;
-  }
 }
 
-// Section CRCs from chunk CRCs + frames.  `frame_at(out_off)` returns the 16
-// frame bytes of the record at that stream offset.
+uint64_t hashed_bytes(const ImagePlan& P) {
+  uint64_t b = 0;
+  for (const auto& s : P.pay_spans) b += s.len;
+  for (const auto& s : P.page_spans) b += s.len;
+  return b;
+}
+
+// Bytes of payload chunk c (all 64 KiB except a region's tail chunk).
+uint64_t chunk_len(const ImagePlan& P, uint64_t c) {
+  const size_t s = size_t(std::upper_bound(P.pay_first.begin(), P.pay_first.end(), c) -
+                          P.pay_first.begin() - 1);
+  const uint64_t off = (c - P.pay_first[s]) * DrainEngine::kChunk;
+  return std::min<uint64_t>(DrainEngine::kChunk, P.pay_spans[s].len - off);
+}
+
+// Section CRCs from chunk CRCs and the frame bytes of every record.
 void fold_sections(const DrainEngine& E, const ImagePlan& P, uint32_t& crc3, uint32_t& crc4) {
   Fold f3;
   size_t span = 0;
@@ -379,10 +493,9 @@ void fold_sections(const DrainEngine& E, const ImagePlan& P, uint32_t& crc3, uin
     if (r.out_off >= P.len3) break;
     f3.add(crc32_host(r.frame, 16), 16);
     const uint64_t c0 = P.pay_first[span], c1 = P.pay_first[span + 1];
-    for (uint64_t c = c0; c < c1; ++c) {
-      const uint64_t len = std::min<uint64_t>(DrainEngine::kChunk, r.len - (c - c0) * DrainEngine::kChunk);
-      f3.add(E.h_pay_crc.ptr[c], len);
-    }
+    for (uint64_t c = c0; c < c1; ++c)
+      f3.add(E.h_pay_crc.ptr[c],
+             std::min<uint64_t>(DrainEngine::kChunk, r.len - (c - c0) * DrainEngine::kChunk));
     ++span;
   }
   crc3 = f3.acc;
@@ -401,8 +514,7 @@ void put_at(uint8_t* p, T v) {
   std::memcpy(p, &v, sizeof(T));
 }
 
-// Writes one complete small section (header, payload, crc) at `p`; returns
-// the byte count.
+// Writes one complete small section (header, payload, crc) at `p`.
 uint64_t write_section(uint8_t* p, uint32_t tag, const std::vector<uint8_t>& payload) {
   put_at<uint32_t>(p, tag);
   put_at<uint32_t>(p + 4, 0);
@@ -418,13 +530,41 @@ struct QuiesceScope {
   ~QuiesceScope() { t.resume(); }
 };
 
+std::vector<BulkItem> live_items(DeviceContext& ctx, const std::vector<AllocationRecord>& active,
+                                 std::vector<std::vector<uint8_t>>& flags, bool with_flags) {
+  std::vector<BulkItem> items;
+  flags.clear();
+  flags.reserve(active.size());
+  for (const AllocationRecord& rec : active) {
+    BulkItem it{rec.id, rec.kind, rec.size, ctx.backing_ptr(rec.id), nullptr};
+    if (with_flags && rec.kind == AllocationKind::Managed) {
+      const auto pages = ctx.managed_pages(rec.id);
+      std::vector<uint8_t> f(pages.size());
+      for (size_t i = 0; i < pages.size(); ++i)
+        f[i] = uint8_t((pages[i].device_resident ? 1 : 0) | (pages[i].dirty ? 2 : 0));
+      flags.push_back(std::move(f));
+      it.flags = &flags.back();
+    }
+    items.push_back(it);
+  }
+  return items;
+}
+
+uint64_t tail_bytes(Session& session) {
+  DeviceContext& ctx = session.device();
+  return (20 + 8 * ctx.live_stream_ids().size()) + (20 + session.app_state().size()) +
+         (20 + registry_bytes(ctx.registered_binaries()).size());
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
 // drain
 // ---------------------------------------------------------------------------
 void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
+  PhaseTrace tr("drain");
   QuiesceScope q(session.table(), session.config().quiesce_timeout);
+  tr.mark("quiesce");
   DeviceContext& ctx = session.device();
   DrainEngine& E = session.drain_engine();
   if (stats) *stats = DrainStats{};
@@ -439,31 +579,18 @@ void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
   const std::vector<uint8_t>& sec6 = session.app_state();
   const std::vector<uint8_t> sec7 = registry_bytes(ctx.registered_binaries());
 
-  // bulk plan
-  std::vector<BulkItem> items;
   std::vector<std::vector<uint8_t>> flags;
-  flags.reserve(active.size());
-  for (const AllocationRecord& rec : active) {
-    BulkItem it{rec.id, rec.kind, rec.size, ctx.backing_ptr(rec.id), nullptr};
-    if (rec.kind == AllocationKind::Managed) {
-      const auto pages = ctx.managed_pages(rec.id);
-      std::vector<uint8_t> f(pages.size());
-      for (size_t i = 0; i < pages.size(); ++i)
-        f[i] = uint8_t((pages[i].device_resident ? 1 : 0) | (pages[i].dirty ? 2 : 0));
-      flags.push_back(std::move(f));
-      it.flags = &flags.back();
-    }
-    items.push_back(it);
-  }
   ImagePlan& P = E.plan;
-  build_plan(items, P);
+  build_plan(live_items(ctx, active, flags, true), P);
   P.log_len = log.size();
+  tr.mark("plan");
 
   // file layout: header | META | LOG | ALLOC hdr | stream | crc4 | STREAMS | APPSTATE | REGISTRY
   const uint64_t s3 = 16 + (20 + sec1.size()) + (20 + sec2.size()) + 16;
   const uint64_t total = s3 + P.stream_len + 4 + (20 + sec5.size()) + (20 + sec6.size()) +
                          (20 + sec7.size());
   out.prepare(total, s3);
+  tr.mark("image-alloc");
   P.s3 = s3;
   P.image_bytes = total;
   uint8_t* img = out.mutable_data();
@@ -476,18 +603,24 @@ void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
   put_at<uint32_t>(img + at, 3);
   put_at<uint32_t>(img + at + 4, 0);
   put_at<uint64_t>(img + at + 8, P.len3);
-  at += 16;
 
   const bool bulk = P.len3 + P.len4 > 0;
   uint32_t crc3 = 0, crc4 = 0;
+  uint64_t windows = 0;
   if (bulk) {
     upload_plan(E, P, E.s_pack);
-    cudaEvent_t uploaded = E.ev_ready[0];
-    check_cuda(cudaEventRecord(uploaded, E.s_pack), "event");
-    check_cuda(cudaStreamWaitEvent(E.s_hash, uploaded, 0), "wait");
-    launch_hash(E, P, E.s_hash, stats);
+    check_cuda(cudaEventRecord(E.ev_ready[0], E.s_pack), "event");
+    check_cuda(cudaStreamWaitEvent(E.s_hash, E.ev_ready[0], 0), "wait");
+    // K1 on all but kPackSMs SMs: the pack kernels never queue behind it
+    const uint32_t k1_ctas = uint32_t(std::max(1, E.sm_count - DrainEngine::kPackSMs));
+    check_cuda(cudaEventRecord(E.ev_h0, E.s_hash), "event");
+    if (P.pay_first.back()) hash_payloads(E, P, 0, P.pay_first.back(), k1_ctas, E.s_hash);
+    if (P.page_first.back()) hash_pages(E, P, k1_ctas, E.s_hash);
+    check_cuda(cudaEventRecord(E.ev_h1, E.s_hash), "event");
+    download_crcs(E, P, E.s_hash);
 
-    const uint64_t windows = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
+    windows = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
+    if (stats) E.ensure_window_events(windows);
     check_cuda(cudaEventRecord(E.ev_c0, E.s_pack), "event");
     for (uint64_t w = 0; w < windows; ++w) {
       const int slot = int(w % DrainEngine::kSlots);
@@ -496,26 +629,24 @@ void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
       const uint64_t len = std::min(DrainEngine::kWindow, P.stream_len - off);
       if (w >= uint64_t(DrainEngine::kSlots))
         check_cuda(cudaStreamWaitEvent(E.s_pack, E.ev_free[slot], 0), "wait");
-      if (stats && w < uint64_t(DrainEngine::kSlots)) cudaEventRecord(E.ev_p0[slot], E.s_pack);
+      if (stats) cudaEventRecord(E.ev_w0[w], E.s_pack);
       check_cuda(cudaError_t(crac_pack_records(E.d_recs.ptr, uint32_t(P.recs.size()),
                                                E.d_tile_rec.ptr + off / CRAC_TILE_BYTES, off, len,
                                                buf, E.s_pack)),
                  "pack");
-      if (stats && w < uint64_t(DrainEngine::kSlots)) cudaEventRecord(E.ev_p1[slot], E.s_pack);
+      if (stats) cudaEventRecord(E.ev_w1[w], E.s_pack);
       check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_pack), "event");
       check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_ready[slot], 0), "wait");
       check_cuda(cudaMemcpyAsync(img + s3 + off, buf, len, cudaMemcpyDeviceToHost, E.s_copy), "D2H");
       check_cuda(cudaEventRecord(E.ev_free[slot], E.s_copy), "event");
     }
     check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
-    if (stats) {
-      stats->pack_launches = windows;
-      stats->pack_bytes = P.stream_len;
-      stats->d2h_bytes = P.stream_len;
-    }
+    tr.mark("enqueue");
     // fold while the D2H is still draining
     check_cuda(cudaStreamSynchronize(E.s_hash), "hash sync");
+    tr.mark("hash-wait");
     fold_sections(E, P, crc3, crc4);
+    tr.mark("fold");
     // seed the incremental table with this image's payload chunk CRCs
     const uint64_t n_pay = P.pay_first.back();
     if (n_pay) {
@@ -527,6 +658,7 @@ void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
     check_cuda(cudaStreamSynchronize(E.s_copy), "copy sync");
     check_cuda(cudaStreamSynchronize(E.s_pack), "pack sync");
     check_cuda(cudaStreamSynchronize(E.s_hash), "hash sync");
+    tr.mark("d2h-wait");
   } else {
     // no bulk bytes: the stream is just crc3 (0) and the UVM_PAGES header
     put_at<uint32_t>(img + s3, 0);
@@ -544,20 +676,22 @@ void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
   if (at != total) raise(Errc::DeviceFault, "image layout mismatch");
   P.valid = true;
   P.tail_bytes = (20 + sec5.size()) + (20 + sec6.size()) + (20 + sec7.size());
+  P.image_ptr = reinterpret_cast<uint64_t>(img);
   E.prev_valid = P.pay_first.back() > 0;
 
   check_cuda(cudaEventRecord(E.ev_t1, E.s_pack), "event");
   check_cuda(cudaEventSynchronize(E.ev_t1), "event sync");
   if (stats) {
-    StreamTimer t;
-    stats->total_ms = t.ms(E.ev_t0, E.ev_t1);
+    stats->total_ms = elapsed(E.ev_t0, E.ev_t1);
     if (bulk) {
-      stats->hash_ms = t.ms(E.ev_h0, E.ev_h1);
-      stats->copy_ms = t.ms(E.ev_c0, E.ev_c1);
-      const uint64_t timed = std::min<uint64_t>(stats->pack_launches, DrainEngine::kSlots);
-      double sum = 0;
-      for (uint64_t i = 0; i < timed; ++i) sum += t.ms(E.ev_p0[i], E.ev_p1[i]);
-      stats->pack_ms = timed ? sum / timed * stats->pack_launches : 0;
+      stats->hash_ms = elapsed(E.ev_h0, E.ev_h1);
+      stats->copy_ms = elapsed(E.ev_c0, E.ev_c1);
+      stats->hash_launches = (P.pay_first.back() ? 1 : 0) + (P.page_first.back() ? 1 : 0);
+      stats->hash_bytes = hashed_bytes(P);
+      stats->pack_launches = windows;
+      stats->pack_bytes = P.stream_len;
+      stats->pack_ms = median_window_ms(E, windows);  // per launch
+      stats->d2h_bytes = P.stream_len;
     }
     stats->image_bytes = total;
     stats->total_chunks = P.pay_first.back() + P.page_first.back();
@@ -570,21 +704,23 @@ void hash_only(Session& session, DrainStats* stats) {
   DeviceContext& ctx = session.device();
   DrainEngine& E = session.drain_engine();
   if (stats) *stats = DrainStats{};
-  std::vector<BulkItem> items;
-  for (const AllocationRecord& rec : active_set(session.log().snapshot()))
-    items.push_back(BulkItem{rec.id, rec.kind, rec.size, ctx.backing_ptr(rec.id), nullptr});
+  std::vector<std::vector<uint8_t>> flags;
   ImagePlan P;
-  build_plan(items, P);
+  build_plan(live_items(ctx, active_set(session.log().snapshot()), flags, false), P);
   upload_plan(E, P, E.s_hash);
-  launch_hash(E, P, E.s_hash, stats);
+  check_cuda(cudaEventRecord(E.ev_h0, E.s_hash), "event");
+  if (P.pay_first.back()) hash_payloads(E, P, 0, P.pay_first.back(), 0, E.s_hash);
+  if (P.page_first.back()) hash_pages(E, P, 0, E.s_hash);
+  check_cuda(cudaEventRecord(E.ev_h1, E.s_hash), "event");
   check_cuda(cudaStreamSynchronize(E.s_hash), "hash sync");
   if (stats) {
-    StreamTimer t;
-    stats->hash_ms = t.ms(E.ev_h0, E.ev_h1);
-    stats->total_ms = stats->hash_ms;
+    stats->hash_ms = stats->total_ms = elapsed(E.ev_h0, E.ev_h1);
+    stats->hash_bytes = hashed_bytes(P);
+    stats->hash_launches = (P.pay_first.back() ? 1 : 0) + (P.page_first.back() ? 1 : 0);
     stats->total_chunks = P.pay_first.back() + P.page_first.back();
   }
   E.plan.valid = false;  // the device tables now describe this pass, not an image
+  E.prev_valid = false;
 }
 
 // ---------------------------------------------------------------------------
@@ -593,9 +729,11 @@ void hash_only(Session& session, DrainStats* stats) {
 Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catalog, TableMode mode,
                       std::chrono::milliseconds quiesce_timeout, DrainStats* stats) {
   if (stats) *stats = DrainStats{};
+  PhaseTrace tr("refill");
   std::vector<uint8_t> storage;
   const std::span<const uint8_t> raw = unwrap(image, storage, nullptr);
   ParsedImage p = parse_image(raw, /*verify_bulk=*/false);
+  tr.mark("parse");
 
   SessionConfig cfg;
   cfg.seed = p.meta.seed;
@@ -606,6 +744,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   DeviceContext& ctx = session.device();
   DrainEngine& E = session.drain_engine();
   check_cuda(cudaEventRecord(E.ev_t0, E.s_pack), "event");
+  tr.mark("session");
 
   std::map<uint64_t, std::vector<KernelDescriptor>> binaries;
   for (const BinaryInfo& b : p.binaries) {
@@ -621,8 +760,8 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
 
   std::set<uint64_t> live;
   {
-    // map every live Device extent up front, coalescing neighbours, so the
-    // replay does no per-allocation driver calls
+    // map every live Device extent up front in coalesced runs, so the replay
+    // itself makes no driver calls
     uint64_t run_lo = 0, run_hi = 0;
     for (const AllocationRecord& r : p.facts.active) {
       live.insert(r.id);
@@ -638,6 +777,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     }
     if (run_hi) ctx.premap(run_lo, run_hi - run_lo);
   }
+  tr.mark("premap");
   ctx.begin_replay(std::move(live));
   try {
     replay_log(ctx, p.log, &binaries);
@@ -646,12 +786,13 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     throw;
   }
   ctx.end_replay();
+  tr.mark("replay");
   if (ctx.live_stream_ids() != p.streams)
     raise(Errc::ReplayDivergence, "live streams after replay do not match the snapshot");
 
   // destinations of every framed record, in image order
   std::vector<BulkItem> items;
-  size_t pi = 0, mi = 0;
+  size_t mi = 0;
   for (const AllocationRecord& rec : p.facts.active) {
     const auto replayed = ctx.find_record(rec.id);
     if (!replayed || replayed->size != rec.size || replayed->kind != rec.kind)
@@ -659,7 +800,6 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
             "record " + std::to_string(rec.id) + " does not match a replayed allocation");
     BulkItem it{rec.id, rec.kind, rec.size, ctx.backing_ptr(rec.id), nullptr};
     if (rec.kind == AllocationKind::Managed) it.flags = &p.managed[mi++].flags;
-    else ++pi;
     items.push_back(it);
   }
   ImagePlan& P = E.plan;
@@ -669,13 +809,17 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   if (P.len3 != p.sec[2].length || P.len4 != p.sec[3].length ||
       s3 + P.stream_len != p.sec[3].payload_off + p.sec[3].length)
     raise(Errc::ImageCorrupt, "bulk sections do not match the log's active set");
+  tr.mark("plan");
 
+  uint64_t windows = 0;
   if (P.stream_len > 20) {
     upload_plan(E, P, E.s_pack);
     check_cuda(cudaEventRecord(E.ev_ready[0], E.s_pack), "event");
     check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_ready[0], 0), "wait");
-    const uint64_t windows = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
+    windows = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
+    if (stats) E.ensure_window_events(windows);
     check_cuda(cudaEventRecord(E.ev_c0, E.s_copy), "event");
+    size_t spans_done = 0;
     for (uint64_t w = 0; w < windows; ++w) {
       const int slot = int(w % DrainEngine::kSlots);
       uint8_t* buf = E.d_ring + slot * (DrainEngine::kWindow + 64);
@@ -689,41 +833,46 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
                  "H2D");
       check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_copy), "event");
       check_cuda(cudaStreamWaitEvent(E.s_pack, E.ev_ready[slot], 0), "wait");
-      if (stats && w < uint64_t(DrainEngine::kSlots)) cudaEventRecord(E.ev_p0[slot], E.s_pack);
+      if (stats) cudaEventRecord(E.ev_w0[w], E.s_pack);
       check_cuda(cudaError_t(crac_scatter_records(E.d_recs.ptr, uint32_t(P.recs.size()),
                                                   E.d_tile_rec.ptr + off / CRAC_TILE_BYTES, buf,
                                                   off, len, E.s_pack)),
                  "scatter");
-      if (stats && w < uint64_t(DrainEngine::kSlots)) cudaEventRecord(E.ev_p1[slot], E.s_pack);
+      if (stats) cudaEventRecord(E.ev_w1[w], E.s_pack);
       check_cuda(cudaEventRecord(E.ev_free[slot], E.s_pack), "event");
+      // verify as we go: re-hash every region whose last byte has landed
+      size_t done = spans_done;
+      while (done < P.pay_spans.size() &&
+             P.pay_rec_off[done] + P.pay_spans[done].len <= off + len)
+        ++done;
+      if (done > spans_done) {
+        hash_payloads(E, P, P.pay_first[spans_done], P.pay_first[done], 0, E.s_pack);
+        if (stats) ++stats->hash_launches;
+        spans_done = done;
+      }
     }
     check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
-    if (stats) {
-      stats->pack_launches = windows;
-      stats->pack_bytes = P.stream_len;
-      stats->h2d_bytes = P.stream_len;
+    if (P.page_first.back()) {
+      hash_pages(E, P, 0, E.s_pack);
+      if (stats) ++stats->hash_launches;
     }
-    // verify: K1 over the refilled regions, folded with the image's frames
-    launch_hash(E, P, E.s_pack, stats);
+    download_crcs(E, P, E.s_pack);
+    tr.mark("enqueue");
     check_cuda(cudaStreamSynchronize(E.s_pack), "refill sync");
+    tr.mark("h2d+verify");
     uint32_t crc3 = 0, crc4 = 0;
     fold_sections(E, P, crc3, crc4);
+    tr.mark("fold");
     if (crc3 != p.sec[2].crc) raise(Errc::ImageCorrupt, "crc mismatch in ALLOC_PAYLOADS");
     if (crc4 != p.sec[3].crc) raise(Errc::ImageCorrupt, "crc mismatch in UVM_PAGES");
-    const uint64_t n_pay = P.pay_first.back();
-    if (n_pay) {
-      E.d_prev_crc.ensure(n_pay);
-      check_cuda(cudaMemcpyAsync(E.d_prev_crc.ptr, E.d_pay_crc.ptr, n_pay * 4,
-                                 cudaMemcpyDeviceToDevice, E.s_pack),
-                 "seed prev crc");
-    }
   } else if (p.sec[2].crc != 0 || p.sec[3].crc != 0) {
     raise(Errc::ImageCorrupt, "crc mismatch in empty bulk section");
   }
   // managed residence and flags
   mi = 0;
   for (const AllocationRecord& rec : p.facts.active)
-    if (rec.kind == AllocationKind::Managed) ctx.restore_managed(rec.id, p.managed[mi++].flags, E.s_pack);
+    if (rec.kind == AllocationKind::Managed)
+      ctx.restore_managed(rec.id, p.managed[mi++].flags, E.s_pack);
   check_cuda(cudaEventRecord(E.ev_t1, E.s_pack), "event");
   check_cuda(cudaEventSynchronize(E.ev_t1), "event sync");
   E.prev_valid = false;  // no pinned image of this session exists yet
@@ -732,15 +881,14 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   session.log().reset(std::move(p.log));
   session.app_state() = std::move(p.app_state);
   if (stats) {
-    StreamTimer t;
-    stats->total_ms = t.ms(E.ev_t0, E.ev_t1);
-    if (P.stream_len > 20) {
-      stats->hash_ms = t.ms(E.ev_h0, E.ev_h1);
-      stats->copy_ms = t.ms(E.ev_c0, E.ev_c1);
-      const uint64_t timed = std::min<uint64_t>(stats->pack_launches, DrainEngine::kSlots);
-      double sum = 0;
-      for (uint64_t i = 0; i < timed; ++i) sum += t.ms(E.ev_p0[i], E.ev_p1[i]);
-      stats->pack_ms = timed ? sum / timed * stats->pack_launches : 0;
+    stats->total_ms = elapsed(E.ev_t0, E.ev_t1);
+    if (windows) {
+      stats->copy_ms = elapsed(E.ev_c0, E.ev_c1);
+      stats->pack_launches = windows;
+      stats->pack_bytes = P.stream_len;
+      stats->pack_ms = median_window_ms(E, windows);
+      stats->h2d_bytes = P.stream_len;
+      stats->hash_bytes = hashed_bytes(P);
     }
     stats->image_bytes = raw.size();
     stats->total_chunks = P.pay_first.back() + P.page_first.back();
@@ -753,8 +901,9 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
 // ---------------------------------------------------------------------------
 namespace {
 
-// Incremental drain body; runs with the dispatch gate held.
+// Runs with the dispatch gate held; the layout of `image` is E.plan's.
 void incremental_locked(Session& session, PinnedImage& image, DrainStats* stats) {
+  PhaseTrace tr("incr");
   DrainEngine& E = session.drain_engine();
   const ImagePlan& P = E.plan;
   DeviceContext& ctx = session.device();
@@ -766,9 +915,11 @@ void incremental_locked(Session& session, PinnedImage& image, DrainStats* stats)
   uint8_t* img = image.mutable_data();
   const uint64_t s3 = P.s3;
 
-  // 1. hash everything (K1), 2. diff against the previous image (K2b)
-  launch_hash(E, P, E.s_pack, stats);
+  // 1. K1 over everything, 2. diff + ordered compaction (K2b)
   const uint64_t n = P.pay_first.back();
+  check_cuda(cudaEventRecord(E.ev_h0, E.s_pack), "event");
+  hash_payloads(E, P, 0, n, 0, E.s_pack);
+  check_cuda(cudaEventRecord(E.ev_h1, E.s_pack), "event");
   E.d_block_counts.ensure((n + 4095) / 4096 + 1);
   E.d_dirty_idx.ensure(std::max<uint64_t>(n, 1));
   E.d_dirty_count.ensure(1);
@@ -779,73 +930,42 @@ void incremental_locked(Session& session, PinnedImage& image, DrainStats* stats)
              "diff");
   check_cuda(cudaMemcpyAsync(E.h_count.ptr, E.d_dirty_count.ptr, 8, cudaMemcpyDeviceToHost, E.s_pack),
              "count");
+  download_crcs(E, P, E.s_pack);
   check_cuda(cudaStreamSynchronize(E.s_pack), "diff sync");
+  tr.mark("hash+diff");
   const uint64_t dirty = E.h_count.ptr[0];
-  E.h_dirty_idx.ensure(std::max<uint64_t>(dirty, 1));
-  if (dirty)
-    check_cuda(cudaMemcpyAsync(E.h_dirty_idx.ptr, E.d_dirty_idx.ptr, dirty * 8,
-                               cudaMemcpyDeviceToHost, E.s_hash),
-               "dirty idx");
 
-  // 3. gather dirty chunks into the device ring, D2H each window as one
-  //    contiguous copy into a pinned host ring, patch the image from there
-  const uint64_t per_win = DrainEngine::kWindow / DrainEngine::kChunk;
-  const uint64_t windows = (dirty + per_win - 1) / per_win;
-  E.h_ring.ensure(DrainEngine::kSlots * DrainEngine::kWindow);
-  if (windows) check_cuda(cudaStreamSynchronize(E.s_hash), "dirty idx sync");
-  check_cuda(cudaEventRecord(E.ev_c0, E.s_pack), "event");
-  auto patch = [&](uint64_t w) {  // host side of window w (its D2H has completed)
-    const int slot = int(w % DrainEngine::kSlots);
-    const uint8_t* hbuf = E.h_ring.ptr + slot * DrainEngine::kWindow;
-    const uint64_t first = w * per_win, count = std::min(per_win, dirty - first);
-    parallel_for(count, [&](uint64_t k) {
-      const uint64_t c = E.h_dirty_idx.ptr[first + k];
-      const size_t s = size_t(std::upper_bound(P.pay_first.begin(), P.pay_first.end(), c) -
-                              P.pay_first.begin() - 1);
-      const uint64_t off = (c - P.pay_first[s]) * DrainEngine::kChunk;
-      const uint64_t len = std::min<uint64_t>(DrainEngine::kChunk, P.pay_spans[s].len - off);
-      std::memcpy(img + s3 + P.pay_rec_off[s] + off, hbuf + k * DrainEngine::kChunk, len);
-    });
-  };
-  for (uint64_t w = 0; w < windows; ++w) {
-    const int slot = int(w % DrainEngine::kSlots);
-    uint8_t* buf = E.d_ring + slot * (DrainEngine::kWindow + 64);
-    const uint64_t first = w * per_win, count = std::min(per_win, dirty - first);
-    if (w >= uint64_t(DrainEngine::kSlots)) {
-      // slot reuse: its previous window must be copied out and patched
-      check_cuda(cudaEventSynchronize(E.ev_free[slot]), "slot sync");
-      patch(w - DrainEngine::kSlots);
+  // 3. the SMs write every dirty chunk straight into the pinned image (one
+  //    launch; the PCIe writes overlap the host-side fold below)
+  if (dirty) {
+    if (E.dst_for_image != P.image_ptr) {
+      std::vector<uint64_t> dst(P.pay_rec_off.size());
+      for (size_t s = 0; s < dst.size(); ++s) dst[s] = s3 + P.pay_rec_off[s];
+      upload(E.d_pay_dst, dst, E.s_copy);
+      E.dst_for_image = P.image_ptr;
     }
-    check_cuda(cudaError_t(crac_gather_chunks(E.d_pay_spans.ptr, E.d_pay_first.ptr,
-                                              uint32_t(P.pay_spans.size()), DrainEngine::kChunk,
-                                              E.d_dirty_idx.ptr, first, count, buf, E.s_pack)),
-               "gather");
-    check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_pack), "event");
-    check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_ready[slot], 0), "wait");
-    check_cuda(cudaMemcpyAsync(E.h_ring.ptr + slot * DrainEngine::kWindow, buf,
-                               count * DrainEngine::kChunk, cudaMemcpyDeviceToHost, E.s_copy),
-               "D2H dirty");
-    check_cuda(cudaEventRecord(E.ev_free[slot], E.s_copy), "event");
+    check_cuda(cudaEventRecord(E.ev_c0, E.s_copy), "event");
+    check_cuda(cudaError_t(crac_gather_chunks_to_host(
+                   E.d_pay_spans.ptr, E.d_pay_first.ptr, uint32_t(P.pay_spans.size()),
+                   DrainEngine::kChunk, E.d_dirty_idx.ptr, 0, dirty, E.d_pay_dst.ptr, img, E.s_copy)),
+               "gather to host");
+    check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
     if (stats) {
-      stats->d2h_bytes += count * DrainEngine::kChunk;
-      stats->pack_launches += 1;
-      stats->pack_bytes += count * DrainEngine::kChunk;
+      E.h_dirty_idx.ensure(dirty);
+      check_cuda(cudaMemcpyAsync(E.h_dirty_idx.ptr, E.d_dirty_idx.ptr, dirty * 8,
+                                 cudaMemcpyDeviceToHost, E.s_copy),
+                 "dirty idx");
     }
   }
-  check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
-  for (uint64_t w = windows > uint64_t(DrainEngine::kSlots) ? windows - DrainEngine::kSlots : 0;
-       w < windows; ++w) {
-    check_cuda(cudaEventSynchronize(E.ev_free[w % DrainEngine::kSlots]), "slot sync");
-    patch(w);
-  }
-  // managed pages are never part of an incremental plan (checked above)
   uint32_t crc3 = 0, crc4 = 0;
   fold_sections(E, P, crc3, crc4);
+  tr.mark("fold");
+  check_cuda(cudaStreamSynchronize(E.s_copy), "gather sync");
+  tr.mark("gather");
   put_at<uint32_t>(img + s3 + P.len3, crc3);
   put_at<uint32_t>(img + s3 + P.stream_len, crc4);
 
-  // small sections can change without a layout change (app_state content,
-  // registry is tied to the log): rewrite the tail sections
+  // the tail sections may change without a layout change (app_state bytes)
   const std::vector<uint8_t> sec5 = streams_bytes(ctx.live_stream_ids());
   const std::vector<uint8_t>& sec6 = session.app_state();
   const std::vector<uint8_t> sec7 = registry_bytes(ctx.registered_binaries());
@@ -857,10 +977,16 @@ void incremental_locked(Session& session, PinnedImage& image, DrainStats* stats)
   check_cuda(cudaEventRecord(E.ev_t1, E.s_pack), "event");
   check_cuda(cudaEventSynchronize(E.ev_t1), "event sync");
   if (stats) {
-    StreamTimer t;
-    stats->total_ms = t.ms(E.ev_t0, E.ev_t1);
-    stats->hash_ms = t.ms(E.ev_h0, E.ev_h1);
-    stats->copy_ms = windows ? t.ms(E.ev_c0, E.ev_c1) : 0;
+    uint64_t bytes = 0;
+    for (uint64_t k = 0; k < dirty; ++k) bytes += chunk_len(P, E.h_dirty_idx.ptr[k]);
+    stats->total_ms = elapsed(E.ev_t0, E.ev_t1);
+    stats->hash_ms = elapsed(E.ev_h0, E.ev_h1);
+    stats->hash_launches = 1;
+    stats->hash_bytes = hashed_bytes(P);
+    stats->copy_ms = dirty ? elapsed(E.ev_c0, E.ev_c1) : 0;
+    stats->pack_launches = dirty ? 1 : 0;
+    stats->pack_bytes = bytes;
+    stats->d2h_bytes = bytes;
     stats->image_bytes = P.image_bytes;
     stats->dirty_chunks = dirty;
     stats->total_chunks = n;
@@ -869,25 +995,16 @@ void incremental_locked(Session& session, PinnedImage& image, DrainStats* stats)
 
 }  // namespace
 
-namespace {
-
-uint64_t tail_bytes(Session& session) {
-  DeviceContext& ctx = session.device();
-  return (20 + 8 * ctx.live_stream_ids().size()) + (20 + session.app_state().size()) +
-         (20 + registry_bytes(ctx.registered_binaries()).size());
-}
-
-}  // namespace
-
 void checkpoint_incremental(Session& session, PinnedImage& image, DrainStats* stats) {
-  // Emits exactly the bytes of a full drain.  Only valid while the layout of
-  // the previous image of this session is unchanged (same log, same bulk
-  // records, no managed allocations, same tail size) and `image` still holds
-  // those bytes; otherwise this is a full drain.
+  // Emits exactly the bytes of a full drain.  Valid while the layout of the
+  // previous image of this session is unchanged (same log, same bulk
+  // records, no managed allocations, same tail size) and `image` is that
+  // image; otherwise this is a full drain.
   DrainEngine& E = session.drain_engine();
   const ImagePlan& P = E.plan;
   auto layout_unchanged = [&] {
     if (!P.valid || !E.prev_valid || image.size() != P.image_bytes ||
+        reinterpret_cast<uint64_t>(image.data()) != P.image_ptr ||
         session.log().size() != P.log_len || tail_bytes(session) != P.tail_bytes)
       return false;
     std::vector<uint64_t> sig;
@@ -905,8 +1022,7 @@ void checkpoint_incremental(Session& session, PinnedImage& image, DrainStats* st
   bool raced = false;
   {
     QuiesceScope q(session.table(), session.config().quiesce_timeout);
-    // re-check under the gate: the log cannot move now
-    raced = !layout_unchanged();
+    raced = !layout_unchanged();  // re-check under the gate: the log cannot move now
     if (!raced) incremental_locked(session, image, stats);
   }
   if (raced) checkpoint_image(session, image, stats);

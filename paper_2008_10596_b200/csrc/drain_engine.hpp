@@ -1,24 +1,36 @@
 // Per-session state of the B200 drain/refill pipeline (internal).
 //
 // HBM layout owned here (allocated once, grown geometrically, reused by every
-// checkpoint so no timed step allocates):
-//   ring      kSlots x (window + 64) bytes  staging for the section stream
+// checkpoint; engines are pooled across sessions so restarts reuse them):
+//   ring      kSlots x (kWindow + 64) bytes  staging for the section stream
 //   recs      crac_record_t per framed record of ALLOC_PAYLOADS + UVM_PAGES
 //   tile_rec  u32 per 64 KiB stream tile: first record overlapping it
 //   spans/first/crc  K1 inputs/outputs: payload spans (64 KiB chunks) and
 //             managed spans (4 KiB chunks = one CRC per page)
-//   prev_crc / dirty_idx / block_counts   incremental state (K2b)
+//   prev_crc / dirty_idx / block_counts / pay_dst   incremental state (K2b)
 #pragma once
 
 #include <cuda_runtime_api.h>
 
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "crac_gpu.h"
 #include "cracsim/ckpt_engine.hpp"
 
 namespace cracsim {
+
+// Phase tracing for diagnosis: CRAC_TRACE=1 prints host-side phase times of
+// every drain / refill to stderr.
+struct PhaseTrace {
+  const char* op;
+  double t0, last;
+  bool on;
+  explicit PhaseTrace(const char* name);
+  void mark(const char* phase);
+  ~PhaseTrace();
+};
 
 template <typename T>
 struct DevArray {
@@ -39,6 +51,7 @@ struct HostArray {  // pinned
 // Layout of the last image this session drained (enables incremental drains).
 struct ImagePlan {
   uint64_t image_bytes = 0;
+  uint64_t image_ptr = 0;   // where that image lives (host)
   uint64_t s3 = 0;          // file offset of the ALLOC_PAYLOADS payload (= stream start)
   uint64_t len3 = 0, len4 = 0;
   uint64_t stream_len = 0;  // len3 + 20 + len4
@@ -46,7 +59,6 @@ struct ImagePlan {
   std::vector<uint32_t> tile_rec;
   std::vector<crac_span_t> pay_spans, page_spans;
   std::vector<uint64_t> pay_first, page_first;
-  std::vector<uint64_t> pay_ids;      // allocation id per payload span
   std::vector<uint64_t> pay_rec_off;  // stream offset of each payload's first byte
   std::vector<uint64_t> log_sizes;    // signature: (id, size) of every bulk record
   uint64_t log_len = 0;
@@ -59,33 +71,39 @@ struct DrainEngine {
   static constexpr uint64_t kWindow = 16ull << 20;  // multiple of CRAC_TILE_BYTES
   static constexpr uint32_t kChunk = 65536;         // payload hash chunk
   static constexpr uint32_t kPageChunk = 4096;      // managed hash chunk (= page)
+  static constexpr int kPackSMs = 16;               // SMs K1 leaves to the pack during a drain
 
   int device = 0;
+  int sm_count = 148;
   cudaStream_t s_pack = nullptr, s_copy = nullptr, s_hash = nullptr;
   cudaEvent_t ev_ready[kSlots] = {}, ev_free[kSlots] = {};
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr, ev_h0 = nullptr, ev_h1 = nullptr;
   cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr;
-  cudaEvent_t ev_p0[kSlots] = {}, ev_p1[kSlots] = {};
+  std::vector<cudaEvent_t> ev_w0, ev_w1;  // per-window kernel timing (stats only)
   uint8_t* d_ring = nullptr;
 
   DevArray<crac_record_t> d_recs;
   DevArray<uint32_t> d_tile_rec;
   DevArray<crac_span_t> d_pay_spans, d_page_spans;
-  DevArray<uint64_t> d_pay_first, d_page_first, d_pay_ids;
+  DevArray<uint64_t> d_pay_first, d_page_first, d_pay_dst;
   DevArray<uint32_t> d_pay_crc, d_page_crc, d_prev_crc, d_block_counts;
   DevArray<uint64_t> d_dirty_idx, d_dirty_count;
   HostArray<uint32_t> h_pay_crc, h_page_crc;
-  HostArray<uint64_t> h_dirty_idx;
-  HostArray<uint64_t> h_count;
-  HostArray<uint8_t> h_ring;  // kSlots x kWindow pinned landing zone (incremental)
+  HostArray<uint64_t> h_count, h_dirty_idx;
 
   ImagePlan plan;
-  bool prev_valid = false;  // d_prev_crc holds the chunk CRCs of `plan`'s image
+  bool prev_valid = false;      // d_prev_crc holds the chunk CRCs of `plan`'s image
+  uint64_t dst_for_image = 0;   // image the d_pay_dst table was built for
 
   explicit DrainEngine(int dev);
   ~DrainEngine();
   DrainEngine(const DrainEngine&) = delete;
   DrainEngine& operator=(const DrainEngine&) = delete;
+  void ensure_window_events(size_t n);
 };
+
+// Process-wide engine pool (Session construction / destruction).
+std::unique_ptr<DrainEngine> acquire_engine(int device);
+void release_engine(std::unique_ptr<DrainEngine> e);
 
 }  // namespace cracsim

@@ -23,6 +23,8 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 #include <mutex>
 #include <vector>
 
@@ -161,12 +163,45 @@ __device__ __forceinline__ uint32_t find_span(const uint64_t* chunk_first, uint3
   return lo;
 }
 
+// Runs one lane's column over `rows` rows of 512 B starting at p (the lane's
+// first word).  Loads of the next kRows rows are in flight while the current
+// kRows rows are hashed.  The last row uses group A (no trailing gap).
+template <int kRows>
+__device__ __forceinline__ uint32_t k1_rows(const LaneLut& lut, const uint8_t* p, uint32_t rows) {
+  uint32_t acc = 0, r = 0;
+  if (rows >= uint32_t(kRows)) {
+    uint4 cur[kRows];
+#pragma unroll
+    for (int k = 0; k < kRows; ++k) cur[k] = ldg_stream(p + k * 512);
+    for (; r + 2 * kRows <= rows; r += kRows) {
+      uint4 nxt[kRows];
+#pragma unroll
+      for (int k = 0; k < kRows; ++k) nxt[k] = ldg_stream(p + (r + kRows + k) * 512);
+#pragma unroll
+      for (int k = 0; k < kRows; ++k) acc = word16<true>(lut, acc, cur[k]);
+#pragma unroll
+      for (int k = 0; k < kRows; ++k) cur[k] = nxt[k];
+    }
+#pragma unroll
+    for (int k = 0; k < kRows - 1; ++k) acc = word16<true>(lut, acc, cur[k]);
+    acc = (r + kRows == rows) ? word16<false>(lut, acc, cur[kRows - 1])
+                              : word16<true>(lut, acc, cur[kRows - 1]);
+    r += kRows;
+  }
+  for (; r < rows; ++r) {
+    const uint4 w = ldg_stream(p + r * 512);
+    acc = (r + 1 == rows) ? word16<false>(lut, acc, w) : word16<true>(lut, acc, w);
+  }
+  return acc;
+}
+
 // ---------------------------------------------------------------------------
 // K1
 // ---------------------------------------------------------------------------
+template <int kRows>
 __global__ void __launch_bounds__(kK1Threads, 1)
     k1_chunk_crc(const crac_span_t* __restrict__ spans, const uint64_t* __restrict__ chunk_first,
-                 uint32_t n_spans, uint32_t chunk_bytes, uint64_t total_chunks,
+                 uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
                  uint32_t* __restrict__ out, uint32_t k_full) {
   extern __shared__ __align__(16) uint32_t s_tab[];
   {
@@ -180,7 +215,8 @@ __global__ void __launch_bounds__(kK1Threads, 1)
   const LaneLut lut = make_lut(static_cast<uint32_t>(__cvta_generic_to_shared(s_tab)), lane);
   const uint64_t gw = blockIdx.x * uint64_t(kK1Warps) + (threadIdx.x >> 5);
   const uint64_t tw = gridDim.x * uint64_t(kK1Warps);
-  const uint64_t c_begin = total_chunks * gw / tw, c_end = total_chunks * (gw + 1) / tw;
+  const uint64_t total_chunks = c_hi - c_lo;
+  const uint64_t c_begin = c_lo + total_chunks * gw / tw, c_end = c_lo + total_chunks * (gw + 1) / tw;
   if (c_begin >= c_end) return;
 
   uint32_t s = find_span(chunk_first, n_spans, c_begin);
@@ -197,37 +233,8 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     const uint8_t* base = reinterpret_cast<const uint8_t*>(sp.ptr + off);
     const uint32_t rows = len >> 9;
 
-    // ---- main body: rows of 512 B, 4-row double-buffered loads ----
-    uint32_t acc = 0;
-    const uint8_t* p = base + lane * 16;
-    uint32_t r = 0;
-    if (rows >= 4) {
-      uint4 cur0 = ldg_stream(p), cur1 = ldg_stream(p + 512), cur2 = ldg_stream(p + 1024),
-            cur3 = ldg_stream(p + 1536);
-      for (; r + 8 <= rows; r += 4) {
-        const uint8_t* q = p + (r + 4) * 512;
-        const uint4 n0 = ldg_stream(q), n1 = ldg_stream(q + 512), n2 = ldg_stream(q + 1024),
-                    n3 = ldg_stream(q + 1536);
-        acc = word16<true>(lut, acc, cur0);
-        acc = word16<true>(lut, acc, cur1);
-        acc = word16<true>(lut, acc, cur2);
-        acc = word16<true>(lut, acc, cur3);
-        cur0 = n0; cur1 = n1; cur2 = n2; cur3 = n3;
-      }
-      acc = word16<true>(lut, acc, cur0);
-      acc = word16<true>(lut, acc, cur1);
-      acc = word16<true>(lut, acc, cur2);
-      if (r + 4 == rows) {
-        acc = word16<false>(lut, acc, cur3);
-      } else {
-        acc = word16<true>(lut, acc, cur3);
-      }
-      r += 4;
-    }
-    for (; r < rows; ++r) {
-      const uint4 w = ldg_stream(p + r * 512);
-      acc = (r + 1 == rows) ? word16<false>(lut, acc, w) : word16<true>(lut, acc, w);
-    }
+    // ---- main body: rows of 512 B, kRows-deep double-buffered loads ----
+    const uint32_t acc = k1_rows<kRows>(lut, base + lane * 16, rows);
     uint32_t L = rows ? warp_xor(crac::gf_mul(g_xp16[31 - lane], acc)) : 0u;
 
     // ---- tail (< 512 B): whole words per lane, then bytes on lane 0 ----
@@ -280,13 +287,71 @@ __device__ __forceinline__ uint4 load_shifted(const uint8_t* p) {
 }
 
 __device__ __forceinline__ void set_byte(uint4& v, uint32_t i, uint32_t b) {
-  uint32_t* w = reinterpret_cast<uint32_t*>(&v);
-  const uint32_t sh = (i & 3) * 8;
-  w[i >> 2] = (w[i >> 2] & ~(0xFFu << sh)) | (b << sh);
+  const uint32_t sh = (i & 3) * 8, keep = ~(0xFFu << sh), put = b << sh;
+  switch (i >> 2) {  // register-resident (no local-memory indexing)
+    case 0: v.x = (v.x & keep) | put; break;
+    case 1: v.y = (v.y & keep) | put; break;
+    case 2: v.z = (v.z & keep) | put; break;
+    default: v.w = (v.w & keep) | put; break;
+  }
+}
+
+// Zeroes bytes [valid, 16) of v.
+__device__ __forceinline__ void keep_prefix(uint4& v, uint32_t valid) {
+  auto mask = [&](uint32_t word) -> uint32_t {
+    const int n = int(valid) - int(4 * word);  // valid bytes in this word
+    return n >= 4 ? 0xFFFFFFFFu : n <= 0 ? 0u : (0xFFFFFFFFu >> (32 - 8 * n));
+  };
+  v.x &= mask(0);
+  v.y &= mask(1);
+  v.z &= mask(2);
+  v.w &= mask(3);
 }
 
 constexpr int kPackThreads = 256;
 constexpr uint32_t kSubTile = 512;
+constexpr uint32_t kTileWords = CRAC_TILE_BYTES / 16;             // 4096
+constexpr uint32_t kWordsPerThread = kTileWords / kPackThreads;   // 16
+
+__device__ __forceinline__ uint4 shfl_down4(uint4 v, int d) {
+  v.x = __shfl_down_sync(0xFFFFFFFFu, v.x, d);
+  v.y = __shfl_down_sync(0xFFFFFFFFu, v.y, d);
+  v.z = __shfl_down_sync(0xFFFFFFFFu, v.z, d);
+  v.w = __shfl_down_sync(0xFFFFFFFFu, v.w, d);
+  return v;
+}
+
+// Copies `nwords` 16-byte words dst[i] = bytes [16 i + shift, +16) of the
+// 16-byte-aligned source `src` (shift 0..15 uniform).  Thread t owns words
+// t, t + 256, ... (coalesced); all loads are issued before any store, and
+// the upper half of a misaligned word comes from the neighbouring lane.
+__device__ __forceinline__ void tile_copy(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                          uint32_t nwords, uint32_t shift) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint4 lo[kWordsPerThread];
+#pragma unroll
+  for (uint32_t k = 0; k < kWordsPerThread; ++k) {
+    const uint32_t w = threadIdx.x + k * kPackThreads;
+    // one word past the end when misaligned: it is the upper half of the
+    // last word, inside the source's 16-byte-rounded extent
+    if (w < nwords || (shift && w == nwords)) lo[k] = ldg_stream(src + w);
+  }
+  if (shift == 0) {
+#pragma unroll
+    for (uint32_t k = 0; k < kWordsPerThread; ++k) {
+      const uint32_t w = threadIdx.x + k * kPackThreads;
+      if (w < nwords) dst[w] = lo[k];
+    }
+    return;
+  }
+#pragma unroll
+  for (uint32_t k = 0; k < kWordsPerThread; ++k) {
+    const uint32_t w = threadIdx.x + k * kPackThreads;
+    uint4 hi = shfl_down4(lo[k], 1);
+    if (lane == 31 && w < nwords) hi = ldg_stream(src + w + 1);
+    if (w < nwords) dst[w] = shift16(lo[k], hi, shift);
+  }
+}
 
 // Byte at stream position x, walking the record cursor forward from r.
 __device__ __forceinline__ uint32_t stream_byte(const crac_record_t* recs, uint32_t n,
@@ -311,7 +376,21 @@ __global__ void __launch_bounds__(kPackThreads)
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t tile0 = win_off + uint64_t(blockIdx.x) * CRAC_TILE_BYTES;
   const uint64_t win_end = win_off + win_len;
+  const uint64_t tile1 = min(tile0 + CRAC_TILE_BYTES, win_end);
   uint32_t rec = tile_rec[blockIdx.x];
+  while (rec + 1 < n && __ldg(&recs[rec + 1].out_off) <= tile0) ++rec;
+  {
+    // whole tile inside one payload (the common case for large regions)
+    const crac_record_t& R = recs[rec];
+    const uint64_t P = R.out_off + R.frame_len;
+    if (P <= tile0 && tile1 <= P + R.len) {
+      const uint64_t rel = tile0 - P;
+      tile_copy(reinterpret_cast<uint4*>(dst + (tile0 - win_off)),
+                reinterpret_cast<const uint4*>(R.ptr) + (rel >> 4),
+                uint32_t((tile1 - tile0 + 15) >> 4), uint32_t(rel & 15));
+      return;
+    }
+  }
   for (uint32_t st = warp; st < CRAC_TILE_BYTES / kSubTile; st += kPackThreads / 32) {
     const uint64_t o = tile0 + uint64_t(st) * kSubTile;
     if (o >= win_end) break;
@@ -326,6 +405,7 @@ __global__ void __launch_bounds__(kPackThreads)
     } else if (x < win_end) {
       uint32_t r = rec;
       uint4 v = make_uint4(0, 0, 0, 0);
+#pragma unroll
       for (uint32_t i = 0; i < 16; ++i) set_byte(v, i, stream_byte(recs, n, r, x + i));
       *out = v;
     }
@@ -353,7 +433,24 @@ __global__ void __launch_bounds__(kPackThreads)
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t tile0 = win_off + uint64_t(blockIdx.x) * CRAC_TILE_BYTES;
   const uint64_t win_end = win_off + win_len;
+  const uint64_t tile1 = min(tile0 + CRAC_TILE_BYTES, win_end);
   uint32_t rec = tile_rec[blockIdx.x];
+  while (rec + 1 < n && __ldg(&recs[rec + 1].out_off) <= tile0) ++rec;
+  {
+    // every destination word starting in this tile is a full data word of
+    // one record: the words are consecutive, sources share one misalignment
+    const crac_record_t& R = recs[rec];
+    const uint64_t P = R.out_off + R.frame_len;
+    if (P <= tile0 && tile1 + 16 <= P + R.len) {
+      const uint64_t d0 = (tile0 - P + 15) >> 4;                 // first dest word
+      const uint64_t d1 = (tile1 - P + 15) >> 4;                 // one past the last
+      const uint64_t f0 = P + 16 * d0 - win_off;                 // its window offset
+      tile_copy(reinterpret_cast<uint4*>(R.ptr) + d0,
+                reinterpret_cast<const uint4*>(win) + (f0 >> 4), uint32_t(d1 - d0),
+                uint32_t(f0 & 15));
+      return;
+    }
+  }
   for (uint32_t st = warp; st < CRAC_TILE_BYTES / kSubTile; st += kPackThreads / 32) {
     const uint64_t o = tile0 + uint64_t(st) * kSubTile;
     if (o >= win_end) break;
@@ -383,9 +480,7 @@ __global__ void __launch_bounds__(kPackThreads)
     const uint64_t f = Pq + 16 * d;
     uint4 v = load_shifted(win + (f - win_off));
     const uint64_t valid = Q.len - 16 * d;  // >= 1
-    if (valid < 16) {
-      for (uint32_t i = uint32_t(valid); i < 16; ++i) set_byte(v, i, 0);
-    }
+    if (valid < 16) keep_prefix(v, uint32_t(valid));
     uint4* dstw = reinterpret_cast<uint4*>(Q.ptr) + d;
     *dstw = v;
     if (16 * (d + 1) >= Q.len) {  // last data word: zero the padding words
@@ -484,6 +579,33 @@ __global__ void __launch_bounds__(kGatherThreads)
   }
 }
 
+// Dirty chunks written by the SMs straight into the pinned image.  The host
+// destination may be misaligned: aligned 16-byte stores cover the interior,
+// byte stores the two edges.
+__global__ void __launch_bounds__(kGatherThreads)
+    k_gather_to_host(const crac_span_t* __restrict__ spans, const uint64_t* __restrict__ chunk_first,
+                     uint32_t n_spans, uint32_t chunk_bytes, const uint64_t* __restrict__ dirty,
+                     uint64_t first, uint64_t count, const uint64_t* __restrict__ dst_off,
+                     uint8_t* __restrict__ host) {
+  for (uint64_t k = blockIdx.x; k < count; k += gridDim.x) {
+    const uint64_t c = dirty[first + k];
+    const uint32_t s = find_span(chunk_first, n_spans, c);
+    const crac_span_t sp = spans[s];
+    const uint64_t off = (c - chunk_first[s]) * chunk_bytes;
+    const uint64_t len = min(uint64_t(chunk_bytes), sp.len - off);
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(sp.ptr + off);
+    uint8_t* dst = host + dst_off[s] + off;
+    const uint32_t head = uint32_t((16 - (reinterpret_cast<uint64_t>(dst) & 15)) & 15);
+    const uint32_t h = uint32_t(min(uint64_t(head), len));
+    for (uint32_t i = threadIdx.x; i < h; i += kGatherThreads) dst[i] = src[i];
+    const uint64_t body = (len - h) >> 4;
+    uint4* d4 = reinterpret_cast<uint4*>(dst + h);
+    for (uint64_t w = threadIdx.x; w < body; w += kGatherThreads)
+      d4[w] = load_shifted(src + h + 16 * w);
+    for (uint64_t i = h + 16 * body + threadIdx.x; i < len; i += kGatherThreads) dst[i] = src[i];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // fixtures
 // ---------------------------------------------------------------------------
@@ -579,8 +701,8 @@ int crac_gpu_init(void) {
     if (!e) e = cudaMemcpyToSymbol(g_xp16, h.xp16.data(), 33 * 4);
     if (!e) e = cudaMemcpyToSymbol(g_xpt, h.xpt.data(), 512 * 4);
     if (!e) e = cudaMemcpyToSymbol(g_pow2, h.pow2.data(), 64 * 4);
-    if (!e) e = cudaFuncSetAttribute(k1_chunk_crc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(kTabBytes));
+    for (auto k : {k1_chunk_crc<4>, k1_chunk_crc<8>, k1_chunk_crc<16>})
+      if (!e) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTabBytes));
     g_init_rc = int(e);
   });
   return g_init_rc;
@@ -588,14 +710,27 @@ int crac_gpu_init(void) {
 
 int crac_chunk_crc32(const crac_span_t* d_spans, const uint64_t* d_chunk_first, uint32_t n_spans,
                      uint32_t chunk_bytes, uint64_t total_chunks, uint32_t* d_crc, void* stream) {
-  if (total_chunks == 0) return 0;
+  return crac_chunk_crc32_range(d_spans, d_chunk_first, n_spans, chunk_bytes, 0, total_chunks,
+                                d_crc, 0, stream);
+}
+
+int crac_chunk_crc32_range(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
+                           uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
+                           uint32_t* d_crc, uint32_t max_ctas, void* stream) {
+  if (c_hi <= c_lo) return 0;
   if (chunk_bytes == 0 || chunk_bytes % 512) return int(cudaErrorInvalidValue);
   if (int rc = crac_gpu_init()) return rc;
-  const uint64_t warps_needed = total_chunks;
+  const uint64_t warps_needed = c_hi - c_lo;
   uint64_t blocks = (warps_needed + kK1Warps - 1) / kK1Warps;
-  if (blocks > uint64_t(sm_count())) blocks = sm_count();
-  k1_chunk_crc<<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
-      d_spans, d_chunk_first, n_spans, chunk_bytes, total_chunks, d_crc, k_full_for(chunk_bytes));
+  const uint64_t cap = max_ctas ? std::min<uint64_t>(max_ctas, sm_count()) : sm_count();
+  if (blocks > cap) blocks = cap;
+  static const int rows = [] {
+    const char* e = std::getenv("CRAC_K1_ROWS");
+    return e ? std::atoi(e) : 16;
+  }();
+  auto kern = rows == 4 ? k1_chunk_crc<4> : rows == 16 ? k1_chunk_crc<16> : k1_chunk_crc<8>;
+  kern<<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
+      d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, k_full_for(chunk_bytes));
   return int(cudaGetLastError());
 }
 
@@ -643,6 +778,19 @@ int crac_gather_chunks(const crac_span_t* d_spans, const uint64_t* d_chunk_first
   if (blocks > uint64_t(sm_count()) * 16) blocks = uint64_t(sm_count()) * 16;
   k_gather<<<unsigned(blocks), kGatherThreads, 0, cudaStream_t(stream)>>>(
       d_spans, d_chunk_first, n_spans, chunk_bytes, d_dirty_idx, first, count, d_staging);
+  return int(cudaGetLastError());
+}
+
+int crac_gather_chunks_to_host(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
+                               uint32_t n_spans, uint32_t chunk_bytes,
+                               const uint64_t* d_dirty_idx, uint64_t first, uint64_t count,
+                               const uint64_t* d_dst_off, uint8_t* host_image, void* stream) {
+  if (count == 0) return 0;
+  uint64_t blocks = count;
+  if (blocks > uint64_t(sm_count()) * 8) blocks = uint64_t(sm_count()) * 8;
+  k_gather_to_host<<<unsigned(blocks), kGatherThreads, 0, cudaStream_t(stream)>>>(
+      d_spans, d_chunk_first, n_spans, chunk_bytes, d_dirty_idx, first, count, d_dst_off,
+      host_image);
   return int(cudaGetLastError());
 }
 

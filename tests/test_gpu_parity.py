@@ -265,22 +265,38 @@ def test_managed_residence_restored(eng):
 # ---------------------------------------------------------------------------
 # incremental drain (new behaviour: must emit exactly the full image)
 # ---------------------------------------------------------------------------
+def _mutate_reference(r, sizes, ids, seed, epoch, threshold, chunk=65536):
+    """The C5 epoch mutation restated on the reference session (crac_gpu.h:
+    chunk c changes iff mix64(seed ^ (epoch << 40) ^ c) < threshold, new content
+    = synth(seed + epoch) of that chunk's words)."""
+    c = 0
+    for size, i in zip(sizes, ids):
+        for off in range(0, size, chunk):
+            if ref.mix64(seed ^ (epoch << 40) ^ c) < threshold:
+                n = min(chunk, size - off)
+                r.copy_h2d(i, off, ref.synth_bytes(seed + epoch, i, n, off // 8))
+            c += 1
+
+
 @pytest.mark.parametrize("pct", [0, 1, 25, 100])
 def test_incremental_equals_full(eng, pct):
+    sizes = [(4 << 20) - k * 4096 - (k % 2) * 100 for k in range(12)]
     s = eng.Session(seed=1, arena_bytes=64 << 20)
-    workloads.build_regions(s, 12, lambda r: (4 << 20) - r * 4096 - (r % 2) * 100, seed=3)
+    r = ref.RefSession(seed=1, arena_bytes=64 << 20)
+    ids = workloads.build_regions(s, 12, lambda k: sizes[k], seed=3)
+    assert workloads.build_regions(r, 12, lambda k: sizes[k], seed=3) == ids
     image = eng.Image()
     st0 = s.checkpoint_into(image)
     assert not st0["incremental"]
+    assert image.tobytes() == r.checkpoint()[0]
     threshold = (2**64 - 1) * pct // 100
     for epoch in range(1, 3):
         mutated = s.mutate(seed=3, epoch=epoch, threshold=threshold)
+        _mutate_reference(r, sizes, ids, 3, epoch, threshold)
         st = s.checkpoint_into(image, incremental=True)
         assert st["incremental"]
-        inc = image.tobytes()
-        full = s.checkpoint()[0]
-        assert inc == full
         assert st["dirty_chunks"] == mutated
+        assert image.tobytes() == r.checkpoint()[0]  # exactly the full image
 
 
 def test_incremental_falls_back_when_layout_changes(eng):
