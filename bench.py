@@ -48,6 +48,10 @@ def parse_args():
     ap.add_argument("--cpu-sample-gib", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-incremental", action="store_true")
+    ap.add_argument("--workload", choices=["c4", "c2", "c3", "c5"], default="c4")
+    ap.add_argument("--c2-calls", type=int, default=40000)
+    ap.add_argument("--c3-footprint-gib", type=float, default=16.0)
+    ap.add_argument("--c5-footprint-gib", type=float, default=64.0)
     return ap.parse_args()
 
 
@@ -265,6 +269,119 @@ def run_reference(args, world, rank) -> None:
 # ---------------------------------------------------------------------------
 # the B200 arm
 # ---------------------------------------------------------------------------
+def pcie_peaks(torch) -> dict:
+    """Copy-engine ceiling of this GPU's link: 2 GiB in 16 MiB pinned copies."""
+    chunk, n = 16 * MIB, 128
+    h = torch.empty(chunk * n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(chunk * n, dtype=torch.uint8, device="cuda")
+    out = {}
+    for name, (dst, src) in {"d2h": (h, d), "h2d": (d, h)}.items():
+        for _ in range(2):  # warm + measure
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for k in range(n):
+                dst[k * chunk:(k + 1) * chunk].copy_(src[k * chunk:(k + 1) * chunk], non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            out[name] = round(chunk * n / (e0.elapsed_time(e1) * 1e-3) / 1e9, 2)
+    del h, d
+    return out
+
+
+def build_workload(args, engine, rank: int, live_cap: int):
+    """Creates the resident state of the chosen config; returns
+    (session, live bytes, config dict)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import workloads
+    region = args.region_mib * MIB
+    seed = rank + 1
+    if args.workload in ("c4", "c5"):
+        want = args.footprint_gib if args.workload == "c4" else args.c5_footprint_gib
+        footprint = min(int(want * GIB), live_cap) // region * region
+        n = footprint // region
+        sess = engine.Session(seed=seed, arena_bytes=footprint + 64 * MIB)
+        workloads.build_regions(sess, n, lambda r: region, seed)
+        return sess, footprint, {"regions_per_gpu": n, "region_bytes": region,
+                                 "requested_footprint_gib": want}
+    if args.workload == "c2":
+        # Rodinia-style: 4 streams, 70 % alloc / 30 % free of 256 B..64 KiB Device
+        # buffers, one fill8 launch per allocation (alloc_churn, harness.cpp:476-499)
+        sess = engine.Session(seed=seed, arena_bytes=2 * GIB)
+        workloads.build_churn(sess, args.c2_calls, seed)
+        recs = sess.live_records()
+        return sess, sum(r.size for r in recs), {"calls": args.c2_calls, "live_regions": len(recs),
+                                                 "log_entries": sess.log_size(), "streams": 4}
+    if args.workload == "c3":
+        # HPGMG-style UVM: cudaMallocManaged regions, alternating 1 MiB runs of
+        # device- and host-resident pages (uvm_tasks, harness.cpp:345-389)
+        total = min(int(args.c3_footprint_gib * GIB), live_cap)
+        mregion = 256 * MIB
+        n = max(1, total // mregion)
+        sess = engine.Session(seed=seed, arena_bytes=n * mregion + 64 * MIB)
+        for _ in range(n):
+            i, _ = sess.alloc(engine.MANAGED, mregion)
+            sess.fill_synthetic(i, seed)  # device-side write: device-resident, dirty
+            for off in range(MIB, mregion, 2 * MIB):
+                sess.page_read(i, off, MIB, engine.HOST_SIDE)  # host touch: host-resident
+        return sess, n * mregion, {"managed_regions": n, "region_bytes": mregion,
+                                   "residence": "alternating 1 MiB runs device/host"}
+    raise SystemExit(f"unknown workload {args.workload}")
+
+
+WORKLOAD_NAMES = {
+    "c4": "C4: full checkpoint drain + restart refill of live device state, independent "
+          "per-GPU drains, host barrier",
+    "c2": "C2: Rodinia-style many small allocations on 4 streams, full checkpoint + restart",
+    "c3": "C3: HPGMG-style cudaMallocManaged footprint with mixed residence, checkpoint + "
+          "residency-restoring restart",
+    "c5": "C5: incremental checkpoint sequence at 1/5/25 % dirty chunks, hash-only vs drain",
+}
+
+
+def run_c5(args, engine, sess, image, live, group, rank, world, peaks) -> None:
+    """Incremental sequence (config C5): per dirty fraction, the hash-only pass
+    and the incremental drain, both device-timed."""
+    sess.checkpoint_into(image)  # full image; seeds the previous-epoch CRCs
+    rows = {}
+    epoch = 0
+    for pct in (1, 5, 25):
+        thr = (2**64 - 1) * pct // 100
+        hs, ds = [], []
+        for _ in range(args.warmup + args.steps):
+            epoch += 1
+            h = sess.hash_only()
+            sess.checkpoint_into(image)  # re-seed (hash_only invalidates the plan)
+            mutated = sess.mutate(seed=rank + 1, epoch=epoch, threshold=thr)
+            d = sess.checkpoint_into(image, incremental=True)
+            assert d["incremental"] and d["dirty_chunks"] == mutated
+            hs.append(h)
+            ds.append(d)
+        hs, ds = hs[args.warmup:], ds[args.warmup:]
+        h_ms = group.max(statistics.mean(h["hash_ms"] for h in hs))
+        d_ms = group.max(statistics.mean(d["total_ms"] for d in ds))
+        dirty = statistics.mean(d["d2h_bytes"] for d in ds)
+        rows[f"{pct}pct"] = {
+            "hash_only_ms": round(h_ms, 3),
+            "hash_GBps": round(live / (h_ms * 1e-3) / 1e9, 1),
+            "hash_frac_of_hbm": round(live / (h_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 3),
+            "drain_ms": round(d_ms, 3), "dirty_bytes": int(dirty),
+            "drain_roofline_ms": round(max(live / peaks["hbm_gbs"] / 1e6,
+                                           dirty / (peaks["pcie"]["d2h"] * 1e6)), 3),
+            "state_GBps": round(live * world / (d_ms * 1e-3) / 1e9, 1)}
+    if rank == 0:
+        r1 = rows["1pct"]
+        print(json.dumps({
+            "metric": "checkpoint & restart GB/s per GPU and whole box at 1/2/4/8 B200; % of roofline",
+            "value": r1["state_GBps"], "unit": "GB/s (live state covered by the incremental drain)",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": r1["drain_ms"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": WORKLOAD_NAMES["c5"], "live_bytes_per_gpu": live,
+                       "chunk_bytes": 65536},
+            "incremental": rows}), flush=True)
+
+
 def main() -> None:
     args = parse_args()
     world, rank, local, local_world = dist_env()
@@ -274,28 +391,28 @@ def main() -> None:
     pin_device(local, world)
 
     import torch
-    import torch.distributed as dist
     from paper_2008_10596_b200 import engine
 
     group = HostGroup(world, rank)
     barrier, max_over_ranks = group.barrier, group.max
 
     torch.cuda.set_device(0)
-    region = args.region_mib * MIB
     # host RAM bounds the per-rank image; HBM bounds the per-rank state
     host_cap = int(0.80 * mem_available() / local_world) - 8 * GIB
     dev_cap = int(torch.cuda.get_device_properties(0).total_memory * 0.85)
-    footprint = min(int(args.footprint_gib * GIB), host_cap, dev_cap) // region * region
-    n_regions = footprint // region
-    live = n_regions * region
+    peaks = measured_peaks()
+    peaks["pcie"] = pcie_peaks(torch)
+    hbm = peaks["hbm_gbs"]
 
     t_setup = time.perf_counter()
-    sess = engine.Session(seed=rank + 1, arena_bytes=live + 64 * MIB)
-    for _ in range(n_regions):
-        i, _ = sess.alloc(engine.DEVICE, region)
-        sess.fill_synthetic(i, rank + 1)
+    sess, live, cfg_extra = build_workload(args, engine, rank, min(host_cap, dev_cap))
     image = engine.Image()
     setup_s = time.perf_counter() - t_setup
+    if args.workload == "c5":
+        run_c5(args, engine, sess, image, live, group, rank, world, peaks)
+        sess.close()
+        group.close()
+        return
 
     def step(s):
         dr = s.checkpoint_into(image)
@@ -336,28 +453,26 @@ def main() -> None:
     refill_ms = max_over_ranks(sum(r["total_ms"] for r in refills) / args.steps)
 
     # kernel roofline: the kernel with the largest device time in the step
-    peaks = measured_peaks()
-    hbm = peaks["hbm_gbs"]
-    k1_ms = statistics.mean(d["hash_ms"] for d in drains)          # one payload launch
-    k1_bytes = drains[-1]["hash_bytes"] / max(drains[-1]["hash_launches"], 1)
-    pack_launches = drains[-1]["pack_launches"]
-    pack_ms_per = statistics.mean(d["pack_ms"] for d in drains) / max(pack_launches, 1)
-    pack_bytes = 2 * drains[-1]["pack_bytes"] / max(pack_launches, 1)   # read + write
-    scat_launches = refills[-1]["pack_launches"]
-    scat_ms_per = statistics.mean(r["pack_ms"] for r in refills) / max(scat_launches, 1)
-    scat_bytes = 2 * refills[-1]["pack_bytes"] / max(scat_launches, 1)
-    kernels = {
-        "k1_chunk_crc (drain)": (k1_ms, k1_bytes, 1),
-        "k_pack_records": (pack_ms_per, pack_bytes, pack_launches),
-        "k_scatter_records": (scat_ms_per, scat_bytes, scat_launches),
-    }
-    dom = max(kernels, key=lambda k: kernels[k][0] * kernels[k][2])
-    dom_ms, dom_bytes, _ = kernels[dom]
+    def mean(key, xs):
+        return statistics.mean(x[key] for x in xs)
+    kernels = {}
+    if drains[-1]["hash_launches"]:
+        kernels["k1_chunk_crc"] = (mean("hash_ms", drains) / drains[-1]["hash_launches"],
+                                   drains[-1]["hash_bytes"] / drains[-1]["hash_launches"],
+                                   drains[-1]["hash_launches"])
+    if drains[-1]["pack_launches"]:
+        n = drains[-1]["pack_launches"]
+        kernels["k_pack_records"] = (mean("pack_ms", drains), 2 * drains[-1]["pack_bytes"] / n, n)
+    if refills[-1]["pack_launches"]:
+        n = refills[-1]["pack_launches"]
+        kernels["k_scatter_records"] = (mean("pack_ms", refills), 2 * refills[-1]["pack_bytes"] / n, n)
+    dom = max(kernels, key=lambda k: kernels[k][0] * kernels[k][2]) if kernels else None
+    dom_ms, dom_bytes, _ = kernels[dom] if dom else (0.0, 0, 0)
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
 
-    # incremental (C5 shape on the resident state): hash-only and 1 % dirty drain
+    # incremental (C5 shape on the resident state): hash-only and a 1 % dirty drain
     incremental = None
-    if not args.no_incremental:
+    if not args.no_incremental and args.workload == "c4":
         h = sess.hash_only()
         sess.checkpoint_into(image)  # seeds the previous-image chunk CRCs
         thr = (2**64 - 1) // 100
@@ -374,26 +489,27 @@ def main() -> None:
 
     # reported CPU baseline (rank 0, N = 1 only)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.cpu_sample_gib, region)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c4":
+        cpu = cpu_baseline(args.cpu_sample_gib, args.region_mib * MIB)
 
     if rank == 0:
         value = 2 * live * world * args.steps / (dev_ms_max * 1e-3) / 1e9
         e2e = 2 * live * world * args.steps / (e2e_ms_max * 1e-3) / 1e9
         launches = sum(d["hash_launches"] + d["pack_launches"] for d in drains) + \
             sum(r["hash_launches"] + r["pack_launches"] for r in refills)
+        pd, ph = peaks["pcie"]["d2h"], peaks["pcie"]["h2d"]
+        link = 2 / (1 / pd + 1 / ph)  # one drain + one refill of the same bytes
+        d2h = drains[-1]["d2h_bytes"] / (mean("copy_ms", drains) * 1e-3) / 1e9 if mean("copy_ms", drains) else 0
+        h2d = refills[-1]["h2d_bytes"] / (mean("copy_ms", refills) * 1e-3) / 1e9 if mean("copy_ms", refills) else 0
         line = {
             "metric": "checkpoint & restart GB/s per GPU and whole box at 1/2/4/8 B200; % of roofline",
             "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(dev_ms_max / args.steps, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic",
-            "config": {"workload": "C4: full checkpoint drain + restart refill of live device "
-                                   "state, independent per-GPU drains, host barrier",
-                       "live_bytes_per_gpu": live, "regions_per_gpu": n_regions,
-                       "region_bytes": region, "requested_footprint_gib": args.footprint_gib,
-                       "parallelism": f"independent drains x{world}",
-                       "l2": "inputs larger than L2 (live state >> 126 MB)"},
+            "config": {"workload": WORKLOAD_NAMES[args.workload], "live_bytes_per_gpu": live,
+                       **cfg_extra, "parallelism": f"independent drains x{world}",
+                       "l2": "inputs larger than L2" if live > 256 * MIB else "inputs may fit L2"},
             "per_gpu": {"checkpoint_GBps": round(live / (drain_ms * 1e-3) / 1e9, 3),
                         "restart_GBps": round(live / (refill_ms * 1e-3) / 1e9, 3),
                         "checkpoint_ms": round(drain_ms, 3), "restart_ms": round(refill_ms, 3),
@@ -403,8 +519,11 @@ def main() -> None:
                          "traffic": None, "peak_source": peaks["source"],
                          "algorithmic_bytes_per_launch": int(dom_bytes),
                          "avg_launch_ms": round(dom_ms, 4)},
-            "pcie_roofline": {"d2h_GBps": round(drains[-1]["d2h_bytes"] / (statistics.mean(d["copy_ms"] for d in drains) * 1e-3) / 1e9, 2),
-                              "h2d_GBps": round(refills[-1]["h2d_bytes"] / (statistics.mean(r["copy_ms"] for r in refills) * 1e-3) / 1e9, 2)},
+            "pcie_roofline": {"d2h_GBps": round(d2h, 2), "h2d_GBps": round(h2d, 2),
+                              "d2h_peak_GBps": pd, "h2d_peak_GBps": ph,
+                              "peak_source": "measured in this run (16 MiB pinned copies)",
+                              "binding_GBps": round(link, 2),
+                              "value_frac": round(value / world / link, 4)},
             "e2e": {"value": round(e2e, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": refills[-1]["h2d_bytes"],
                     "d2h_bytes_per_step": drains[-1]["d2h_bytes"],

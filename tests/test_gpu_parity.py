@@ -309,3 +309,36 @@ def test_incremental_falls_back_when_layout_changes(eng):
     st = s.checkpoint_into(image, incremental=True)
     assert not st["incremental"]
     assert image.tobytes() == s.checkpoint()[0]
+
+
+# ---------------------------------------------------------------------------
+# config shapes: C2 churn, C3 managed with mixed residence
+# ---------------------------------------------------------------------------
+def test_c2_churn_matches_reference(eng):
+    s = eng.Session(seed=2, arena_bytes=256 << 20)
+    r = ref.RefSession(seed=2, arena_bytes=256 << 20)
+    for api in (s, r):
+        workloads.build_churn(api, 3000, seed=5, max_size=16384)
+    img, st = s.checkpoint()
+    assert img == r.checkpoint()[0]
+    rs, _ = eng.restart(img)
+    assert rs.checkpoint()[0] == img
+    assert _state(rs) == _state(s)
+
+
+def test_c3_managed_mixed_residence_matches_reference(eng):
+    s = eng.Session(seed=3, arena_bytes=64 << 20)
+    r = ref.RefSession(seed=3, arena_bytes=64 << 20)
+    for api in (s, r):
+        for k in range(6):
+            i, _ = api.alloc(workloads.MANAGED, (1 << 20) + 4096 * k + 123 * (k % 2))
+            api.fill_synthetic(i, 7, workloads.DEVICE_SIDE)
+            for off in range(64 << 10, 1 << 20, 128 << 10):
+                api.page_read(i, off, 64 << 10, workloads.HOST_SIDE)
+        d, _ = api.alloc(workloads.DEVICE, 100000)
+        api.fill_synthetic(d, 7)
+    img, _ = s.checkpoint()
+    assert img == r.checkpoint()[0]
+    rs, _ = eng.restart(img)
+    assert _state(rs) == _state(s)
+    assert rs.checkpoint()[0] == img
