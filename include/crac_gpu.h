@@ -71,6 +71,16 @@ int crac_chunk_crc32_range(const crac_span_t* d_spans, const uint64_t* d_chunk_f
                            uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
                            uint32_t* d_crc, uint32_t max_ctas, void* stream);
 
+/* Fused incremental drain (K1 + K2b in one pass): hashes chunks [c_lo, c_hi)
+ * into d_crc; every chunk whose CRC differs from d_crc_prev is written by the
+ * hashing warp straight into host_image + d_dst_off[span] + chunk offset
+ * (pinned, UVA-mapped) and its d_crc_prev entry updated.  d_counters[0] +=
+ * dirty chunks, d_counters[1] += dirty bytes (caller zeroes them). */
+int crac_hash_drain_range(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
+                          uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
+                          uint32_t* d_crc, uint32_t* d_crc_prev, const uint64_t* d_dst_off,
+                          uint8_t* host_image, unsigned long long* d_counters, void* stream);
+
 /* Incremental drain straight to the host image: dirty chunk k (index
  * d_dirty_idx[first + k]) of payload span s is written by the SMs to
  * host_image + d_dst_off[s] + chunk offset (pinned, UVA-mapped memory). */
@@ -78,6 +88,15 @@ int crac_gather_chunks_to_host(const crac_span_t* d_spans, const uint64_t* d_chu
                                uint32_t n_spans, uint32_t chunk_bytes,
                                const uint64_t* d_dirty_idx, uint64_t first, uint64_t count,
                                const uint64_t* d_dst_off, uint8_t* host_image, void* stream);
+
+/* Same as crac_gather_chunks_to_host over d_dirty_idx[0 .. *d_count) where
+ * the count is read on the device (no host round trip after the diff);
+ * max_count bounds it, max_ctas caps the grid (0 = 8 per SM). */
+int crac_gather_chunks_to_host_dev(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
+                                   uint32_t n_spans, uint32_t chunk_bytes,
+                                   const uint64_t* d_dirty_idx, const uint64_t* d_count,
+                                   uint64_t max_count, uint32_t max_ctas,
+                                   const uint64_t* d_dst_off, uint8_t* host_image, void* stream);
 
 /* K2a: writes stream bytes [win_off, win_off + win_len) into d_out (16-byte
  * aligned; win_off multiple of 16).  Records sorted by out_off; bytes not
@@ -102,6 +121,12 @@ int crac_scatter_records(const crac_record_t* d_recs, uint32_t n_recs,
 int crac_diff_compact(const uint32_t* d_crc_new, uint32_t* d_crc_prev, uint64_t n_chunks,
                       uint32_t* d_block_counts, uint64_t* d_dirty_idx, uint64_t* d_dirty_count,
                       void* stream);
+
+/* crac_diff_compact over the chunk range [c_lo, c_hi): indices written are
+ * absolute; d_block_counts needs ceil((c_hi - c_lo) / 4096) entries. */
+int crac_diff_compact_range(const uint32_t* d_crc_new, uint32_t* d_crc_prev, uint64_t c_lo,
+                            uint64_t c_hi, uint32_t* d_block_counts, uint64_t* d_dirty_idx,
+                            uint64_t* d_dirty_count, void* stream);
 
 /* Copies dirty chunks d_dirty_idx[first .. first+count) (chunk numbering as in
  * crac_chunk_crc32) to d_staging + k * chunk_bytes, k = 0..count-1. */

@@ -67,7 +67,7 @@ std::map<uint64_t, uint64_t> replay_log(
           diverged(e, "id " + std::to_string(rec.id) + " != logged " + std::to_string(e.id));
         if (rec.address != e.address)
           diverged(e, "address mismatch for allocation " + std::to_string(e.id));
-        placed.emplace(e.seq, rec.address);
+        placed.emplace_hint(placed.end(), e.seq, rec.address);  // seq ascends
         break;
       }
       case LogOp::Free: ctx.free(e.id); break;

@@ -141,6 +141,7 @@ DrainEngine::~DrainEngine() {
   d_block_counts.release();
   d_dirty_idx.release();
   d_dirty_count.release();
+  d_counters.release();
   h_pay_crc.release();
   h_page_crc.release();
   h_count.release();
@@ -299,13 +300,33 @@ const Shift& shift_for(uint64_t n) {
   return n == 16 ? s16 : n == 4096 ? s4k : s64k;
 }
 
+// Shift by any length < 2^17 as a product of power-of-two shifts, four table
+// lookups per set bit (chunk tails and odd record lengths); longer lengths
+// fall back to bit-serial multiplication.
+const Shift* pow2_shifts() {
+  static const std::vector<Shift>* t = [] {
+    auto* v = new std::vector<Shift>();
+    for (int k = 0; k < 17; ++k) v->emplace_back(uint64_t(1) << k);
+    return v;
+  }();
+  return t->data();
+}
+
+uint32_t advance_any(uint32_t v, uint64_t len) {
+  if (len >> 17) return crac::advance(v, len, pow2_table());
+  const Shift* p = pow2_shifts();
+  for (int k = 0; len; ++k, len >>= 1)
+    if (len & 1) v = p[k](v);
+  return v;
+}
+
 struct Fold {
   uint32_t acc = 0;
   void add(uint32_t crc, uint64_t len) {
     if (len == 16 || len == 4096 || len == 65536)
       acc = shift_for(len)(acc) ^ crc;
     else
-      acc = crac::advance(acc, len, pow2_table()) ^ crc;
+      acc = advance_any(acc, len) ^ crc;
   }
 };
 
@@ -915,53 +936,35 @@ void incremental_locked(Session& session, PinnedImage& image, DrainStats* stats)
   uint8_t* img = image.mutable_data();
   const uint64_t s3 = P.s3;
 
-  // 1. K1 over everything, 2. diff + ordered compaction (K2b)
+  // One fused pass (K1 + K2b): every warp hashes its chunks and, where the
+  // CRC differs from the previous image's, writes the chunk straight into the
+  // pinned image; the PCIe writes of dirty chunks overlap the hashing.
   const uint64_t n = P.pay_first.back();
-  check_cuda(cudaEventRecord(E.ev_h0, E.s_pack), "event");
-  hash_payloads(E, P, 0, n, 0, E.s_pack);
-  check_cuda(cudaEventRecord(E.ev_h1, E.s_pack), "event");
-  E.d_block_counts.ensure((n + 4095) / 4096 + 1);
-  E.d_dirty_idx.ensure(std::max<uint64_t>(n, 1));
-  E.d_dirty_count.ensure(1);
-  E.h_count.ensure(1);
-  check_cuda(cudaError_t(crac_diff_compact(E.d_pay_crc.ptr, E.d_prev_crc.ptr, n,
-                                           E.d_block_counts.ptr, E.d_dirty_idx.ptr,
-                                           E.d_dirty_count.ptr, E.s_pack)),
-             "diff");
-  check_cuda(cudaMemcpyAsync(E.h_count.ptr, E.d_dirty_count.ptr, 8, cudaMemcpyDeviceToHost, E.s_pack),
-             "count");
-  download_crcs(E, P, E.s_pack);
-  check_cuda(cudaStreamSynchronize(E.s_pack), "diff sync");
-  tr.mark("hash+diff");
-  const uint64_t dirty = E.h_count.ptr[0];
-
-  // 3. the SMs write every dirty chunk straight into the pinned image (one
-  //    launch; the PCIe writes overlap the host-side fold below)
-  if (dirty) {
-    if (E.dst_for_image != P.image_ptr) {
-      std::vector<uint64_t> dst(P.pay_rec_off.size());
-      for (size_t s = 0; s < dst.size(); ++s) dst[s] = s3 + P.pay_rec_off[s];
-      upload(E.d_pay_dst, dst, E.s_copy);
-      E.dst_for_image = P.image_ptr;
-    }
-    check_cuda(cudaEventRecord(E.ev_c0, E.s_copy), "event");
-    check_cuda(cudaError_t(crac_gather_chunks_to_host(
-                   E.d_pay_spans.ptr, E.d_pay_first.ptr, uint32_t(P.pay_spans.size()),
-                   DrainEngine::kChunk, E.d_dirty_idx.ptr, 0, dirty, E.d_pay_dst.ptr, img, E.s_copy)),
-               "gather to host");
-    check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
-    if (stats) {
-      E.h_dirty_idx.ensure(dirty);
-      check_cuda(cudaMemcpyAsync(E.h_dirty_idx.ptr, E.d_dirty_idx.ptr, dirty * 8,
-                                 cudaMemcpyDeviceToHost, E.s_copy),
-                 "dirty idx");
-    }
+  E.d_counters.ensure(2);
+  E.h_count.ensure(2);
+  if (E.dst_for_image != P.image_ptr) {
+    std::vector<uint64_t> dst(P.pay_rec_off.size());
+    for (size_t s = 0; s < dst.size(); ++s) dst[s] = s3 + P.pay_rec_off[s];
+    upload(E.d_pay_dst, dst, E.s_pack);
+    E.dst_for_image = P.image_ptr;
   }
+  check_cuda(cudaMemsetAsync(E.d_counters.ptr, 0, 16, E.s_pack), "counters");
+  check_cuda(cudaEventRecord(E.ev_h0, E.s_pack), "event");
+  check_cuda(cudaError_t(crac_hash_drain_range(
+                 E.d_pay_spans.ptr, E.d_pay_first.ptr, uint32_t(P.pay_spans.size()),
+                 DrainEngine::kChunk, 0, n, E.d_pay_crc.ptr, E.d_prev_crc.ptr, E.d_pay_dst.ptr, img,
+                 E.d_counters.ptr, E.s_pack)),
+             "hash+drain");
+  check_cuda(cudaEventRecord(E.ev_h1, E.s_pack), "event");
+  check_cuda(cudaMemcpyAsync(E.h_count.ptr, E.d_counters.ptr, 16, cudaMemcpyDeviceToHost, E.s_pack),
+             "counters");
+  download_crcs(E, P, E.s_pack);
+  check_cuda(cudaStreamSynchronize(E.s_pack), "hash sync");
+  tr.mark("hash+drain");
+  const uint64_t dirty = E.h_count.ptr[0], dirty_bytes = E.h_count.ptr[1];
   uint32_t crc3 = 0, crc4 = 0;
   fold_sections(E, P, crc3, crc4);
   tr.mark("fold");
-  check_cuda(cudaStreamSynchronize(E.s_copy), "gather sync");
-  tr.mark("gather");
   put_at<uint32_t>(img + s3 + P.len3, crc3);
   put_at<uint32_t>(img + s3 + P.stream_len, crc4);
 
@@ -977,16 +980,14 @@ void incremental_locked(Session& session, PinnedImage& image, DrainStats* stats)
   check_cuda(cudaEventRecord(E.ev_t1, E.s_pack), "event");
   check_cuda(cudaEventSynchronize(E.ev_t1), "event sync");
   if (stats) {
-    uint64_t bytes = 0;
-    for (uint64_t k = 0; k < dirty; ++k) bytes += chunk_len(P, E.h_dirty_idx.ptr[k]);
     stats->total_ms = elapsed(E.ev_t0, E.ev_t1);
     stats->hash_ms = elapsed(E.ev_h0, E.ev_h1);
     stats->hash_launches = 1;
     stats->hash_bytes = hashed_bytes(P);
-    stats->copy_ms = dirty ? elapsed(E.ev_c0, E.ev_c1) : 0;
-    stats->pack_launches = dirty ? 1 : 0;
-    stats->pack_bytes = bytes;
-    stats->d2h_bytes = bytes;
+    stats->copy_ms = stats->hash_ms;  // the drain writes ride inside the hash pass
+    stats->pack_launches = 0;
+    stats->pack_bytes = dirty_bytes;
+    stats->d2h_bytes = dirty_bytes;
     stats->image_bytes = P.image_bytes;
     stats->dirty_chunks = dirty;
     stats->total_chunks = n;

@@ -88,6 +88,7 @@ struct DrainEngine {
   DevArray<uint64_t> d_pay_first, d_page_first, d_pay_dst;
   DevArray<uint32_t> d_pay_crc, d_page_crc, d_prev_crc, d_block_counts;
   DevArray<uint64_t> d_dirty_idx, d_dirty_count;
+  DevArray<unsigned long long> d_counters;
   HostArray<uint32_t> h_pay_crc, h_page_crc;
   HostArray<uint64_t> h_count, h_dirty_idx;
 

@@ -163,6 +163,35 @@ __device__ __forceinline__ uint32_t find_span(const uint64_t* chunk_first, uint3
   return lo;
 }
 
+// ---------------------------------------------------------------------------
+// byte-shift helper: the 16 bytes starting at byte d (0..15) of (a || b)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 shift16(uint4 a, uint4 b, uint32_t d) {
+  uint32_t x0, x1, x2, x3, x4;
+  switch (d >> 2) {
+    case 0: x0 = a.x; x1 = a.y; x2 = a.z; x3 = a.w; x4 = b.x; break;
+    case 1: x0 = a.y; x1 = a.z; x2 = a.w; x3 = b.x; x4 = b.y; break;
+    case 2: x0 = a.z; x1 = a.w; x2 = b.x; x3 = b.y; x4 = b.z; break;
+    default: x0 = a.w; x1 = b.x; x2 = b.y; x3 = b.z; x4 = b.w; break;
+  }
+  const uint32_t sh = (d & 3) * 8;
+  uint4 r;
+  r.x = __funnelshift_r(x0, x1, sh);
+  r.y = __funnelshift_r(x1, x2, sh);
+  r.z = __funnelshift_r(x2, x3, sh);
+  r.w = __funnelshift_r(x3, x4, sh);
+  return r;
+}
+
+__device__ __forceinline__ uint4 load_shifted(const uint8_t* p) {
+  const uint64_t a = reinterpret_cast<uint64_t>(p);
+  const uint4* q = reinterpret_cast<const uint4*>(a & ~uint64_t(15));
+  const uint32_t d = uint32_t(a & 15);
+  const uint4 lo = q[0];
+  if (d == 0) return lo;
+  return shift16(lo, q[1], d);
+}
+
 // Runs one lane's column over `rows` rows of 512 B starting at p (the lane's
 // first word).  Loads of the next kRows rows are in flight while the current
 // kRows rows are hashed.  The last row uses group A (no trailing gap).
@@ -198,11 +227,51 @@ __device__ __forceinline__ uint32_t k1_rows(const LaneLut& lut, const uint8_t* p
 // ---------------------------------------------------------------------------
 // K1
 // ---------------------------------------------------------------------------
-template <int kRows>
+// Fused incremental drain (K1 + K2b in one pass): after a chunk is hashed,
+// the same warp compares it with the previous image's CRC and, if it changed,
+// writes the chunk straight into the pinned host image at its final offset.
+// PCIe writes of dirty chunks overlap the hashing of the others; no
+// compaction list, no host round trip, one read of HBM (plus an L2/HBM
+// re-read of dirty chunks only).
+struct HashDrain {
+  uint32_t* prev;                // previous chunk CRCs; updated for dirty chunks
+  const uint64_t* dst_off;       // per span: image offset of its first payload byte
+  uint8_t* host;                 // pinned image (UVA)
+  unsigned long long* counters;  // [0] dirty chunks, [1] dirty bytes
+};
+
+__device__ __forceinline__ void chunk_to_host(uint8_t* dst, const uint8_t* src, uint32_t len,
+                                              uint32_t lane) {
+  if ((reinterpret_cast<uint64_t>(dst) & 15) == 0) {
+    const uint32_t words = len >> 4;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (uint32_t w0 = lane; w0 < words; w0 += 32 * 8) {
+      uint4 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (w0 + 32 * k < words) v[k] = s4[w0 + 32 * k];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (w0 + 32 * k < words) d4[w0 + 32 * k] = v[k];
+    }
+    for (uint32_t i = (words << 4) + lane; i < len; i += 32) dst[i] = src[i];
+    return;
+  }
+  const uint32_t head = uint32_t((16 - (reinterpret_cast<uint64_t>(dst) & 15)) & 15);
+  const uint32_t h = head < len ? head : len;
+  for (uint32_t i = lane; i < h; i += 32) dst[i] = src[i];
+  const uint32_t body = (len - h) >> 4;
+  uint4* d4 = reinterpret_cast<uint4*>(dst + h);
+  for (uint32_t w = lane; w < body; w += 32) d4[w] = load_shifted(src + h + 16 * w);
+  for (uint32_t i = h + 16 * body + lane; i < len; i += 32) dst[i] = src[i];
+}
+
+template <int kRows, bool kDrain>
 __global__ void __launch_bounds__(kK1Threads, 1)
     k1_chunk_crc(const crac_span_t* __restrict__ spans, const uint64_t* __restrict__ chunk_first,
                  uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
-                 uint32_t* __restrict__ out, uint32_t k_full) {
+                 uint32_t* __restrict__ out, uint32_t k_full, HashDrain hd) {
   extern __shared__ __align__(16) uint32_t s_tab[];
   {
     const uint4* src = reinterpret_cast<const uint4*>(g_tab);
@@ -253,37 +322,22 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         L = crac::gf_mul(g_xpt[t], L) ^ lt;
       }
     }
-    if (lane == 0) out[c] = L ^ (len == chunk_bytes ? k_full : crac::crc_affine(len, g_pow2));
+    if (lane == 0) L ^= (len == chunk_bytes ? k_full : crac::crc_affine(len, g_pow2));
+    if (!kDrain) {
+      if (lane == 0) out[c] = L;
+      continue;
+    }
+    const uint32_t crc = __shfl_sync(0xFFFFFFFFu, L, 0);
+    if (lane == 0) out[c] = crc;
+    if (crc != hd.prev[c]) {  // warp-uniform
+      if (lane == 0) {
+        hd.prev[c] = crc;
+        atomicAdd(&hd.counters[0], 1ull);
+        atomicAdd(&hd.counters[1], (unsigned long long)len);
+      }
+      chunk_to_host(hd.host + hd.dst_off[s] + off, base, len, lane);
+    }
   }
-}
-
-// ---------------------------------------------------------------------------
-// byte-shift helper: the 16 bytes starting at byte d (0..15) of (a || b)
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint4 shift16(uint4 a, uint4 b, uint32_t d) {
-  uint32_t x0, x1, x2, x3, x4;
-  switch (d >> 2) {
-    case 0: x0 = a.x; x1 = a.y; x2 = a.z; x3 = a.w; x4 = b.x; break;
-    case 1: x0 = a.y; x1 = a.z; x2 = a.w; x3 = b.x; x4 = b.y; break;
-    case 2: x0 = a.z; x1 = a.w; x2 = b.x; x3 = b.y; x4 = b.z; break;
-    default: x0 = a.w; x1 = b.x; x2 = b.y; x3 = b.z; x4 = b.w; break;
-  }
-  const uint32_t sh = (d & 3) * 8;
-  uint4 r;
-  r.x = __funnelshift_r(x0, x1, sh);
-  r.y = __funnelshift_r(x1, x2, sh);
-  r.z = __funnelshift_r(x2, x3, sh);
-  r.w = __funnelshift_r(x3, x4, sh);
-  return r;
-}
-
-__device__ __forceinline__ uint4 load_shifted(const uint8_t* p) {
-  const uint64_t a = reinterpret_cast<uint64_t>(p);
-  const uint4* q = reinterpret_cast<const uint4*>(a & ~uint64_t(15));
-  const uint32_t d = uint32_t(a & 15);
-  const uint4 lo = q[0];
-  if (d == 0) return lo;
-  return shift16(lo, q[1], d);
 }
 
 __device__ __forceinline__ void set_byte(uint4& v, uint32_t i, uint32_t b) {
@@ -520,7 +574,7 @@ __global__ void __launch_bounds__(kDiffThreads)
 __global__ void __launch_bounds__(kDiffThreads)
     k_diff_write(const uint32_t* __restrict__ a, uint32_t* __restrict__ b, uint64_t n,
                  const uint32_t* __restrict__ block_counts, uint64_t* __restrict__ idx,
-                 uint64_t* __restrict__ count) {
+                 uint64_t* __restrict__ count, uint64_t index_base) {
   __shared__ uint64_t s_base;
   __shared__ uint32_t s_warp[kDiffThreads / 32];
   // block offset = sum of the counts of all preceding blocks
@@ -551,7 +605,7 @@ __global__ void __launch_bounds__(kDiffThreads)
   for (uint32_t w = 0; w < warp; ++w) before += s_warp[w];
   uint64_t pos = s_base + before + incl - mine;
   for (uint32_t k = 0; k < kDiffPerThread; ++k)
-    if (mask & (1u << k)) idx[pos++] = i0 + k;
+    if (mask & (1u << k)) idx[pos++] = index_base + i0 + k;
   if (blockIdx.x + 1 == gridDim.x && threadIdx.x == kDiffThreads - 1) *count = pos;
   __syncthreads();
   for (uint32_t k = 0; k < kDiffPerThread; ++k) {
@@ -585,8 +639,9 @@ __global__ void __launch_bounds__(kGatherThreads)
 __global__ void __launch_bounds__(kGatherThreads)
     k_gather_to_host(const crac_span_t* __restrict__ spans, const uint64_t* __restrict__ chunk_first,
                      uint32_t n_spans, uint32_t chunk_bytes, const uint64_t* __restrict__ dirty,
-                     uint64_t first, uint64_t count, const uint64_t* __restrict__ dst_off,
-                     uint8_t* __restrict__ host) {
+                     uint64_t first, uint64_t count, const uint64_t* __restrict__ d_count,
+                     const uint64_t* __restrict__ dst_off, uint8_t* __restrict__ host) {
+  if (d_count) count = min(count, *d_count);  // produced on the device by the diff
   for (uint64_t k = blockIdx.x; k < count; k += gridDim.x) {
     const uint64_t c = dirty[first + k];
     const uint32_t s = find_span(chunk_first, n_spans, c);
@@ -595,6 +650,11 @@ __global__ void __launch_bounds__(kGatherThreads)
     const uint64_t len = min(uint64_t(chunk_bytes), sp.len - off);
     const uint8_t* src = reinterpret_cast<const uint8_t*>(sp.ptr + off);
     uint8_t* dst = host + dst_off[s] + off;
+    if ((reinterpret_cast<uint64_t>(dst) & 15) == 0 && len == kTileWords * 16) {
+      // aligned full chunk: every load in flight before the PCIe stores
+      tile_copy(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), kTileWords, 0);
+      continue;
+    }
     const uint32_t head = uint32_t((16 - (reinterpret_cast<uint64_t>(dst) & 15)) & 15);
     const uint32_t h = uint32_t(min(uint64_t(head), len));
     for (uint32_t i = threadIdx.x; i < h; i += kGatherThreads) dst[i] = src[i];
@@ -701,7 +761,8 @@ int crac_gpu_init(void) {
     if (!e) e = cudaMemcpyToSymbol(g_xp16, h.xp16.data(), 33 * 4);
     if (!e) e = cudaMemcpyToSymbol(g_xpt, h.xpt.data(), 512 * 4);
     if (!e) e = cudaMemcpyToSymbol(g_pow2, h.pow2.data(), 64 * 4);
-    for (auto k : {k1_chunk_crc<4>, k1_chunk_crc<8>, k1_chunk_crc<16>})
+    for (auto k : {k1_chunk_crc<4, false>, k1_chunk_crc<8, false>, k1_chunk_crc<16, false>,
+                   k1_chunk_crc<16, true>})
       if (!e) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTabBytes));
     g_init_rc = int(e);
   });
@@ -728,9 +789,26 @@ int crac_chunk_crc32_range(const crac_span_t* d_spans, const uint64_t* d_chunk_f
     const char* e = std::getenv("CRAC_K1_ROWS");
     return e ? std::atoi(e) : 16;
   }();
-  auto kern = rows == 4 ? k1_chunk_crc<4> : rows == 16 ? k1_chunk_crc<16> : k1_chunk_crc<8>;
+  auto kern = rows == 4 ? k1_chunk_crc<4, false>
+              : rows == 16 ? k1_chunk_crc<16, false> : k1_chunk_crc<8, false>;
   kern<<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
-      d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, k_full_for(chunk_bytes));
+      d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, k_full_for(chunk_bytes),
+      HashDrain{});
+  return int(cudaGetLastError());
+}
+
+int crac_hash_drain_range(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
+                          uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
+                          uint32_t* d_crc, uint32_t* d_crc_prev, const uint64_t* d_dst_off,
+                          uint8_t* host_image, unsigned long long* d_counters, void* stream) {
+  if (c_hi <= c_lo) return 0;
+  if (chunk_bytes == 0 || chunk_bytes % 512) return int(cudaErrorInvalidValue);
+  if (int rc = crac_gpu_init()) return rc;
+  uint64_t blocks = (c_hi - c_lo + kK1Warps - 1) / kK1Warps;
+  if (blocks > uint64_t(sm_count())) blocks = sm_count();
+  k1_chunk_crc<16, true><<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
+      d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, k_full_for(chunk_bytes),
+      HashDrain{d_crc_prev, d_dst_off, host_image, d_counters});
   return int(cudaGetLastError());
 }
 
@@ -765,7 +843,22 @@ int crac_diff_compact(const uint32_t* d_crc_new, uint32_t* d_crc_prev, uint64_t 
                                                           d_block_counts);
   k_diff_write<<<unsigned(blocks), kDiffThreads, 0, st>>>(d_crc_new, d_crc_prev, n_chunks,
                                                           d_block_counts, d_dirty_idx,
-                                                          d_dirty_count);
+                                                          d_dirty_count, 0);
+  return int(cudaGetLastError());
+}
+
+int crac_diff_compact_range(const uint32_t* d_crc_new, uint32_t* d_crc_prev, uint64_t c_lo,
+                            uint64_t c_hi, uint32_t* d_block_counts, uint64_t* d_dirty_idx,
+                            uint64_t* d_dirty_count, void* stream) {
+  cudaStream_t st = cudaStream_t(stream);
+  const uint64_t n = c_hi > c_lo ? c_hi - c_lo : 0;
+  if (n == 0) return int(cudaMemsetAsync(d_dirty_count, 0, 8, st));
+  const uint64_t blocks = (n + kDiffPerBlock - 1) / kDiffPerBlock;
+  k_diff_count<<<unsigned(blocks), kDiffThreads, 0, st>>>(d_crc_new + c_lo, d_crc_prev + c_lo, n,
+                                                          d_block_counts);
+  k_diff_write<<<unsigned(blocks), kDiffThreads, 0, st>>>(d_crc_new + c_lo, d_crc_prev + c_lo, n,
+                                                          d_block_counts, d_dirty_idx,
+                                                          d_dirty_count, c_lo);
   return int(cudaGetLastError());
 }
 
@@ -789,7 +882,22 @@ int crac_gather_chunks_to_host(const crac_span_t* d_spans, const uint64_t* d_chu
   uint64_t blocks = count;
   if (blocks > uint64_t(sm_count()) * 8) blocks = uint64_t(sm_count()) * 8;
   k_gather_to_host<<<unsigned(blocks), kGatherThreads, 0, cudaStream_t(stream)>>>(
-      d_spans, d_chunk_first, n_spans, chunk_bytes, d_dirty_idx, first, count, d_dst_off,
+      d_spans, d_chunk_first, n_spans, chunk_bytes, d_dirty_idx, first, count, nullptr, d_dst_off,
+      host_image);
+  return int(cudaGetLastError());
+}
+
+int crac_gather_chunks_to_host_dev(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
+                                   uint32_t n_spans, uint32_t chunk_bytes,
+                                   const uint64_t* d_dirty_idx, const uint64_t* d_count,
+                                   uint64_t max_count, uint32_t max_ctas,
+                                   const uint64_t* d_dst_off, uint8_t* host_image, void* stream) {
+  if (max_count == 0) return 0;
+  uint64_t blocks = max_count;
+  const uint64_t cap = max_ctas ? max_ctas : uint64_t(sm_count()) * 8;
+  if (blocks > cap) blocks = cap;
+  k_gather_to_host<<<unsigned(blocks), kGatherThreads, 0, cudaStream_t(stream)>>>(
+      d_spans, d_chunk_first, n_spans, chunk_bytes, d_dirty_idx, 0, max_count, d_count, d_dst_off,
       host_image);
   return int(cudaGetLastError());
 }
