@@ -98,6 +98,16 @@ int crac_gather_chunks_to_host_dev(const crac_span_t* d_spans, const uint64_t* d
                                    uint64_t max_count, uint32_t max_ctas,
                                    const uint64_t* d_dst_off, uint8_t* host_image, void* stream);
 
+/* K4: the linear parts of the ALLOC_PAYLOADS and UVM_PAGES CRCs from chunk
+ * and page CRCs plus the frame bytes (d_out[0], d_out[1]; the caller xors in
+ * K(section length) = crc32 of that many zero bytes' affine term).  Records
+ * as for crac_pack_records, sec3 first (record i <-> payload span i), the
+ * 20-byte gap record at len3, then sec4 with page records carrying their page
+ * CRC index in `reserved`. */
+int crac_fold_sections(const crac_record_t* d_recs, uint32_t n_recs, const uint64_t* d_pay_first,
+                       const uint32_t* d_pay_crc, uint32_t n_pay, const uint32_t* d_page_crc,
+                       uint64_t len3, uint64_t total_pay_chunks, uint32_t* d_out, void* stream);
+
 /* K2a: writes stream bytes [win_off, win_off + win_len) into d_out (16-byte
  * aligned; win_off multiple of 16).  Records sorted by out_off; bytes not
  * covered by any record are written as zero.  d_tile_rec[t] = first record

@@ -31,6 +31,31 @@ class HoleIndex {
     root_ = merge(a, c);
   }
 
+  // Re-keys / resizes the hole starting at `addr` in place.  The caller
+  // guarantees ordering is preserved (no other hole between the old and the
+  // new start) — true for the allocator's split and merge steps, which only
+  // move a hole's boundary inside the gap it already occupies.
+  void update(uint64_t addr, uint64_t new_addr, uint64_t new_len) {
+    int path[128];
+    int depth = 0;
+    for (int t = root_; t >= 0;) {
+      if (depth == 128) {  // pathological depth: fall back to erase + insert
+        erase(addr);
+        insert(new_addr, new_len);
+        return;
+      }
+      path[depth++] = t;
+      Node& n = nodes_[t];
+      if (n.key == addr) {
+        n.key = new_addr;
+        n.len = new_len;
+        while (depth) pull(path[--depth]);
+        return;
+      }
+      t = addr < n.key ? n.l : n.r;
+    }
+  }
+
   // Lowest-address hole whose length is at least `need`.
   bool first_fit(uint64_t need, uint64_t& addr, uint64_t& len) const {
     int t = root_;

@@ -30,6 +30,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <atomic>
 #include <mutex>
 #include <set>
 #include <thread>
@@ -142,8 +143,8 @@ DrainEngine::~DrainEngine() {
   d_dirty_idx.release();
   d_dirty_count.release();
   d_counters.release();
-  h_pay_crc.release();
-  h_page_crc.release();
+  d_fold.release();
+  h_fold.release();
   h_count.release();
   h_dirty_idx.release();
   cudaStreamDestroy(s_pack);
@@ -266,7 +267,7 @@ void PinnedImage::prepare(uint64_t size, uint64_t align_at) {
 }
 
 // ---------------------------------------------------------------------------
-// CRC folding on the host
+// CRC helpers
 // ---------------------------------------------------------------------------
 namespace {
 
@@ -282,53 +283,23 @@ const uint32_t* pow2_table() {
   return t.data();
 }
 
-// Multiplication by x^(8n) mod P as four byte tables (a linear map).
-struct Shift {
-  uint32_t t[4][256];
-  explicit Shift(uint64_t n) {
-    const uint32_t c = crac::x8n(n, pow2_table());
-    for (int k = 0; k < 4; ++k)
-      for (uint32_t b = 0; b < 256; ++b) t[k][b] = crac::gf_mul(c, b << (8 * k));
+// fn(0..n-1) on up to 16 host threads (only worth it for big plans).
+template <typename Fn>
+void parallel_for(uint64_t n, Fn&& fn) {
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (n < 4096 || hw == 1) {
+    for (uint64_t i = 0; i < n; ++i) fn(i);
+    return;
   }
-  uint32_t operator()(uint32_t v) const {
-    return t[0][v & 0xFF] ^ t[1][(v >> 8) & 0xFF] ^ t[2][(v >> 16) & 0xFF] ^ t[3][v >> 24];
-  }
-};
-
-const Shift& shift_for(uint64_t n) {
-  static const Shift s16(16), s4k(4096), s64k(65536);
-  return n == 16 ? s16 : n == 4096 ? s4k : s64k;
+  std::atomic<uint64_t> next{0};
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < hw; ++t)
+    pool.emplace_back([&] {
+      for (uint64_t b; (b = next.fetch_add(1024)) < n;)
+        for (uint64_t i = b; i < std::min(n, b + 1024); ++i) fn(i);
+    });
+  for (auto& th : pool) th.join();
 }
-
-// Shift by any length < 2^17 as a product of power-of-two shifts, four table
-// lookups per set bit (chunk tails and odd record lengths); longer lengths
-// fall back to bit-serial multiplication.
-const Shift* pow2_shifts() {
-  static const std::vector<Shift>* t = [] {
-    auto* v = new std::vector<Shift>();
-    for (int k = 0; k < 17; ++k) v->emplace_back(uint64_t(1) << k);
-    return v;
-  }();
-  return t->data();
-}
-
-uint32_t advance_any(uint32_t v, uint64_t len) {
-  if (len >> 17) return crac::advance(v, len, pow2_table());
-  const Shift* p = pow2_shifts();
-  for (int k = 0; len; ++k, len >>= 1)
-    if (len & 1) v = p[k](v);
-  return v;
-}
-
-struct Fold {
-  uint32_t acc = 0;
-  void add(uint32_t crc, uint64_t len) {
-    if (len == 16 || len == 4096 || len == 65536)
-      acc = shift_for(len)(acc) ^ crc;
-    else
-      acc = advance_any(acc, len) ^ crc;
-  }
-};
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
   float v = 0;
@@ -400,45 +371,61 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
     P.recs.push_back(g);
     pos += 20;
   }
+  // managed allocations: lay out offsets first, then fill the page records of
+  // every allocation in parallel (C3 has millions of pages)
+  struct Slot {
+    const BulkItem* it;
+    size_t rec0;
+    uint64_t pos0, page0;
+  };
+  std::vector<Slot> slots;
   for (const BulkItem& it : items) {
     if (it.kind != AllocationKind::Managed) continue;
     const uint64_t pages = page_count_for(it.size);
-    crac_record_t h{};
-    h.out_off = pos;
+    slots.push_back(Slot{&it, P.recs.size() + 0, pos, P.page_first.back()});
+    P.recs.resize(P.recs.size() + 1 + pages);
+    pos += 16 + 16 * pages + it.size;
+    P.page_spans.push_back(crac_span_t{it.ptr, it.size});
+    P.page_first.push_back(P.page_first.back() + pages);
+  }
+  parallel_for(slots.size(), [&](uint64_t k) {
+    const Slot& sl = slots[k];
+    const BulkItem& it = *sl.it;
+    const uint64_t pages = page_count_for(it.size), padded = round_up_align(it.size);
+    crac_record_t& h = P.recs[sl.rec0];
+    h = crac_record_t{};
+    h.out_off = sl.pos0;
     h.frame_len = 16;
     std::memcpy(h.frame, &it.id, 8);
     std::memcpy(h.frame + 8, &pages, 8);
-    P.recs.push_back(h);
-    pos += 16;
-    P.page_spans.push_back(crac_span_t{it.ptr, it.size});
-    P.page_first.push_back(P.page_first.back() + pages);
-    const uint64_t padded = round_up_align(it.size);
+    uint64_t at = sl.pos0 + 16;
     for (uint64_t p = 0; p < pages; ++p) {
       const uint64_t off = p * kPageSize;
       const uint32_t len = uint32_t(std::min<uint64_t>(kPageSize, it.size - off));
       const uint32_t fl = it.flags ? (*it.flags)[p] : 0;
-      crac_record_t r{};
-      r.out_off = pos;
+      crac_record_t& r = P.recs[sl.rec0 + 1 + p];
+      r = crac_record_t{};
+      r.out_off = at;
       r.ptr = it.ptr + off;
       r.len = len;
       r.ext = p + 1 == pages ? padded - off : len;
       r.frame_len = 16;
+      r.reserved = uint32_t(sl.page0 + p);  // its page-CRC index
       std::memcpy(r.frame, &p, 8);
       std::memcpy(r.frame + 8, &fl, 4);
       std::memcpy(r.frame + 12, &len, 4);
-      P.recs.push_back(r);
-      pos += 16 + len;
+      at += 16 + len;
     }
-  }
+  });
   P.stream_len = pos;
   const uint64_t tiles = (pos + CRAC_TILE_BYTES - 1) / CRAC_TILE_BYTES;
   P.tile_rec.resize(tiles);
-  uint32_t r = 0;
-  for (uint64_t t = 0; t < tiles; ++t) {
+  parallel_for(tiles, [&](uint64_t t) {  // last record starting at or before the tile
     const uint64_t start = t * CRAC_TILE_BYTES;
-    while (r + 1 < P.recs.size() && P.recs[r + 1].out_off <= start) ++r;
-    P.tile_rec[t] = r;
-  }
+    const auto it = std::upper_bound(P.recs.begin(), P.recs.end(), start,
+                                     [](uint64_t v, const crac_record_t& r) { return v < r.out_off; });
+    P.tile_rec[t] = uint32_t((it - P.recs.begin()) - 1);
+  });
 }
 
 template <typename D, typename H>
@@ -460,8 +447,6 @@ void upload_plan(DrainEngine& E, const ImagePlan& P, cudaStream_t st) {
   const uint64_t n_pay = P.pay_first.back(), n_page = P.page_first.back();
   E.d_pay_crc.ensure(std::max<uint64_t>(n_pay, 1));
   E.d_page_crc.ensure(std::max<uint64_t>(n_page, 1));
-  E.h_pay_crc.ensure(std::max<uint64_t>(n_pay, 1));
-  E.h_page_crc.ensure(std::max<uint64_t>(n_page, 1));
 }
 
 void hash_payloads(DrainEngine& E, const ImagePlan& P, uint64_t c_lo, uint64_t c_hi,
@@ -480,17 +465,6 @@ void hash_pages(DrainEngine& E, const ImagePlan& P, uint32_t max_ctas, cudaStrea
              "K1 pages");
 }
 
-void download_crcs(DrainEngine& E, const ImagePlan& P, cudaStream_t st) {
-  const uint64_t n_pay = P.pay_first.back(), n_page = P.page_first.back();
-  if (n_pay)
-    check_cuda(cudaMemcpyAsync(E.h_pay_crc.ptr, E.d_pay_crc.ptr, n_pay * 4, cudaMemcpyDeviceToHost, st),
-               "crc download");
-  if (n_page)
-    check_cuda(cudaMemcpyAsync(E.h_page_crc.ptr, E.d_page_crc.ptr, n_page * 4,
-                               cudaMemcpyDeviceToHost, st),
-               "crc download");
-}
-
 uint64_t hashed_bytes(const ImagePlan& P) {
   uint64_t b = 0;
   for (const auto& s : P.pay_spans) b += s.len;
@@ -498,36 +472,22 @@ uint64_t hashed_bytes(const ImagePlan& P) {
   return b;
 }
 
-// Bytes of payload chunk c (all 64 KiB except a region's tail chunk).
-uint64_t chunk_len(const ImagePlan& P, uint64_t c) {
-  const size_t s = size_t(std::upper_bound(P.pay_first.begin(), P.pay_first.end(), c) -
-                          P.pay_first.begin() - 1);
-  const uint64_t off = (c - P.pay_first[s]) * DrainEngine::kChunk;
-  return std::min<uint64_t>(DrainEngine::kChunk, P.pay_spans[s].len - off);
+// Section CRCs on the device (K4): enqueues the fold and the 8-byte readback
+// on `st`; finish_fold() applies K(section length) once `st` has completed.
+void enqueue_fold(DrainEngine& E, const ImagePlan& P, cudaStream_t st) {
+  E.d_fold.ensure(2);
+  E.h_fold.ensure(2);
+  check_cuda(cudaError_t(crac_fold_sections(E.d_recs.ptr, uint32_t(P.recs.size()), E.d_pay_first.ptr,
+                                            E.d_pay_crc.ptr, uint32_t(P.pay_spans.size()),
+                                            E.d_page_crc.ptr, P.len3, P.pay_first.back(),
+                                            E.d_fold.ptr, st)),
+             "fold");
+  check_cuda(cudaMemcpyAsync(E.h_fold.ptr, E.d_fold.ptr, 8, cudaMemcpyDeviceToHost, st), "fold out");
 }
 
-// Section CRCs from chunk CRCs and the frame bytes of every record.
-void fold_sections(const DrainEngine& E, const ImagePlan& P, uint32_t& crc3, uint32_t& crc4) {
-  Fold f3;
-  size_t span = 0;
-  for (const crac_record_t& r : P.recs) {
-    if (r.out_off >= P.len3) break;
-    f3.add(crc32_host(r.frame, 16), 16);
-    const uint64_t c0 = P.pay_first[span], c1 = P.pay_first[span + 1];
-    for (uint64_t c = c0; c < c1; ++c)
-      f3.add(E.h_pay_crc.ptr[c],
-             std::min<uint64_t>(DrainEngine::kChunk, r.len - (c - c0) * DrainEngine::kChunk));
-    ++span;
-  }
-  crc3 = f3.acc;
-  Fold f4;
-  uint64_t page = 0;
-  for (const crac_record_t& r : P.recs) {
-    if (r.out_off < P.len3 + 20) continue;
-    f4.add(crc32_host(r.frame, 16), 16);
-    if (r.len) f4.add(E.h_page_crc.ptr[page++], r.len);
-  }
-  crc4 = f4.acc;
+void finish_fold(const DrainEngine& E, const ImagePlan& P, uint32_t& crc3, uint32_t& crc4) {
+  crc3 = E.h_fold.ptr[0] ^ crac::crc_affine(P.len3, pow2_table());
+  crc4 = E.h_fold.ptr[1] ^ crac::crc_affine(P.len4, pow2_table());
 }
 
 template <typename T>
@@ -628,6 +588,10 @@ void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
   const bool bulk = P.len3 + P.len4 > 0;
   uint32_t crc3 = 0, crc4 = 0;
   uint64_t windows = 0;
+  std::vector<uint64_t> managed_ids;
+  for (const AllocationRecord& rec : active)
+    if (rec.kind == AllocationKind::Managed) managed_ids.push_back(rec.id);
+  for (uint64_t id : managed_ids) ctx.managed_remote_access(id, true);
   if (bulk) {
     upload_plan(E, P, E.s_pack);
     check_cuda(cudaEventRecord(E.ev_ready[0], E.s_pack), "event");
@@ -638,7 +602,7 @@ void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
     if (P.pay_first.back()) hash_payloads(E, P, 0, P.pay_first.back(), k1_ctas, E.s_hash);
     if (P.page_first.back()) hash_pages(E, P, k1_ctas, E.s_hash);
     check_cuda(cudaEventRecord(E.ev_h1, E.s_hash), "event");
-    download_crcs(E, P, E.s_hash);
+    enqueue_fold(E, P, E.s_hash);
 
     windows = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
     if (stats) E.ensure_window_events(windows);
@@ -663,11 +627,10 @@ void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
     }
     check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
     tr.mark("enqueue");
-    // fold while the D2H is still draining
+    // the section CRCs are ready long before the D2H finishes
     check_cuda(cudaStreamSynchronize(E.s_hash), "hash sync");
-    tr.mark("hash-wait");
-    fold_sections(E, P, crc3, crc4);
-    tr.mark("fold");
+    tr.mark("hash+fold");
+    finish_fold(E, P, crc3, crc4);
     // seed the incremental table with this image's payload chunk CRCs
     const uint64_t n_pay = P.pay_first.back();
     if (n_pay) {
@@ -680,6 +643,7 @@ void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
     check_cuda(cudaStreamSynchronize(E.s_pack), "pack sync");
     check_cuda(cudaStreamSynchronize(E.s_hash), "hash sync");
     tr.mark("d2h-wait");
+    for (uint64_t id : managed_ids) ctx.managed_remote_access(id, false);
   } else {
     // no bulk bytes: the stream is just crc3 (0) and the UVM_PAGES header
     put_at<uint32_t>(img + s3, 0);
@@ -832,6 +796,16 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     raise(Errc::ImageCorrupt, "bulk sections do not match the log's active set");
   tr.mark("plan");
 
+  // managed pages: populate each run where the image says it lives, and let
+  // the scatter write host-resident pages over the link without migrating
+  mi = 0;
+  for (const AllocationRecord& rec : p.facts.active)
+    if (rec.kind == AllocationKind::Managed) {
+      ctx.place_managed(rec.id, p.managed[mi++].flags, E.s_pack);
+      ctx.managed_remote_access(rec.id, true);
+    }
+  tr.mark("place");
+
   uint64_t windows = 0;
   if (P.stream_len > 20) {
     upload_plan(E, P, E.s_pack);
@@ -877,23 +851,19 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       hash_pages(E, P, 0, E.s_pack);
       if (stats) ++stats->hash_launches;
     }
-    download_crcs(E, P, E.s_pack);
+    enqueue_fold(E, P, E.s_pack);
     tr.mark("enqueue");
     check_cuda(cudaStreamSynchronize(E.s_pack), "refill sync");
     tr.mark("h2d+verify");
     uint32_t crc3 = 0, crc4 = 0;
-    fold_sections(E, P, crc3, crc4);
-    tr.mark("fold");
+    finish_fold(E, P, crc3, crc4);
     if (crc3 != p.sec[2].crc) raise(Errc::ImageCorrupt, "crc mismatch in ALLOC_PAYLOADS");
     if (crc4 != p.sec[3].crc) raise(Errc::ImageCorrupt, "crc mismatch in UVM_PAGES");
   } else if (p.sec[2].crc != 0 || p.sec[3].crc != 0) {
     raise(Errc::ImageCorrupt, "crc mismatch in empty bulk section");
   }
-  // managed residence and flags
-  mi = 0;
   for (const AllocationRecord& rec : p.facts.active)
-    if (rec.kind == AllocationKind::Managed)
-      ctx.restore_managed(rec.id, p.managed[mi++].flags, E.s_pack);
+    if (rec.kind == AllocationKind::Managed) ctx.managed_remote_access(rec.id, false);
   check_cuda(cudaEventRecord(E.ev_t1, E.s_pack), "event");
   check_cuda(cudaEventSynchronize(E.ev_t1), "event sync");
   E.prev_valid = false;  // no pinned image of this session exists yet
@@ -958,13 +928,12 @@ void incremental_locked(Session& session, PinnedImage& image, DrainStats* stats)
   check_cuda(cudaEventRecord(E.ev_h1, E.s_pack), "event");
   check_cuda(cudaMemcpyAsync(E.h_count.ptr, E.d_counters.ptr, 16, cudaMemcpyDeviceToHost, E.s_pack),
              "counters");
-  download_crcs(E, P, E.s_pack);
+  enqueue_fold(E, P, E.s_pack);
   check_cuda(cudaStreamSynchronize(E.s_pack), "hash sync");
-  tr.mark("hash+drain");
+  tr.mark("hash+drain+fold");
   const uint64_t dirty = E.h_count.ptr[0], dirty_bytes = E.h_count.ptr[1];
   uint32_t crc3 = 0, crc4 = 0;
-  fold_sections(E, P, crc3, crc4);
-  tr.mark("fold");
+  finish_fold(E, P, crc3, crc4);
   put_at<uint32_t>(img + s3 + P.len3, crc3);
   put_at<uint32_t>(img + s3 + P.stream_len, crc4);
 

@@ -89,7 +89,8 @@ struct DrainEngine {
   DevArray<uint32_t> d_pay_crc, d_page_crc, d_prev_crc, d_block_counts;
   DevArray<uint64_t> d_dirty_idx, d_dirty_count;
   DevArray<unsigned long long> d_counters;
-  HostArray<uint32_t> h_pay_crc, h_page_crc;
+  DevArray<uint32_t> d_fold;   // linear parts of crc3 / crc4 (K4)
+  HostArray<uint32_t> h_fold;
   HostArray<uint64_t> h_count, h_dirty_idx;
 
   ImagePlan plan;

@@ -545,6 +545,65 @@ __global__ void __launch_bounds__(kPackThreads)
 }
 
 // ---------------------------------------------------------------------------
+// K4: section CRCs on the device
+// ---------------------------------------------------------------------------
+// crc(S) = L(S) ^ K(|S|) and L(S) = XOR over pieces p of A^(bytes after p)(L(p)),
+// L(p) = crc(p) ^ K(|p|).  One thread per piece (a payload chunk, a page, or a
+// 16-byte frame) computes its shifted linear term; the XOR is reduced per
+// warp and folded into out[section] with one atomic.  The host applies the
+// final K(|S|).  Record `reserved` carries the index of the record's first
+// CRC (payload span index for ALLOC_PAYLOADS records, page index for pages).
+constexpr int kFoldThreads = 256;
+
+__device__ __forceinline__ uint32_t frame_linear(const uint8_t* f, uint32_t n) {
+  uint32_t s = 0;
+  for (uint32_t i = 0; i < n; ++i) s = (s >> 8) ^ g_t0[(s ^ f[i]) & 0xFFu];
+  return s;
+}
+
+__global__ void __launch_bounds__(kFoldThreads)
+    k_fold_sections(const crac_record_t* __restrict__ recs, uint32_t n_recs,
+                    const uint64_t* __restrict__ pay_first, const uint32_t* __restrict__ pay_crc,
+                    uint32_t n_pay, const uint32_t* __restrict__ page_crc, uint64_t len3,
+                    uint64_t total_chunks, uint32_t* __restrict__ out) {
+  const uint64_t t = blockIdx.x * uint64_t(kFoldThreads) + threadIdx.x;
+  uint32_t term = 0;
+  int sec = -1;
+  if (t < total_chunks) {
+    // an ALLOC_PAYLOADS chunk
+    const uint32_t s = find_span(pay_first, n_pay, t);
+    const crac_record_t& R = recs[s];
+    const uint64_t off = (t - pay_first[s]) * 65536ull;
+    const uint64_t len = min(uint64_t(65536), R.len - off);
+    const uint64_t end = R.out_off + R.frame_len + off + len;
+    term = crac::advance(pay_crc[t] ^ crac::crc_affine(len, g_pow2), len3 - end, g_pow2);
+    sec = 0;
+  } else if (t - total_chunks < n_recs) {
+    const crac_record_t& R = recs[t - total_chunks];
+    if (R.out_off < len3) {  // an ALLOC_PAYLOADS frame
+      term = crac::advance(frame_linear(R.frame, 16), len3 - (R.out_off + 16), g_pow2);
+      sec = 0;
+    } else if (R.out_off >= len3 + 20) {  // a UVM_PAGES header or page
+      // sec4 offsets are relative to the first byte after the 20-byte gap;
+      // the section end is the end of the stream (the last record's end)
+      const crac_record_t& last = recs[n_recs - 1];
+      const uint64_t sec_end = last.out_off + last.frame_len + last.len;
+      uint32_t l = crac::advance(frame_linear(R.frame, 16), R.len, g_pow2);
+      if (R.len) l ^= page_crc[R.reserved] ^ crac::crc_affine(R.len, g_pow2);
+      term = crac::advance(l, sec_end - (R.out_off + 16 + R.len), g_pow2);
+      sec = 1;
+    }
+  }
+  // reduce per warp and section
+  const uint32_t lane = threadIdx.x & 31;
+  for (int which = 0; which < 2; ++which) {
+    uint32_t v = sec == which ? term : 0u;
+    for (int o = 16; o; o >>= 1) v ^= __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if (lane == 0 && v) atomicXor(out + which, v);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K2b: dirty detection + compaction + gather
 // ---------------------------------------------------------------------------
 constexpr int kDiffThreads = 256;
@@ -809,6 +868,19 @@ int crac_hash_drain_range(const crac_span_t* d_spans, const uint64_t* d_chunk_fi
   k1_chunk_crc<16, true><<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
       d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, k_full_for(chunk_bytes),
       HashDrain{d_crc_prev, d_dst_off, host_image, d_counters});
+  return int(cudaGetLastError());
+}
+
+int crac_fold_sections(const crac_record_t* d_recs, uint32_t n_recs, const uint64_t* d_pay_first,
+                       const uint32_t* d_pay_crc, uint32_t n_pay, const uint32_t* d_page_crc,
+                       uint64_t len3, uint64_t total_pay_chunks, uint32_t* d_out, void* stream) {
+  cudaStream_t st = cudaStream_t(stream);
+  if (cudaError_t e = cudaMemsetAsync(d_out, 0, 8, st)) return int(e);
+  if (int rc = crac_gpu_init()) return rc;
+  const uint64_t threads = total_pay_chunks + n_recs;
+  if (threads == 0) return 0;
+  k_fold_sections<<<unsigned((threads + kFoldThreads - 1) / kFoldThreads), kFoldThreads, 0, st>>>(
+      d_recs, n_recs, d_pay_first, d_pay_crc, n_pay, d_page_crc, len3, total_pay_chunks, d_out);
   return int(cudaGetLastError());
 }
 

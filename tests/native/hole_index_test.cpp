@@ -48,22 +48,26 @@ struct IdxAlloc {  // DeviceContext's logic over HoleIndex
   bool alloc(uint64_t need, uint64_t& addr) {
     uint64_t len = 0;
     if (!holes.first_fit(need, addr, len)) return false;
-    holes.erase(addr);
-    if (len > need) holes.insert(addr + need, len - need);
+    if (len > need)
+      holes.update(addr, addr + need, len - need);
+    else
+      holes.erase(addr);
     return true;
   }
   void free(uint64_t addr, uint64_t len) {
     uint64_t next_len = 0, ps = 0, pl = 0;
-    if (holes.at(addr + len, next_len)) {
+    const bool next = holes.at(addr + len, next_len);
+    const bool prev = holes.before(addr, ps, pl) && ps + pl == addr;
+    if (prev && next) {
       holes.erase(addr + len);
-      len += next_len;
+      holes.update(ps, ps, pl + len + next_len);
+    } else if (prev) {
+      holes.update(ps, ps, pl + len);
+    } else if (next) {
+      holes.update(addr + len, addr, len + next_len);
+    } else {
+      holes.insert(addr, len);
     }
-    if (holes.before(addr, ps, pl) && ps + pl == addr) {
-      holes.erase(ps);
-      addr = ps;
-      len += pl;
-    }
-    holes.insert(addr, len);
   }
 };
 
