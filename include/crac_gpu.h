@@ -39,7 +39,9 @@ typedef struct crac_span {
  * `frame_len` literal bytes at stream offset `out_off`, followed by `len`
  * payload bytes that live at device-visible address `ptr`.
  * Refill writes `ext` >= len bytes at `ptr`; bytes past `len` are zeroed
- * (the allocator's 256-byte padding, ref: device_core.cpp:48,65). */
+ * (the allocator's 256-byte padding, ref: device_core.cpp:48,65).
+ * ptr == 0 with len > 0 marks host-filled content: pack emits zeros for it
+ * and scatter skips it (host-resident managed pages are copied by the host). */
 typedef struct crac_record {
   uint64_t out_off;
   uint64_t ptr;

@@ -189,7 +189,8 @@ void release_engine(std::unique_ptr<DrainEngine> e) {
       cudaStreamSynchronize(e->s_copy) != cudaSuccess ||
       cudaStreamSynchronize(e->s_hash) != cudaSuccess)
     return;  // a broken engine is dropped (and leaked), never pooled
-  e->plan = ImagePlan{};
+  e->plan.valid = false;  // keep the vectors' capacity for the next session
+  e->plan.image_ptr = 0;
   e->prev_valid = false;
   e->dst_for_image = 0;
   std::lock_guard lk(g_pool_mu);
@@ -328,6 +329,7 @@ struct BulkItem {
 };
 
 void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
+  PhaseTrace tr("  plan");
   P.recs.clear();
   P.pay_spans.clear();
   P.page_spans.clear();
@@ -335,6 +337,12 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
   P.page_first.assign(1, 0);
   P.pay_rec_off.clear();
   P.log_sizes.clear();
+  {  // one allocation for the whole record table
+    uint64_t n = 1;
+    for (const BulkItem& it : items)
+      n += it.kind == AllocationKind::Managed ? 1 + page_count_for(it.size) : 1;
+    P.recs.reserve(n);
+  }
   uint64_t pos = 0, len4 = 0;
   for (const BulkItem& it : items) {
     P.log_sizes.push_back(it.id);
@@ -371,6 +379,7 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
     P.recs.push_back(g);
     pos += 20;
   }
+  tr.mark("payloads");
   // managed allocations: lay out offsets first, then fill the page records of
   // every allocation in parallel (C3 has millions of pages)
   struct Slot {
@@ -388,6 +397,18 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
     P.page_spans.push_back(crac_span_t{it.ptr, it.size});
     P.page_first.push_back(P.page_first.back() + pages);
   }
+  // host-resident pages (flag bit0 clear) are moved by host threads, not by
+  // the SMs: pack emits zeros for them, scatter skips them
+  std::vector<uint64_t> host_first(slots.size() + 1, 0);
+  for (size_t k = 0; k < slots.size(); ++k) {
+    const BulkItem& it = *slots[k].it;
+    uint64_t h = 0;
+    if (it.flags)
+      for (uint8_t f : *it.flags) h += (f & 1) ? 0 : 1;
+    host_first[k + 1] = host_first[k] + h;
+  }
+  tr.mark("layout");
+  P.host_pages.assign(host_first.back(), HostPage{});
   parallel_for(slots.size(), [&](uint64_t k) {
     const Slot& sl = slots[k];
     const BulkItem& it = *sl.it;
@@ -399,6 +420,7 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
     std::memcpy(h.frame, &it.id, 8);
     std::memcpy(h.frame + 8, &pages, 8);
     uint64_t at = sl.pos0 + 16;
+    uint64_t hp = host_first[k];
     for (uint64_t p = 0; p < pages; ++p) {
       const uint64_t off = p * kPageSize;
       const uint32_t len = uint32_t(std::min<uint64_t>(kPageSize, it.size - off));
@@ -414,9 +436,14 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
       std::memcpy(r.frame, &p, 8);
       std::memcpy(r.frame + 8, &fl, 4);
       std::memcpy(r.frame + 12, &len, 4);
+      if (it.flags && !((*it.flags)[p] & 1)) {
+        P.host_pages[hp++] = HostPage{at + 16, r.ptr, len, uint32_t(r.ext)};
+        r.ptr = 0;
+      }
       at += 16 + len;
     }
   });
+  tr.mark("pages");
   P.stream_len = pos;
   const uint64_t tiles = (pos + CRAC_TILE_BYTES - 1) / CRAC_TILE_BYTES;
   P.tile_rec.resize(tiles);
@@ -600,7 +627,9 @@ void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
     const uint32_t k1_ctas = uint32_t(std::max(1, E.sm_count - DrainEngine::kPackSMs));
     check_cuda(cudaEventRecord(E.ev_h0, E.s_hash), "event");
     if (P.pay_first.back()) hash_payloads(E, P, 0, P.pay_first.back(), k1_ctas, E.s_hash);
-    if (P.page_first.back()) hash_pages(E, P, k1_ctas, E.s_hash);
+    // pages: host-resident ones are read over the link, so a modest grid
+    // saturates it and leaves the rest of the SMs to the pack
+    if (P.page_first.back()) hash_pages(E, P, std::min<uint32_t>(k1_ctas, 48), E.s_hash);
     check_cuda(cudaEventRecord(E.ev_h1, E.s_hash), "event");
     enqueue_fold(E, P, E.s_hash);
 
@@ -643,6 +672,13 @@ void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
     check_cuda(cudaStreamSynchronize(E.s_pack), "pack sync");
     check_cuda(cudaStreamSynchronize(E.s_hash), "hash sync");
     tr.mark("d2h-wait");
+    // host-resident pages: managed memory -> image by host threads (the
+    // windows carried zeros there; every D2H has landed)
+    parallel_for(P.host_pages.size(), [&](uint64_t i) {
+      const HostPage& h = P.host_pages[i];
+      std::memcpy(img + s3 + h.stream_off, reinterpret_cast<const void*>(h.ptr), h.len);
+    });
+    tr.mark("host-pages");
     for (uint64_t id : managed_ids) ctx.managed_remote_access(id, false);
   } else {
     // no bulk bytes: the stream is just crc3 (0) and the UVM_PAGES header
@@ -787,6 +823,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     if (rec.kind == AllocationKind::Managed) it.flags = &p.managed[mi++].flags;
     items.push_back(it);
   }
+  tr.mark("items");
   ImagePlan& P = E.plan;
   build_plan(items, P);
   P.log_len = p.log.size();
@@ -798,12 +835,29 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
 
   // managed pages: populate each run where the image says it lives, and let
   // the scatter write host-resident pages over the link without migrating
+  // managed pages land where they were: device-resident ones are first
+  // touched by the scatter kernel, host-resident ones by the host threads
+  // below, so no prefetch (or migration) is needed to restore residence
   mi = 0;
   for (const AllocationRecord& rec : p.facts.active)
     if (rec.kind == AllocationKind::Managed) {
-      ctx.place_managed(rec.id, p.managed[mi++].flags, E.s_pack);
-      ctx.managed_remote_access(rec.id, true);
+      ctx.set_managed_flags(rec.id, p.managed[mi++].flags);
+      ctx.managed_remote_access(rec.id, true);  // K1 verify reads host pages in place
     }
+  std::thread host_fill([&] {
+    parallel_for(P.host_pages.size(), [&](uint64_t i) {
+      const HostPage& h = P.host_pages[i];
+      uint8_t* dst = reinterpret_cast<uint8_t*>(h.ptr);
+      std::memcpy(dst, raw.data() + s3 + h.stream_off, h.len);
+      if (h.ext > h.len) std::memset(dst + h.len, 0, h.ext - h.len);
+    });
+  });
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } joiner{host_fill};
   tr.mark("place");
 
   uint64_t windows = 0;
@@ -847,6 +901,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       }
     }
     check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
+    host_fill.join();  // host-resident pages must be in place before their K1
     if (P.page_first.back()) {
       hash_pages(E, P, 0, E.s_pack);
       if (stats) ++stats->hash_launches;

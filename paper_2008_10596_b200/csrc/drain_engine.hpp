@@ -49,6 +49,14 @@ struct HostArray {  // pinned
 };
 
 // Layout of the last image this session drained (enables incremental drains).
+// A host-resident managed page: its content is copied by host threads
+// between the managed allocation and the image (never crosses PCIe).
+struct HostPage {
+  uint64_t stream_off;  // content offset in the bulk stream
+  uint64_t ptr;         // managed address of the page
+  uint32_t len, ext;    // content bytes; bytes to write on refill (zero tail)
+};
+
 struct ImagePlan {
   uint64_t image_bytes = 0;
   uint64_t image_ptr = 0;   // where that image lives (host)
@@ -61,6 +69,7 @@ struct ImagePlan {
   std::vector<uint64_t> pay_first, page_first;
   std::vector<uint64_t> pay_rec_off;  // stream offset of each payload's first byte
   std::vector<uint64_t> log_sizes;    // signature: (id, size) of every bulk record
+  std::vector<HostPage> host_pages;   // host-resident managed pages
   uint64_t log_len = 0;
   uint64_t tail_bytes = 0;  // STREAMS + APPSTATE + KERNEL_REGISTRY, framed
   bool valid = false;

@@ -416,8 +416,8 @@ __device__ __forceinline__ uint32_t stream_byte(const crac_record_t* recs, uint3
   const uint64_t rel = x - R.out_off;
   if (rel < R.frame_len) return R.frame[rel];
   const uint64_t pl = rel - R.frame_len;
-  if (pl < R.len) return reinterpret_cast<const uint8_t*>(R.ptr)[pl];
-  return 0;
+  if (pl < R.len && R.ptr) return reinterpret_cast<const uint8_t*>(R.ptr)[pl];
+  return 0;  // outside any record, or host-filled content (ptr == 0)
 }
 
 // ---------------------------------------------------------------------------
@@ -438,6 +438,12 @@ __global__ void __launch_bounds__(kPackThreads)
     const crac_record_t& R = recs[rec];
     const uint64_t P = R.out_off + R.frame_len;
     if (P <= tile0 && tile1 <= P + R.len) {
+      if (!R.ptr) {  // host-filled content: the host writes it after the D2H
+        uint4* o = reinterpret_cast<uint4*>(dst + (tile0 - win_off));
+        for (uint32_t w = threadIdx.x; w < ((tile1 - tile0 + 15) >> 4); w += kPackThreads)
+          o[w] = make_uint4(0, 0, 0, 0);
+        return;
+      }
       const uint64_t rel = tile0 - P;
       tile_copy(reinterpret_cast<uint4*>(dst + (tile0 - win_off)),
                 reinterpret_cast<const uint4*>(R.ptr) + (rel >> 4),
@@ -455,7 +461,9 @@ __global__ void __launch_bounds__(kPackThreads)
     const uint64_t P = R.out_off + R.frame_len;
     if (o >= P && o + kSubTile <= P + R.len) {
       // whole sub-tile inside one payload: aligned stores, shifted loads
-      if (x < win_end) *out = load_shifted(reinterpret_cast<const uint8_t*>(R.ptr) + (x - P));
+      if (x < win_end)
+        *out = R.ptr ? load_shifted(reinterpret_cast<const uint8_t*>(R.ptr) + (x - P))
+                     : make_uint4(0, 0, 0, 0);
     } else if (x < win_end) {
       uint32_t r = rec;
       uint4 v = make_uint4(0, 0, 0, 0);
@@ -496,6 +504,7 @@ __global__ void __launch_bounds__(kPackThreads)
     const crac_record_t& R = recs[rec];
     const uint64_t P = R.out_off + R.frame_len;
     if (P <= tile0 && tile1 + 16 <= P + R.len) {
+      if (!R.ptr) return;  // host-filled content
       const uint64_t d0 = (tile0 - P + 15) >> 4;                 // first dest word
       const uint64_t d1 = (tile1 - P + 15) >> 4;                 // one past the last
       const uint64_t f0 = P + 16 * d0 - win_off;                 // its window offset
@@ -514,6 +523,7 @@ __global__ void __launch_bounds__(kPackThreads)
     const uint64_t P = R.out_off + R.frame_len;
     if (o >= P && o + kSubTile + 16 <= P + R.len) {
       // fast path: every lane owns one full data word of R
+      if (!R.ptr) continue;
       const uint64_t d = (x - P + 15) >> 4;
       const uint64_t f = P + 16 * d;
       *reinterpret_cast<uint4*>(R.ptr + 16 * d) = load_shifted(win + (f - win_off));
@@ -530,6 +540,7 @@ __global__ void __launch_bounds__(kPackThreads)
     }
     if (d == ~0ull) continue;
     const crac_record_t& Q = recs[r];
+    if (!Q.ptr) continue;  // host-filled content
     const uint64_t Pq = Q.out_off + Q.frame_len;
     const uint64_t f = Pq + 16 * d;
     uint4 v = load_shifted(win + (f - win_off));
@@ -844,10 +855,14 @@ int crac_chunk_crc32_range(const crac_span_t* d_spans, const uint64_t* d_chunk_f
   uint64_t blocks = (warps_needed + kK1Warps - 1) / kK1Warps;
   const uint64_t cap = max_ctas ? std::min<uint64_t>(max_ctas, sm_count()) : sm_count();
   if (blocks > cap) blocks = cap;
-  static const int rows = [] {
+  // prefetch depth: 16 rows in flight for 64 KiB chunks; 8 for 4 KiB pages
+  // (one batch covers the page, so remote host-resident pages are read with
+  // every load in flight)
+  static const int forced = [] {
     const char* e = std::getenv("CRAC_K1_ROWS");
-    return e ? std::atoi(e) : 16;
+    return e ? std::atoi(e) : 0;
   }();
+  const int rows = forced ? forced : (chunk_bytes >= 32 * 512 ? 16 : chunk_bytes >= 8 * 512 ? 8 : 4);
   auto kern = rows == 4 ? k1_chunk_crc<4, false>
               : rows == 16 ? k1_chunk_crc<16, false> : k1_chunk_crc<8, false>;
   kern<<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
