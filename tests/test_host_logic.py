@@ -17,3 +17,35 @@ def test_hole_index_matches_reference_first_fit(tmp_path):
     out = subprocess.run([str(exe), "60"], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.strip() == "ok"
+
+
+def _build_dropin(tmp_path):
+    from paper_2008_10596_b200 import engine
+    if not engine.LIB_PATH.exists():
+        from paper_2008_10596_b200 import build
+        build.build()
+    exe = tmp_path / "dropin_test"
+    lib_dir = engine.LIB_PATH.parent
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", str(ROOT / "include"),
+                    "-I", "/usr/local/cuda/include",
+                    str(ROOT / "tests" / "native" / "dropin_test.cpp"), "-o", str(exe),
+                    "-L", str(lib_dir), "-lcrac_b200", f"-Wl,-rpath,{lib_dir}"],
+                   check=True)
+    return exe
+
+
+def test_reference_style_client_compiles_against_dropin_headers(tmp_path):
+    """A client written against the reference's C++ API (test_ckpt_engine.cpp
+    shapes) compiles and links unchanged against include/cracsim + the .so."""
+    assert _build_dropin(tmp_path).exists()
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_reference_style_client_runs_on_b200(tmp_path):
+    exe = _build_dropin(tmp_path)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.strip().endswith("ok")
