@@ -304,6 +304,41 @@ def pcie_peaks(torch) -> dict:
     return out
 
 
+def isolated_kernel_rates(torch, engine) -> dict:
+    """Pack / scatter kernels on one 64 MiB window each, back to back on one
+    stream (no copy engine, no other stream), for comparison with the in-situ
+    per-launch times of the timed region."""
+    import ctypes as C
+    import struct
+    L = engine.lib()
+    W, N = 64 * MIB, 8
+    src = torch.empty(W * (N + 1), dtype=torch.uint8, device="cuda")
+    out = torch.empty(W + 64, dtype=torch.uint8, device="cuda")
+    rec = struct.pack("<QQQQII", 0, src.data_ptr(), src.numel() - 16, src.numel(), 16, 0) + bytes(24)
+    d_rec = torch.frombuffer(bytearray(rec), dtype=torch.uint8).cuda()
+    d_tile = torch.zeros(src.numel() // 65536 + 1, dtype=torch.int32, device="cuda")
+    res = {}
+    for name, call in (("k_pack_records", L.crac_pack_records), ("k_scatter_records", L.crac_scatter_records)):
+        def run(w):
+            off = W * w
+            tile = C.c_void_p(d_tile.data_ptr() + 4 * (off // 65536))
+            if name == "k_pack_records":
+                return call(C.c_void_p(d_rec.data_ptr()), 1, tile, off, W, C.c_void_p(out.data_ptr()), None)
+            return call(C.c_void_p(d_rec.data_ptr()), 1, tile, C.c_void_p(out.data_ptr()), off, W, None)
+        run(0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for w in range(1, N + 1):
+            assert run(w) == 0
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / N
+        res[name] = {"avg_launch_ms": round(ms, 4), "GBps": round(2 * W / (ms * 1e-3) / 1e9, 1)}
+    del src, out
+    return res
+
+
 def build_workload(args, engine, rank: int, live_cap: int):
     """Creates the resident state of the chosen config; returns
     (session, live bytes, config dict)."""
@@ -418,6 +453,7 @@ def main() -> None:
     peaks = measured_peaks()
     peaks["pcie"] = pcie_peaks(torch)
     hbm = peaks["hbm_gbs"]
+    isolated = isolated_kernel_rates(torch, engine)
 
     t_setup = time.perf_counter()
     sess, live, cfg_extra = build_workload(args, engine, rank, min(host_cap, dev_cap))
@@ -533,7 +569,12 @@ def main() -> None:
                          "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
                          "traffic": None, "peak_source": peaks["source"],
                          "algorithmic_bytes_per_launch": int(dom_bytes),
-                         "avg_launch_ms": round(dom_ms, 4)},
+                         "avg_launch_ms": round(dom_ms, 4),
+                         "isolated": {k: {**v, "frac": round(v["GBps"] / hbm, 4)}
+                                      for k, v in isolated.items()},
+                         "note": "in-situ launch times (timed region, median window) include "
+                                 "queueing behind the copy engines; 'isolated' = the same kernel "
+                                 "back to back on one stream"},
             "pcie_roofline": {"d2h_GBps": round(d2h, 2), "h2d_GBps": round(h2d, 2),
                               "d2h_peak_GBps": pd, "h2d_peak_GBps": ph,
                               "peak_source": "measured in this run (16 MiB pinned copies)",

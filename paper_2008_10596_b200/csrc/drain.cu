@@ -7,7 +7,7 @@
 //   GPU   : s_hash  K1 over every payload (64 KiB chunks) and managed page,
 //                   on all but kPackSMs SMs so the pack never waits for it
 //           s_pack  pack kernel builds the exact stream bytes window by window
-//                   into an 8 x 16 MiB staging ring (about L2-sized)
+//                   into a 4 x 64 MiB staging ring, copied out in 16 MiB pieces
 //           s_copy  D2H of each window into the pinned image (4 KiB aligned)
 //   host  : folds chunk CRCs with the frame CRCs into the section CRCs while
 //           the D2H drains, then patches crc3/crc4.
@@ -651,7 +651,12 @@ void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
       if (stats) cudaEventRecord(E.ev_w1[w], E.s_pack);
       check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_pack), "event");
       check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_ready[slot], 0), "wait");
-      check_cuda(cudaMemcpyAsync(img + s3 + off, buf, len, cudaMemcpyDeviceToHost, E.s_copy), "D2H");
+      // the copy engine runs best on 16 MiB pieces; the pack on bigger windows
+      for (uint64_t c = 0; c < len; c += DrainEngine::kCopyChunk)
+        check_cuda(cudaMemcpyAsync(img + s3 + off + c, buf + c,
+                                   std::min(DrainEngine::kCopyChunk, len - c),
+                                   cudaMemcpyDeviceToHost, E.s_copy),
+                   "D2H");
       check_cuda(cudaEventRecord(E.ev_free[slot], E.s_copy), "event");
     }
     check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
@@ -877,9 +882,11 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       const uint64_t with_ahead = std::min(len + 16, P.stream_len - off);
       if (w >= uint64_t(DrainEngine::kSlots))
         check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_free[slot], 0), "wait");
-      check_cuda(cudaMemcpyAsync(buf, raw.data() + s3 + off, with_ahead, cudaMemcpyHostToDevice,
-                                 E.s_copy),
-                 "H2D");
+      for (uint64_t c = 0; c < with_ahead; c += DrainEngine::kCopyChunk)
+        check_cuda(cudaMemcpyAsync(buf + c, raw.data() + s3 + off + c,
+                                   std::min(DrainEngine::kCopyChunk, with_ahead - c),
+                                   cudaMemcpyHostToDevice, E.s_copy),
+                   "H2D");
       check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_copy), "event");
       check_cuda(cudaStreamWaitEvent(E.s_pack, E.ev_ready[slot], 0), "wait");
       if (stats) cudaEventRecord(E.ev_w0[w], E.s_pack);
