@@ -342,3 +342,86 @@ def test_c3_managed_mixed_residence_matches_reference(eng):
     rs, _ = eng.restart(img)
     assert _state(rs) == _state(s)
     assert rs.checkpoint()[0] == img
+
+
+# ---------------------------------------------------------------------------
+# edge shapes and error parity (test_device_core.cpp / test_shim.cpp cases)
+# ---------------------------------------------------------------------------
+def _shape_tiny(api):
+    for kind in (workloads.DEVICE, workloads.PINNED, workloads.MANAGED):
+        i, _ = api.alloc(kind, 1)
+        if kind == workloads.MANAGED:
+            api.page_write(i, 0, b"\x7f", workloads.HOST_SIDE)
+        else:
+            api.copy_h2d(i, 0, b"\x7f")
+
+
+def _shape_chunk_edges(api):
+    for k, size in enumerate([65535, 65536, 65537, 131073, 4096 * 3, 255, 257]):
+        i, _ = api.alloc(workloads.DEVICE, size)
+        api.fill_synthetic(i, 11 + k)
+    for size in (4096, 8192, 4097):
+        i, _ = api.alloc(workloads.MANAGED, size)
+        api.fill_synthetic(i, 5, workloads.DEVICE_SIDE)
+
+
+def _shape_streams_and_binaries(api):
+    ids = [api.stream_create() for _ in range(128)]
+    for s in ids[::3]:
+        api.stream_destroy(s)
+    hs = [api.register_fat_binary([(f"k{b}_{j}", 1 + j, j) for j in range(3)]) for b in range(40)]
+    for h in hs[::3]:
+        api.unregister_fat_binary(h)
+    api.set_app_state(bytes(range(256)) * 4096)  # 1 MiB of app state
+
+
+@pytest.mark.parametrize("shape", [_shape_tiny, _shape_chunk_edges, _shape_streams_and_binaries])
+def test_edge_shapes_match_reference(eng, shape):
+    s = eng.Session(seed=8, arena_bytes=4 << 20)
+    r = ref.RefSession(seed=8, arena_bytes=4 << 20)
+    shape(s)
+    shape(r)
+    img = s.checkpoint()[0]
+    assert img == r.checkpoint()[0]
+    if shape is not _shape_streams_and_binaries:  # generated kernels have no bodies
+        rs, _ = eng.restart(img)
+        assert rs.checkpoint()[0] == img
+
+
+def _errc(fn):
+    try:
+        fn()
+    except (ref.RefError, Exception) as e:  # noqa: B014
+        return getattr(e, "errc", type(e).__name__)
+    return None
+
+
+def test_error_codes_match_reference(eng):
+    cases = []
+    for api in (eng.Session(seed=1, arena_bytes=1 << 20), ref.RefSession(seed=1, arena_bytes=1 << 20)):
+        a, _ = api.alloc(workloads.DEVICE, 1024)
+        m, _ = api.alloc(workloads.MANAGED, 8192)
+        api.register_fat_binary(workloads.STD_KERNELS)
+        st = api.stream_create()
+        api.free(a)
+        out = [
+            _errc(lambda: api.free(a)),                                   # DoubleFree
+            _errc(lambda: api.free(999)),                                 # UnknownId
+            _errc(lambda: api.alloc(workloads.DEVICE, 0)),                # InvalidArgument
+            _errc(lambda: api.alloc(workloads.DEVICE, 2 << 20)),          # OutOfArena
+            _errc(lambda: api.launch(st, "nope", [(m, 0)], [1, 2])),      # UnregisteredKernel
+            _errc(lambda: api.launch(st, "fill8", [(m, 0)], [1])),        # arity: InvalidArgument
+            _errc(lambda: api.launch(st, "fill8", [(m, 9000)], [1, 1])),  # OutOfRange
+            _errc(lambda: api.copy_h2d(m, 8190, b"1234")),                # OutOfRange
+            _errc(lambda: api.stream_destroy(77)),                        # UnknownId
+            _errc(lambda: api.register_fat_binary([("fill8", 1, 2)])),    # DuplicateKernelId
+        ]
+        api.launch(st, "fill8", [(m, 0)], [3, 8192])
+        out.append(_errc(lambda: api.stream_destroy(st)))                 # BusyStream
+        api.synchronize()
+        out.append(_errc(lambda: api.stream_destroy(st)))                 # None
+        d2, _ = api.alloc(workloads.DEVICE, 64)
+        out.append(_errc(lambda: api.page_read(d2, 0, 8, workloads.HOST_SIDE)))  # NotManaged
+        cases.append(out)
+    assert cases[0] == cases[1]
+    assert cases[0][0] == "DoubleFree" and cases[0][10] == "BusyStream"
