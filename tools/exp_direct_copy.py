@@ -1,0 +1,34 @@
+"""Does the copy engine keep PCIe speed when the host side of a D2H/H2D is
+misaligned (image payloads sit 16/24 bytes after their frame)?"""
+import torch
+
+MIB = 1 << 20
+N = 1024 * MIB
+dev = torch.empty(N + 4096, dtype=torch.uint8, device="cuda")
+host = torch.empty(N + 4096, dtype=torch.uint8).pin_memory()
+s = torch.cuda.Stream()
+
+
+def bw(direction, host_off, dev_off, piece):
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for rep in range(2):
+        torch.cuda.synchronize()
+        t0.record(s)
+        with torch.cuda.stream(s):
+            for c in range(0, N, piece):
+                h = host[host_off + c:host_off + c + piece]
+                d = dev[dev_off + c:dev_off + c + piece]
+                if direction == "d2h":
+                    h.copy_(d, non_blocking=True)
+                else:
+                    d.copy_(h, non_blocking=True)
+        t1.record(s)
+        torch.cuda.synchronize()
+    return N / (t0.elapsed_time(t1) * 1e-3) / 1e9
+
+
+for direction in ("d2h", "h2d"):
+    for host_off, dev_off in ((0, 0), (16, 0), (24, 0), (3, 0), (16, 16), (4096, 0)):
+        for piece in (16 * MIB, 64 * MIB, N):
+            print(f"{direction} host+{host_off:<5} dev+{dev_off:<3} piece {piece // MIB:5d} MiB "
+                  f"{bw(direction, host_off, dev_off, piece):6.1f} GB/s", flush=True)

@@ -22,7 +22,11 @@ d_tile = torch.zeros(W * NWIN // 65536 + 1, dtype=torch.int32, device="cuda")
 sp, sc = torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=-1)
 
 
-def run(copy=True, wait=True, piece=PIECE):
+other = torch.empty(W, dtype=torch.uint8, device="cuda")
+other_h = torch.empty(W, dtype=torch.uint8).pin_memory()
+
+
+def run(copy=True, wait=True, piece=PIECE, foreign=None):
     ev_ready = [torch.cuda.Event() for _ in range(SLOTS)]
     ev_free = [torch.cuda.Event() for _ in range(SLOTS)]
     e0 = [torch.cuda.Event(enable_timing=True) for _ in range(NWIN)]
@@ -45,7 +49,15 @@ def run(copy=True, wait=True, piece=PIECE):
             ev_ready[s].record(sp)
         with torch.cuda.stream(sc):
             sc.wait_event(ev_ready[s])
-            if copy:
+            if foreign == "d2h":  # same traffic, but not from the ring
+                for c in range(0, W, piece):
+                    other_h[c:c + piece].copy_(other[c:c + piece], non_blocking=True)
+            elif foreign == "h2d":
+                for c in range(0, W, piece):
+                    other[c:c + piece].copy_(other_h[c:c + piece], non_blocking=True)
+            elif foreign == "d2d":  # a device-side copy of the same size
+                other.copy_(ring[((s + 2) % SLOTS) * (W + 64):][:W], non_blocking=True)
+            elif copy:
                 for c in range(0, W, piece):
                     host[w * W + c:w * W + c + piece].copy_(buf[c:c + piece], non_blocking=True)
             ev_free[s].record(sc)
@@ -56,7 +68,9 @@ def run(copy=True, wait=True, piece=PIECE):
 
 
 for name, kw in [("pipeline (copy, wait)", {}), ("no copy", {"copy": False}),
-                 ("copy, no wait", {"wait": False}), ("copy 64MiB pieces", {"piece": W})]:
+                 ("copy, no wait", {"wait": False}), ("copy 64MiB pieces", {"piece": W}),
+                 ("foreign d2h", {"foreign": "d2h"}), ("foreign h2d", {"foreign": "h2d"}),
+                 ("foreign d2d", {"foreign": "d2d"}), ("no copy, no wait", {"copy": False, "wait": False})]:
     med, mn, tot = run(**kw)
     print(f"{name:24s} pack median {med:7.1f} us  min {mn:7.1f} us  total {tot:8.1f} ms "
           f"({W * NWIN / (tot * 1e-3) / 1e9:5.1f} GB/s)")
