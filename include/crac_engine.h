@@ -31,6 +31,8 @@ typedef struct crac_stats {
   uint64_t d2h_bytes, h2d_bytes, image_bytes, dirty_chunks, total_chunks;
   int32_t incremental;
   int32_t reserved;
+  double stall_ms;       /* quiesce -> the app may resume */
+  uint64_t shadow_bytes; /* stream bytes staged in the HBM shadow */
 } crac_stats_t;
 
 const char* crac_last_error(void);
@@ -76,6 +78,15 @@ void crac_image_destroy(crac_image_t* img);
 int crac_image_view(crac_image_t* img, const uint8_t** data, uint64_t* size);
 int crac_checkpoint(crac_session_t* s, crac_image_t* img, crac_stats_t* stats);
 int crac_checkpoint_incremental(crac_session_t* s, crac_image_t* img, crac_stats_t* stats);
+/* Stall-reduced drain (new): the app is quiesced only while the
+ * state is snapshotted into HBM reserved with crac_reserve_shadow; the D2H
+ * into `img` continues after crac_checkpoint_begin returns and
+ * crac_checkpoint_finish completes it.  Bytes equal crac_checkpoint's at the
+ * instant of begin.  crac_reserve_shadow(s, 0) releases the reservation;
+ * OutOfArena (1 + 8) if the HBM is not available. */
+int crac_reserve_shadow(crac_session_t* s, uint64_t bytes);
+int crac_checkpoint_begin(crac_session_t* s, crac_image_t* img, crac_stats_t* stats);
+int crac_checkpoint_finish(crac_session_t* s, crac_stats_t* stats);
 /* checkpoint(Session&) -> Snapshot -> encode_image, into a malloc'd buffer
  * released with crac_buffer_free (the reference-shaped value API). */
 int crac_checkpoint_value(crac_session_t* s, uint8_t** image, uint64_t* size);

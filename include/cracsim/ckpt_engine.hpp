@@ -107,6 +107,8 @@ struct DrainStats {
   uint64_t dirty_chunks = 0;
   uint64_t total_chunks = 0;
   bool incremental = false;
+  double stall_ms = 0;       // quiesce -> app may resume (device events)
+  uint64_t shadow_bytes = 0; // stream bytes staged in the HBM shadow
 };
 
 // ---- reference surface ----
@@ -124,6 +126,16 @@ Session restart_from_file(const std::filesystem::path& path, const KernelCatalog
 // ---- B200 fast path ----
 void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats = nullptr);
 void checkpoint_incremental(Session& session, PinnedImage& image, DrainStats* stats = nullptr);
+// Stall-reduced drain.  checkpoint_begin quiesces, drains the
+// head of the bulk stream through the ring and packs the rest into the HBM
+// shadow reserved with reserve_shadow (K1 and K4 run meanwhile), then resumes
+// the app and starts the shadow -> image D2H.  checkpoint_finish waits for it
+// and completes `out`: the bytes equal checkpoint_image's at the instant of
+// checkpoint_begin, whatever the app does in between.  With no shadow this is
+// checkpoint_image.  Any other drain first finishes a pending one.
+void reserve_shadow(Session& session, uint64_t bytes);
+void checkpoint_begin(Session& session, PinnedImage& out, DrainStats* stats = nullptr);
+void checkpoint_finish(Session& session, DrainStats* stats = nullptr);
 // K1 over every live allocation (hash-only timing; no drain).
 void hash_only(Session& session, DrainStats* stats);
 Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catalog,

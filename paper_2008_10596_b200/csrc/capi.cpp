@@ -59,6 +59,8 @@ void to_c(const DrainStats& d, crac_stats_t* o) {
   o->dirty_chunks = d.dirty_chunks;
   o->total_chunks = d.total_chunks;
   o->incremental = d.incremental ? 1 : 0;
+  o->stall_ms = d.stall_ms;
+  o->shadow_bytes = d.shadow_bytes;
 }
 
 template <typename T>
@@ -202,6 +204,26 @@ int crac_checkpoint(crac_session_t* s, crac_image_t* img, crac_stats_t* stats) {
   return guard([&] {
     DrainStats d;
     checkpoint_image(s->s, img->img, stats ? &d : nullptr);
+    to_c(d, stats);
+  });
+}
+
+int crac_reserve_shadow(crac_session_t* s, uint64_t bytes) {
+  return guard([&] { reserve_shadow(s->s, bytes); });
+}
+
+int crac_checkpoint_begin(crac_session_t* s, crac_image_t* img, crac_stats_t* stats) {
+  return guard([&] {
+    DrainStats d;
+    checkpoint_begin(s->s, img->img, stats ? &d : nullptr);
+    to_c(d, stats);
+  });
+}
+
+int crac_checkpoint_finish(crac_session_t* s, crac_stats_t* stats) {
+  return guard([&] {
+    DrainStats d;
+    checkpoint_finish(s->s, stats ? &d : nullptr);
     to_c(d, stats);
   });
 }

@@ -108,6 +108,9 @@ DrainEngine::DrainEngine(int dev) : device(dev) {
   check_cuda(cudaStreamCreateWithPriority(&s_pack, cudaStreamNonBlocking, hi), "pack stream");
   check_cuda(cudaStreamCreateWithPriority(&s_copy, cudaStreamNonBlocking, hi), "copy stream");
   check_cuda(cudaStreamCreateWithPriority(&s_hash, cudaStreamNonBlocking, lo), "hash stream");
+  check_cuda(cudaStreamCreateWithPriority(&s_shadow, cudaStreamNonBlocking, hi), "shadow stream");
+  check_cuda(cudaEventCreate(&ev_s1), "event");
+  for (cudaEvent_t& e : ev_join) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   for (int i = 0; i < kSlots; ++i) {
     check_cuda(cudaEventCreateWithFlags(&ev_ready[i], cudaEventDisableTiming), "event");
     check_cuda(cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming), "event");
@@ -129,6 +132,10 @@ DrainEngine::~DrainEngine() {
   for (cudaEvent_t e : ev_w1) cudaEventDestroy(e);
   for (cudaEvent_t e : {ev_t0, ev_t1, ev_h0, ev_h1, ev_c0, ev_c1}) cudaEventDestroy(e);
   cudaFree(d_ring);
+  if (d_shadow) cudaFree(d_shadow);
+  cudaEventDestroy(ev_s1);
+  for (cudaEvent_t e : ev_join) cudaEventDestroy(e);
+  cudaStreamDestroy(s_shadow);
   d_recs.release();
   d_tile_rec.release();
   d_pay_spans.release();
@@ -187,8 +194,13 @@ void release_engine(std::unique_ptr<DrainEngine> e) {
   if (!e) return;
   if (cudaStreamSynchronize(e->s_pack) != cudaSuccess ||
       cudaStreamSynchronize(e->s_copy) != cudaSuccess ||
-      cudaStreamSynchronize(e->s_hash) != cudaSuccess)
+      cudaStreamSynchronize(e->s_hash) != cudaSuccess ||
+      cudaStreamSynchronize(e->s_shadow) != cudaSuccess)
     return;  // a broken engine is dropped (and leaked), never pooled
+  e->pending = DrainEngine::Pending{};  // an unfinished async drain is abandoned
+  if (e->d_shadow) cudaFree(e->d_shadow);  // the shadow belongs to its session
+  e->d_shadow = nullptr;
+  e->shadow_cap = 0;
   e->plan.valid = false;  // keep the vectors' capacity for the next session
   e->plan.image_ptr = 0;
   e->prev_valid = false;
@@ -437,7 +449,7 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
       std::memcpy(r.frame + 8, &fl, 4);
       std::memcpy(r.frame + 12, &len, 4);
       if (it.flags && !((*it.flags)[p] & 1)) {
-        P.host_pages[hp++] = HostPage{at + 16, r.ptr, len, uint32_t(r.ext)};
+        P.host_pages[hp++] = HostPage{at + 16, r.ptr, len, uint32_t(r.ext), sl.rec0 + 1 + p};
         r.ptr = 0;
       }
       at += 16 + len;
@@ -569,10 +581,15 @@ uint64_t tail_bytes(Session& session) {
 // ---------------------------------------------------------------------------
 // drain
 // ---------------------------------------------------------------------------
-void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
+namespace {
+
+// Everything of a full drain that needs the app stopped: the plan, K1 + K4
+// over the live state, the ring windows [0, head) drained to the image and
+// the shadow windows [head, stream_len) packed into HBM.  Returns with every
+// kernel that reads app memory complete; the shadow D2H (if any) is enqueued
+// on s_copy and finished by drain_finish.  Runs with the gate held.
+void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStats* stats) {
   PhaseTrace tr("drain");
-  QuiesceScope q(session.table(), session.config().quiesce_timeout);
-  tr.mark("quiesce");
   DeviceContext& ctx = session.device();
   DrainEngine& E = session.drain_engine();
   if (stats) *stats = DrainStats{};
@@ -611,121 +628,234 @@ void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
   put_at<uint32_t>(img + at, 3);
   put_at<uint32_t>(img + at + 4, 0);
   put_at<uint64_t>(img + at + 8, P.len3);
+  // the tail lies past the stream: no D2H touches it
+  at = s3 + P.stream_len + 4;
+  at += write_section(img + at, 5, sec5);
+  at += write_section(img + at, 6, sec6);
+  at += write_section(img + at, 7, sec7);
+  if (at != total) raise(Errc::DeviceFault, "image layout mismatch");
+  P.tail_bytes = (20 + sec5.size()) + (20 + sec6.size()) + (20 + sec7.size());
 
+  DrainEngine::Pending& Q = E.pending;
+  Q = DrainEngine::Pending{};
+  Q.out = &out;
   const bool bulk = P.len3 + P.len4 > 0;
-  uint32_t crc3 = 0, crc4 = 0;
-  uint64_t windows = 0;
-  std::vector<uint64_t> managed_ids;
-  for (const AllocationRecord& rec : active)
-    if (rec.kind == AllocationKind::Managed) managed_ids.push_back(rec.id);
-  for (uint64_t id : managed_ids) ctx.managed_remote_access(id, true);
-  if (bulk) {
-    upload_plan(E, P, E.s_pack);
-    check_cuda(cudaEventRecord(E.ev_ready[0], E.s_pack), "event");
-    check_cuda(cudaStreamWaitEvent(E.s_hash, E.ev_ready[0], 0), "wait");
-    // K1 on all but kPackSMs SMs: the pack kernels never queue behind it
-    const uint32_t k1_ctas = uint32_t(std::max(1, E.sm_count - DrainEngine::kPackSMs));
-    check_cuda(cudaEventRecord(E.ev_h0, E.s_hash), "event");
-    if (P.pay_first.back()) hash_payloads(E, P, 0, P.pay_first.back(), k1_ctas, E.s_hash);
-    // pages: host-resident ones are read over the link, so a modest grid
-    // saturates it and leaves the rest of the SMs to the pack
-    if (P.page_first.back()) hash_pages(E, P, std::min<uint32_t>(k1_ctas, 48), E.s_hash);
-    check_cuda(cudaEventRecord(E.ev_h1, E.s_hash), "event");
-    enqueue_fold(E, P, E.s_hash);
-
-    windows = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
-    if (stats) E.ensure_window_events(windows);
-    check_cuda(cudaEventRecord(E.ev_c0, E.s_pack), "event");
-    for (uint64_t w = 0; w < windows; ++w) {
-      const int slot = int(w % DrainEngine::kSlots);
-      uint8_t* buf = E.d_ring + slot * (DrainEngine::kWindow + 64);
-      const uint64_t off = w * DrainEngine::kWindow;
-      const uint64_t len = std::min(DrainEngine::kWindow, P.stream_len - off);
-      if (w >= uint64_t(DrainEngine::kSlots))
-        check_cuda(cudaStreamWaitEvent(E.s_pack, E.ev_free[slot], 0), "wait");
-      if (stats) cudaEventRecord(E.ev_w0[w], E.s_pack);
-      check_cuda(cudaError_t(crac_pack_records(E.d_recs.ptr, uint32_t(P.recs.size()),
-                                               E.d_tile_rec.ptr + off / CRAC_TILE_BYTES, off, len,
-                                               buf, E.s_pack)),
-                 "pack");
-      if (stats) cudaEventRecord(E.ev_w1[w], E.s_pack);
-      check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_pack), "event");
-      check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_ready[slot], 0), "wait");
-      // the copy engine runs best on 16 MiB pieces; the pack on bigger windows
-      for (uint64_t c = 0; c < len; c += DrainEngine::kCopyChunk)
-        check_cuda(cudaMemcpyAsync(img + s3 + off + c, buf + c,
-                                   std::min(DrainEngine::kCopyChunk, len - c),
-                                   cudaMemcpyDeviceToHost, E.s_copy),
-                   "D2H");
-      check_cuda(cudaEventRecord(E.ev_free[slot], E.s_copy), "event");
-    }
-    check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
-    tr.mark("enqueue");
-    // the section CRCs are ready long before the D2H finishes
-    check_cuda(cudaStreamSynchronize(E.s_hash), "hash sync");
-    tr.mark("hash+fold");
-    finish_fold(E, P, crc3, crc4);
-    // seed the incremental table with this image's payload chunk CRCs
-    const uint64_t n_pay = P.pay_first.back();
-    if (n_pay) {
-      E.d_prev_crc.ensure(n_pay);
-      check_cuda(cudaMemcpyAsync(E.d_prev_crc.ptr, E.d_pay_crc.ptr, n_pay * 4,
-                                 cudaMemcpyDeviceToDevice, E.s_hash),
-                 "seed prev crc");
-    }
-    check_cuda(cudaStreamSynchronize(E.s_copy), "copy sync");
-    check_cuda(cudaStreamSynchronize(E.s_pack), "pack sync");
-    check_cuda(cudaStreamSynchronize(E.s_hash), "hash sync");
-    tr.mark("d2h-wait");
-    // host-resident pages: managed memory -> image by host threads (the
-    // windows carried zeros there; every D2H has landed)
-    parallel_for(P.host_pages.size(), [&](uint64_t i) {
-      const HostPage& h = P.host_pages[i];
-      std::memcpy(img + s3 + h.stream_off, reinterpret_cast<const void*>(h.ptr), h.len);
-    });
-    tr.mark("host-pages");
-    for (uint64_t id : managed_ids) ctx.managed_remote_access(id, false);
-  } else {
+  if (!bulk) {
     // no bulk bytes: the stream is just crc3 (0) and the UVM_PAGES header
     put_at<uint32_t>(img + s3, 0);
     put_at<uint32_t>(img + s3 + 4, 4);
     put_at<uint32_t>(img + s3 + 8, 0);
     put_at<uint64_t>(img + s3 + 12, 0);
+    Q.active = true;
+    check_cuda(cudaEventRecord(E.ev_s1, E.s_pack), "event");
+    return;
   }
-  put_at<uint32_t>(img + s3 + P.len3, crc3);
-  at = s3 + P.stream_len;
-  put_at<uint32_t>(img + at, crc4);
-  at += 4;
-  at += write_section(img + at, 5, sec5);
-  at += write_section(img + at, 6, sec6);
-  at += write_section(img + at, 7, sec7);
-  if (at != total) raise(Errc::DeviceFault, "image layout mismatch");
+
+  // split: ring windows [0, head) during the stall, shadow [head, end) after
+  constexpr uint64_t W = DrainEngine::kWindow;
+  uint64_t head = P.stream_len;
+  if (use_shadow && E.shadow_cap) {
+    const uint64_t want = P.stream_len > E.shadow_cap ? P.stream_len - E.shadow_cap : 0;
+    head = std::min(P.stream_len, (want + W - 1) / W * W);
+  }
+  Q.head = head;
+  // host-resident pages reaching into the shadow part are read by the pack
+  // kernels over the link (the app may touch them once it resumes); pages
+  // wholly in the ring part keep the host-thread copy after its D2H
+  std::vector<HostPage> ring_pages;
+  for (const HostPage& h : P.host_pages) {
+    if (h.stream_off + h.len > head)
+      P.recs[h.rec].ptr = h.ptr;
+    else
+      ring_pages.push_back(h);
+  }
+
+  std::vector<uint64_t> managed_ids;
+  for (const AllocationRecord& rec : active)
+    if (rec.kind == AllocationKind::Managed) managed_ids.push_back(rec.id);
+  for (uint64_t id : managed_ids) ctx.managed_remote_access(id, true);
+
+  upload_plan(E, P, E.s_pack);
+  check_cuda(cudaEventRecord(E.ev_ready[0], E.s_pack), "event");
+  check_cuda(cudaStreamWaitEvent(E.s_hash, E.ev_ready[0], 0), "wait");
+  check_cuda(cudaStreamWaitEvent(E.s_shadow, E.ev_ready[0], 0), "wait");
+  // K1 on all but kPackSMs SMs: the pack kernels never queue behind it
+  const uint32_t k1_ctas = uint32_t(std::max(1, E.sm_count - DrainEngine::kPackSMs));
+  check_cuda(cudaEventRecord(E.ev_h0, E.s_hash), "event");
+  if (P.pay_first.back()) hash_payloads(E, P, 0, P.pay_first.back(), k1_ctas, E.s_hash);
+  // pages: host-resident ones are read over the link, so a modest grid
+  // saturates it and leaves the rest of the SMs to the pack
+  if (P.page_first.back()) hash_pages(E, P, std::min<uint32_t>(k1_ctas, 48), E.s_hash);
+  check_cuda(cudaEventRecord(E.ev_h1, E.s_hash), "event");
+  enqueue_fold(E, P, E.s_hash);
+
+  // shadow windows: pack at HBM speed on their own stream, beside the ring
+  for (uint64_t off = head; off < P.stream_len; off += W) {
+    const uint64_t len = std::min(W, P.stream_len - off);
+    check_cuda(cudaError_t(crac_pack_records(E.d_recs.ptr, uint32_t(P.recs.size()),
+                                             E.d_tile_rec.ptr + off / CRAC_TILE_BYTES, off, len,
+                                             E.d_shadow + (off - head), E.s_shadow)),
+               "pack shadow");
+  }
+
+  const uint64_t windows = (head + W - 1) / W;
+  Q.windows = windows;
+  if (stats) E.ensure_window_events(windows);
+  check_cuda(cudaEventRecord(E.ev_c0, E.s_pack), "event");
+  for (uint64_t w = 0; w < windows; ++w) {
+    const int slot = int(w % DrainEngine::kSlots);
+    uint8_t* buf = E.d_ring + slot * (W + 64);
+    const uint64_t off = w * W;
+    const uint64_t len = std::min(W, head - off);
+    if (w >= uint64_t(DrainEngine::kSlots))
+      check_cuda(cudaStreamWaitEvent(E.s_pack, E.ev_free[slot], 0), "wait");
+    if (stats) cudaEventRecord(E.ev_w0[w], E.s_pack);
+    check_cuda(cudaError_t(crac_pack_records(E.d_recs.ptr, uint32_t(P.recs.size()),
+                                             E.d_tile_rec.ptr + off / CRAC_TILE_BYTES, off, len,
+                                             buf, E.s_pack)),
+               "pack");
+    if (stats) cudaEventRecord(E.ev_w1[w], E.s_pack);
+    check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_pack), "event");
+    check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_ready[slot], 0), "wait");
+    // the copy engine runs best on 16 MiB pieces; the pack on bigger windows
+    for (uint64_t c = 0; c < len; c += DrainEngine::kCopyChunk)
+      check_cuda(cudaMemcpyAsync(img + s3 + off + c, buf + c,
+                                 std::min(DrainEngine::kCopyChunk, len - c),
+                                 cudaMemcpyDeviceToHost, E.s_copy),
+                 "D2H");
+    check_cuda(cudaEventRecord(E.ev_free[slot], E.s_copy), "event");
+  }
+  // snapshot complete = K1/K4, the shadow packs and the ring D2H have landed
+  check_cuda(cudaEventRecord(E.ev_join[0], E.s_hash), "event");
+  check_cuda(cudaEventRecord(E.ev_join[1], E.s_shadow), "event");
+  check_cuda(cudaEventRecord(E.ev_join[2], E.s_copy), "event");
+  for (cudaEvent_t e : E.ev_join) check_cuda(cudaStreamWaitEvent(E.s_pack, e, 0), "wait");
+  check_cuda(cudaEventRecord(E.ev_s1, E.s_pack), "event");
+  tr.mark("enqueue");
+  // the section CRCs are ready long before the D2H finishes
+  check_cuda(cudaStreamSynchronize(E.s_hash), "hash sync");
+  tr.mark("hash+fold");
+  finish_fold(E, P, Q.crc3, Q.crc4);
+  // seed the incremental table with this image's payload chunk CRCs
+  const uint64_t n_pay = P.pay_first.back();
+  if (n_pay) {
+    E.d_prev_crc.ensure(n_pay);
+    check_cuda(cudaMemcpyAsync(E.d_prev_crc.ptr, E.d_pay_crc.ptr, n_pay * 4,
+                               cudaMemcpyDeviceToDevice, E.s_hash),
+               "seed prev crc");
+  }
+  check_cuda(cudaEventSynchronize(E.ev_s1), "snapshot sync");
+  tr.mark("d2h-wait");
+  // host-resident pages of the ring part: managed memory -> image by host
+  // threads (the windows carried zeros there; their D2H has landed)
+  parallel_for(ring_pages.size(), [&](uint64_t i) {
+    const HostPage& h = ring_pages[i];
+    std::memcpy(img + s3 + h.stream_off, reinterpret_cast<const void*>(h.ptr), h.len);
+  });
+  tr.mark("host-pages");
+  for (uint64_t id : managed_ids) ctx.managed_remote_access(id, false);
+  for (const HostPage& h : P.host_pages) P.recs[h.rec].ptr = 0;  // the plan's invariant
+
+  // the app may run from here on: the shadow -> image D2H reads only HBM
+  // that belongs to the engine
+  for (uint64_t c = 0; head + c < P.stream_len; c += DrainEngine::kCopyChunk)
+    check_cuda(cudaMemcpyAsync(img + s3 + head + c, E.d_shadow + c,
+                               std::min(DrainEngine::kCopyChunk, P.stream_len - head - c),
+                               cudaMemcpyDeviceToHost, E.s_copy),
+               "D2H shadow");
+  check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
+  Q.active = true;
+}
+
+// Waits for the shadow D2H and completes the image.  No gate needed.
+void drain_finish(Session& session, DrainStats* stats) {
+  DrainEngine& E = session.drain_engine();
+  DrainEngine::Pending& Q = E.pending;
+  if (!Q.active) return;
+  ImagePlan& P = E.plan;
+  uint8_t* img = Q.out->mutable_data();
+  check_cuda(cudaStreamWaitEvent(E.s_pack, E.ev_c1, 0), "wait");
+  check_cuda(cudaEventRecord(E.ev_t1, E.s_pack), "event");
+  check_cuda(cudaEventSynchronize(E.ev_t1), "drain sync");
+  // crc3 lies inside the stream (the windows carried zeros there)
+  put_at<uint32_t>(img + P.s3 + P.len3, Q.crc3);
+  put_at<uint32_t>(img + P.s3 + P.stream_len, Q.crc4);
   P.valid = true;
-  P.tail_bytes = (20 + sec5.size()) + (20 + sec6.size()) + (20 + sec7.size());
   P.image_ptr = reinterpret_cast<uint64_t>(img);
   E.prev_valid = P.pay_first.back() > 0;
-
-  check_cuda(cudaEventRecord(E.ev_t1, E.s_pack), "event");
-  check_cuda(cudaEventSynchronize(E.ev_t1), "event sync");
+  const bool bulk = P.len3 + P.len4 > 0;
   if (stats) {
+    *stats = DrainStats{};
     stats->total_ms = elapsed(E.ev_t0, E.ev_t1);
+    stats->stall_ms = elapsed(E.ev_t0, E.ev_s1);
     if (bulk) {
       stats->hash_ms = elapsed(E.ev_h0, E.ev_h1);
       stats->copy_ms = elapsed(E.ev_c0, E.ev_c1);
       stats->hash_launches = (P.pay_first.back() ? 1 : 0) + (P.page_first.back() ? 1 : 0);
       stats->hash_bytes = hashed_bytes(P);
-      stats->pack_launches = windows;
+      stats->pack_launches = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
       stats->pack_bytes = P.stream_len;
-      stats->pack_ms = median_window_ms(E, windows);  // per launch
+      stats->pack_ms = Q.windows ? median_window_ms(E, Q.windows) : 0;  // per ring launch
       stats->d2h_bytes = P.stream_len;
+      stats->shadow_bytes = P.stream_len - Q.head;
     }
-    stats->image_bytes = total;
+    stats->image_bytes = P.image_bytes;
     stats->total_chunks = P.pay_first.back() + P.page_first.back();
     stats->dirty_chunks = stats->total_chunks;
   }
+  Q = DrainEngine::Pending{};
 }
 
+void finish_pending(Session& session) {
+  if (session.drain_engine().pending.active) drain_finish(session, nullptr);
+}
+
+}  // namespace
+
+void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
+  finish_pending(session);
+  {
+    QuiesceScope q(session.table(), session.config().quiesce_timeout);
+    drain_locked(session, out, false, stats);
+  }
+  drain_finish(session, stats);
+}
+
+void reserve_shadow(Session& session, uint64_t bytes) {
+  finish_pending(session);
+  DrainEngine& E = session.drain_engine();
+  bytes = (bytes + DrainEngine::kWindow - 1) / DrainEngine::kWindow * DrainEngine::kWindow;
+  if (bytes == E.shadow_cap) return;
+  if (E.d_shadow) check_cuda(cudaFree(E.d_shadow), "free shadow");
+  E.d_shadow = nullptr;
+  E.shadow_cap = 0;
+  if (!bytes) return;
+  // +64: the pack of the last window writes whole 16-byte words
+  const cudaError_t e = cudaMalloc(&E.d_shadow, bytes + 64);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    E.d_shadow = nullptr;
+    raise(Errc::OutOfArena, "reserve_shadow: " + std::to_string(bytes) + " bytes of HBM unavailable");
+  }
+  E.shadow_cap = bytes;
+}
+
+void checkpoint_begin(Session& session, PinnedImage& out, DrainStats* stats) {
+  finish_pending(session);
+  QuiesceScope q(session.table(), session.config().quiesce_timeout);
+  drain_locked(session, out, true, nullptr);
+  if (stats) {
+    *stats = DrainStats{};
+    DrainEngine& E = session.drain_engine();
+    stats->stall_ms = elapsed(E.ev_t0, E.ev_s1);
+    stats->shadow_bytes = E.plan.stream_len - E.pending.head;
+  }
+}
+
+void checkpoint_finish(Session& session, DrainStats* stats) { drain_finish(session, stats); }
+
 void hash_only(Session& session, DrainStats* stats) {
+  finish_pending(session);
   QuiesceScope q(session.table(), session.config().quiesce_timeout);
   DeviceContext& ctx = session.device();
   DrainEngine& E = session.drain_engine();
@@ -1032,6 +1162,7 @@ void checkpoint_incremental(Session& session, PinnedImage& image, DrainStats* st
   // previous image of this session is unchanged (same log, same bulk
   // records, no managed allocations, same tail size) and `image` is that
   // image; otherwise this is a full drain.
+  finish_pending(session);
   DrainEngine& E = session.drain_engine();
   const ImagePlan& P = E.plan;
   auto layout_unchanged = [&] {

@@ -55,6 +55,7 @@ struct HostPage {
   uint64_t stream_off;  // content offset in the bulk stream
   uint64_t ptr;         // managed address of the page
   uint32_t len, ext;    // content bytes; bytes to write on refill (zero tail)
+  uint64_t rec;         // its record in ImagePlan::recs (ptr zeroed there)
 };
 
 struct ImagePlan {
@@ -102,6 +103,23 @@ struct DrainEngine {
   DevArray<uint32_t> d_fold;   // linear parts of crc3 / crc4 (K4)
   HostArray<uint32_t> h_fold;
   HostArray<uint64_t> h_count, h_dirty_idx;
+
+  // Stall-reduced drain (checkpoint_begin/finish): the tail of the bulk
+  // stream is packed into this HBM shadow while the app is quiesced and copied
+  // out after it resumes.  Reserved explicitly (reserve_shadow), never inside
+  // a drain.
+  cudaStream_t s_shadow = nullptr;
+  cudaEvent_t ev_s1 = nullptr, ev_join[3] = {};
+  uint8_t* d_shadow = nullptr;
+  uint64_t shadow_cap = 0;
+  struct Pending {
+    bool active = false;
+    PinnedImage* out = nullptr;
+    uint64_t head = 0;       // stream bytes drained through the ring (stall)
+    uint32_t crc3 = 0, crc4 = 0;
+    uint64_t windows = 0;    // ring windows (stats)
+    double stall_ms = 0;
+  } pending;
 
   ImagePlan plan;
   bool prev_valid = false;      // d_prev_crc holds the chunk CRCs of `plan`'s image

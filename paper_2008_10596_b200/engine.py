@@ -40,7 +40,8 @@ class Stats(C.Structure):
                 ("d2h_bytes", C.c_uint64), ("h2d_bytes", C.c_uint64),
                 ("image_bytes", C.c_uint64), ("dirty_chunks", C.c_uint64),
                 ("total_chunks", C.c_uint64), ("incremental", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("reserved", C.c_int32), ("stall_ms", C.c_double),
+                ("shadow_bytes", C.c_uint64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
@@ -77,6 +78,9 @@ _SIGS = {
     "crac_checkpoint": (C.c_int, [_P, _P, C.POINTER(Stats)]),
     "crac_checkpoint_incremental": (C.c_int, [_P, _P, C.POINTER(Stats)]),
     "crac_checkpoint_value": (C.c_int, [_P, C.POINTER(_P), _PU64]),
+    "crac_reserve_shadow": (C.c_int, [_P, _U64]),
+    "crac_checkpoint_begin": (C.c_int, [_P, _P, C.POINTER(Stats)]),
+    "crac_checkpoint_finish": (C.c_int, [_P, C.POINTER(Stats)]),
     "crac_restart": (C.c_int, [_P, _U64, C.c_int, C.POINTER(_P), C.POINTER(Stats)]),
     "crac_decode_check": (C.c_int, [_P, _U64]),
     "crac_summarize": (C.c_int, [_P, _U64, _PU64, _PU32, _PU64]),
@@ -281,6 +285,21 @@ class Session:
         st = Stats()
         fn = lib().crac_checkpoint_incremental if incremental else lib().crac_checkpoint
         _check(fn(self._h, image._h, C.byref(st)))
+        return st.as_dict()
+
+    def reserve_shadow(self, nbytes: int) -> None:
+        """HBM the stall-reduced drain may stage the stream in (0 releases it)."""
+        _check(lib().crac_reserve_shadow(self._h, nbytes))
+
+    def checkpoint_begin(self, image: Image) -> dict:
+        """Quiesce, snapshot into the shadow, resume; the D2H keeps running."""
+        st = Stats()
+        _check(lib().crac_checkpoint_begin(self._h, image._h, C.byref(st)))
+        return st.as_dict()
+
+    def checkpoint_finish(self) -> dict:
+        st = Stats()
+        _check(lib().crac_checkpoint_finish(self._h, C.byref(st)))
         return st.as_dict()
 
     def checkpoint_value(self) -> bytes:

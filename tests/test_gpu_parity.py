@@ -425,3 +425,81 @@ def test_error_codes_match_reference(eng):
         cases.append(out)
     assert cases[0] == cases[1]
     assert cases[0][0] == "DoubleFree" and cases[0][10] == "BusyStream"
+
+
+# ---------------------------------------------------------------------------
+# stall-reduced drain (checkpoint_begin / checkpoint_finish)
+# ---------------------------------------------------------------------------
+MIB = 1 << 20
+
+
+def _big_state(api):
+    """3 x 40 MiB device regions, an 80 MiB managed allocation with 1 MiB
+    alternating residence, plus every small section populated."""
+    workloads.drive_small(api, seed=4)
+    for k in range(3):
+        i, _ = api.alloc(workloads.DEVICE, 40 * MIB - 17 * k)
+        api.fill_synthetic(i, 20 + k)
+    m, _ = api.alloc(workloads.MANAGED, 80 * MIB + 333)
+    api.fill_synthetic(m, 9, workloads.DEVICE_SIDE)
+    for off in range(MIB, 80 * MIB, 2 * MIB):
+        api.page_read(m, off, MIB, workloads.HOST_SIDE)
+    return m
+
+
+@pytest.mark.parametrize("shadow_mib", [0, 64, 128, 512])
+def test_async_drain_is_the_image_at_begin(eng, shadow_mib):
+    s = eng.Session(seed=6, arena_bytes=512 * MIB)
+    m = _big_state(s)
+    want = s.checkpoint()[0]
+    s.reserve_shadow(shadow_mib * MIB)
+    img = eng.Image()
+    st = s.checkpoint_begin(img)
+    stream = len(want) - 1000  # roughly the bulk stream
+    if shadow_mib >= 512:
+        assert st["shadow_bytes"] > stream - 64 * MIB
+    elif shadow_mib == 0:
+        assert st["shadow_bytes"] == 0
+    else:
+        assert 0 < st["shadow_bytes"] <= shadow_mib * MIB
+    # the app runs while the D2H drains: none of this may reach the image
+    s.mutate(seed=1, epoch=1, threshold=(1 << 64) - 1)
+    s.page_write(m, 5 * MIB, b"\xEE" * 8192, workloads.HOST_SIDE)
+    s.page_write(m, 6 * MIB, b"\xDD" * 8192, workloads.DEVICE_SIDE)
+    x, _ = s.alloc(workloads.DEVICE, 4096)
+    s.free(x)
+    done = s.checkpoint_finish()
+    assert img.tobytes() == want
+    assert done["stall_ms"] <= done["total_ms"]
+    assert done["d2h_bytes"] > 0
+    rs, _ = eng.restart(img.tobytes())
+    assert rs.checkpoint()[0] == want
+    assert s.checkpoint()[0] != want  # the mutations are live
+
+
+def test_async_drain_matches_reference_small(eng):
+    s = eng.Session(seed=2, arena_bytes=1 << 22)
+    r = ref.RefSession(seed=2, arena_bytes=1 << 22)
+    for api in (s, r):
+        workloads.drive_small(api, seed=3)
+    s.reserve_shadow(64 * MIB)
+    img = eng.Image()
+    s.checkpoint_begin(img)
+    s.copy_h2d(s.live_records()[0].id, 0, b"\x01" * 16)
+    s.checkpoint_finish()
+    assert img.tobytes() == r.checkpoint()[0]
+
+
+def test_async_then_incremental_and_implicit_finish(eng):
+    s = eng.Session(seed=1, arena_bytes=256 * MIB)
+    workloads.build_regions(s, 5, lambda k: 20 * MIB + k, seed=3)
+    s.reserve_shadow(256 * MIB)
+    img = eng.Image()
+    s.checkpoint_begin(img)
+    # any other drain finishes the pending one first
+    s.mutate(seed=5, epoch=1, threshold=1 << 61)  # new content = synth(6)
+    st = s.checkpoint_into(img, incremental=True)
+    assert st["incremental"] == 1 and 0 < st["dirty_chunks"] < st["total_chunks"]
+    assert img.tobytes() == s.checkpoint()[0]
+    s.reserve_shadow(0)
+    assert s.checkpoint_finish()["total_ms"] == 0  # nothing pending
