@@ -143,6 +143,7 @@ DrainEngine::~DrainEngine() {
   d_pay_first.release();
   d_page_first.release();
   d_pay_dst.release();
+  d_pay_soff.release();
   d_pay_crc.release();
   d_page_crc.release();
   d_prev_crc.release();
@@ -675,14 +676,30 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
     if (rec.kind == AllocationKind::Managed) managed_ids.push_back(rec.id);
   for (uint64_t id : managed_ids) ctx.managed_remote_access(id, true);
 
+  // With the whole stream in the shadow, K1 copies every payload chunk to
+  // its stream position right after hashing it: one HBM read of the state
+  // instead of two; frames and the UVM_PAGES part are written beside it.
+  const bool fused = use_shadow && head == 0 && !P.pay_spans.empty();
   upload_plan(E, P, E.s_pack);
+  if (fused) upload(E.d_pay_soff, P.pay_rec_off, E.s_pack);
   check_cuda(cudaEventRecord(E.ev_ready[0], E.s_pack), "event");
   check_cuda(cudaStreamWaitEvent(E.s_hash, E.ev_ready[0], 0), "wait");
   check_cuda(cudaStreamWaitEvent(E.s_shadow, E.ev_ready[0], 0), "wait");
   // K1 on all but kPackSMs SMs: the pack kernels never queue behind it
   const uint32_t k1_ctas = uint32_t(std::max(1, E.sm_count - DrainEngine::kPackSMs));
   check_cuda(cudaEventRecord(E.ev_h0, E.s_hash), "event");
-  if (P.pay_first.back()) hash_payloads(E, P, 0, P.pay_first.back(), k1_ctas, E.s_hash);
+  if (fused) {
+    check_cuda(cudaError_t(crac_hash_drain_range(
+                   E.d_pay_spans.ptr, E.d_pay_first.ptr, uint32_t(P.pay_spans.size()),
+                   DrainEngine::kChunk, 0, P.pay_first.back(), E.d_pay_crc.ptr, nullptr,
+                   E.d_pay_soff.ptr, E.d_shadow, nullptr, E.s_hash)),
+               "K1 hash+copy");
+    check_cuda(cudaError_t(crac_write_frames(E.d_recs.ptr, uint32_t(P.pay_spans.size()),
+                                             E.d_shadow, E.s_shadow)),
+               "frames");
+  } else if (P.pay_first.back()) {
+    hash_payloads(E, P, 0, P.pay_first.back(), k1_ctas, E.s_hash);
+  }
   // pages: host-resident ones are read over the link, so a modest grid
   // saturates it and leaves the rest of the SMs to the pack
   if (P.page_first.back()) hash_pages(E, P, std::min<uint32_t>(k1_ctas, 48), E.s_hash);
@@ -690,7 +707,9 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   enqueue_fold(E, P, E.s_hash);
 
   // shadow windows: pack at HBM speed on their own stream, beside the ring
-  for (uint64_t off = head; off < P.stream_len; off += W) {
+  // (fused: only from the 16-byte word holding crc3 on; the payload bytes
+  // that word shares are rewritten with the same values)
+  for (uint64_t off = fused ? (P.len3 & ~uint64_t(15)) : head; off < P.stream_len; off += W) {
     const uint64_t len = std::min(W, P.stream_len - off);
     check_cuda(cudaError_t(crac_pack_records(E.d_recs.ptr, uint32_t(P.recs.size()),
                                              E.d_tile_rec.ptr + off / CRAC_TILE_BYTES, off, len,

@@ -96,7 +96,7 @@ struct DrainEngine {
   DevArray<crac_record_t> d_recs;
   DevArray<uint32_t> d_tile_rec;
   DevArray<crac_span_t> d_pay_spans, d_page_spans;
-  DevArray<uint64_t> d_pay_first, d_page_first, d_pay_dst;
+  DevArray<uint64_t> d_pay_first, d_page_first, d_pay_dst, d_pay_soff;
   DevArray<uint32_t> d_pay_crc, d_page_crc, d_prev_crc, d_block_counts;
   DevArray<uint64_t> d_dirty_idx, d_dirty_count;
   DevArray<unsigned long long> d_counters;

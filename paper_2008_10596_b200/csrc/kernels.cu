@@ -329,9 +329,9 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     }
     const uint32_t crc = __shfl_sync(0xFFFFFFFFu, L, 0);
     if (lane == 0) out[c] = crc;
-    if (crc != hd.prev[c]) {  // warp-uniform
-      if (lane == 0) {
-        hd.prev[c] = crc;
+    if (!hd.prev || crc != hd.prev[c]) {  // warp-uniform; no prev table = copy every chunk
+      if (lane == 0 && hd.prev) hd.prev[c] = crc;
+      if (lane == 0 && hd.counters) {
         atomicAdd(&hd.counters[0], 1ull);
         atomicAdd(&hd.counters[1], (unsigned long long)len);
       }
@@ -472,6 +472,18 @@ __global__ void __launch_bounds__(kPackThreads)
       *out = v;
     }
   }
+}
+
+// Frame bytes of records [0, n) at dst + out_off, byte by byte: the words
+// they share with payload bytes are written by other warps (the hash+copy
+// pass), so nothing outside the frame may be stored.
+__global__ void k_write_frames(const crac_record_t* __restrict__ recs, uint32_t n,
+                               uint8_t* __restrict__ dst) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  const uint64_t r = i / 32, b = i % 32;
+  if (r >= n) return;
+  const crac_record_t& R = recs[r];
+  if (b < R.frame_len) dst[R.out_off + b] = R.frame[b];
 }
 
 // ---------------------------------------------------------------------------
@@ -886,6 +898,15 @@ int crac_hash_drain_range(const crac_span_t* d_spans, const uint64_t* d_chunk_fi
   return int(cudaGetLastError());
 }
 
+int crac_write_frames(const crac_record_t* d_recs, uint32_t n_recs, uint8_t* d_stream,
+                      void* stream) {
+  if (n_recs == 0) return 0;
+  const uint64_t threads = uint64_t(n_recs) * 32;
+  k_write_frames<<<unsigned((threads + 255) / 256), 256, 0, cudaStream_t(stream)>>>(d_recs, n_recs,
+                                                                                   d_stream);
+  return int(cudaGetLastError());
+}
+
 int crac_fold_sections(const crac_record_t* d_recs, uint32_t n_recs, const uint64_t* d_pay_first,
                        const uint32_t* d_pay_crc, uint32_t n_pay, const uint32_t* d_page_crc,
                        uint64_t len3, uint64_t total_pay_chunks, uint32_t* d_out, void* stream) {
@@ -902,7 +923,9 @@ int crac_fold_sections(const crac_record_t* d_recs, uint32_t n_recs, const uint6
 int crac_pack_records(const crac_record_t* d_recs, uint32_t n_recs, const uint32_t* d_tile_rec,
                       uint64_t win_off, uint64_t win_len, uint8_t* d_out, void* stream) {
   if (win_len == 0 || n_recs == 0) return 0;
-  if (win_off % CRAC_TILE_BYTES) return int(cudaErrorInvalidValue);
+  // tile b of the launch starts at win_off + b * TILE; d_tile_rec[b] (the
+  // record of the aligned tile containing that) never lies past its record
+  if (win_off % 16) return int(cudaErrorInvalidValue);
   const uint64_t tiles = (win_len + CRAC_TILE_BYTES - 1) / CRAC_TILE_BYTES;
   k_pack_records<<<unsigned(tiles), kPackThreads, 0, cudaStream_t(stream)>>>(
       d_recs, n_recs, d_tile_rec, win_off, win_len, d_out);

@@ -199,6 +199,14 @@ def test_pack_scatter_round_trip_random_records(eng):
     want = b"".join(struct.pack("<QQ", k + 1, s) + bytes(t[:s].cpu().numpy())
                     for k, (t, s, e) in enumerate(regions))
     assert bytes(packed[:stream_len].cpu().numpy()) == want
+    # windows need only 16-byte alignment
+    for w0, wl in ((tile + 48, 2 * tile + 5), (16, stream_len - 16),
+                   ((stream_len - 40) & ~15, stream_len - ((stream_len - 40) & ~15))):
+        buf = torch.zeros(wl + 64, dtype=torch.uint8).cuda()
+        assert L.crac_pack_records(_p(d_recs), len(recs), C.c_void_p(d_tile.data_ptr() + 4 * (w0 // tile)),
+                                   w0, wl, _p(buf), None) == 0
+        torch.cuda.synchronize()
+        assert bytes(buf[:wl].cpu().numpy()) == want[w0:w0 + wl]
     # scatter back into scribbled regions
     for t, s, e in regions:
         t.fill_(0xEE)
