@@ -391,6 +391,29 @@ WORKLOAD_NAMES = {
 }
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the newest
+    committed `ncu --set full` summary (profiles/*/ncu_full.json)."""
+    if not kernel:
+        return None, None
+    name = kernel.split(" ")[0]
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    for path in sorted(Path(__file__).parent.glob("profiles/*/ncu_full.json"), reverse=True):
+        try:
+            full = json.loads(path.read_text())
+        except (OSError, ValueError):
+            continue
+        for key, m in full.items():
+            if name not in key:
+                continue
+            total = 0.0
+            for metric in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                val, unit = m[metric].split()
+                total += float(val) * units[unit]
+            return int(total), f"{path.parent.name}/{path.name}: {key}"
+    return None, None
+
+
 def measure_stall(torch, sess, image, stream_bytes: int, sync_ms: float, args) -> dict:
     """checkpoint_begin/finish with the largest shadow free HBM allows: the
     app-visible stall (quiesce -> resume) against the synchronous drain."""
@@ -546,9 +569,14 @@ def main() -> None:
     if refills[-1]["pack_launches"]:
         n = refills[-1]["pack_launches"]
         kernels["k_scatter_records"] = (mean("pack_ms", refills), 2 * refills[-1]["pack_bytes"] / n, n)
+    if refills[-1]["hash_launches"]:  # the refill's verify K1 (batches of completed regions)
+        n = refills[-1]["hash_launches"]
+        kernels["k1_chunk_crc (refill verify)"] = (mean("hash_ms", refills) / n,
+                                                   refills[-1]["hash_bytes"] / n, n)
     dom = max(kernels, key=lambda k: kernels[k][0] * kernels[k][2]) if kernels else None
     dom_ms, dom_bytes, _ = kernels[dom] if dom else (0.0, 0, 0)
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
+    traffic, traffic_src = ncu_traffic(dom)
 
     # incremental (C5 shape on the resident state): hash-only and a 1 % dirty drain
     incremental = None
@@ -602,14 +630,17 @@ def main() -> None:
                         "image_bytes": drains[-1]["image_bytes"]},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                          "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                         "traffic": None, "peak_source": peaks["source"],
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peaks["source"],
                          "algorithmic_bytes_per_launch": int(dom_bytes),
                          "avg_launch_ms": round(dom_ms, 4),
                          "isolated": {k: {**v, "frac": round(v["GBps"] / hbm, 4)}
                                       for k, v in isolated.items()},
-                         "note": "in-situ launch times (timed region, median window) include "
-                                 "queueing behind the copy engines; 'isolated' = the same kernel "
-                                 "back to back on one stream"},
+                         "note": "in-situ launch times (timed region, median window) run "
+                                 "beside PCIe copy traffic, which slows this kernel ~2x "
+                                 "(profiles/r01/pack_insitu.txt); 'isolated' = the same kernel "
+                                 "back to back on one stream; traffic = ncu DRAM bytes per "
+                                 "launch (writes still in L2 at kernel end are not counted)"},
             "pcie_roofline": {"d2h_GBps": round(d2h, 2), "h2d_GBps": round(h2d, 2),
                               "d2h_peak_GBps": pd, "h2d_peak_GBps": ph,
                               "peak_source": "measured in this run (16 MiB pinned copies)",

@@ -130,6 +130,8 @@ DrainEngine::~DrainEngine() {
   }
   for (cudaEvent_t e : ev_w0) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_w1) cudaEventDestroy(e);
+  for (cudaEvent_t e : ev_v0) cudaEventDestroy(e);
+  for (cudaEvent_t e : ev_v1) cudaEventDestroy(e);
   for (cudaEvent_t e : {ev_t0, ev_t1, ev_h0, ev_h1, ev_c0, ev_c1}) cudaEventDestroy(e);
   cudaFree(d_ring);
   if (d_shadow) cudaFree(d_shadow);
@@ -158,6 +160,16 @@ DrainEngine::~DrainEngine() {
   cudaStreamDestroy(s_pack);
   cudaStreamDestroy(s_copy);
   cudaStreamDestroy(s_hash);
+}
+
+void DrainEngine::ensure_verify_events(size_t n) {
+  while (ev_v0.size() < n) {
+    cudaEvent_t a, b;
+    check_cuda(cudaEventCreate(&a), "event");
+    check_cuda(cudaEventCreate(&b), "event");
+    ev_v0.push_back(a);
+    ev_v1.push_back(b);
+  }
 }
 
 void DrainEngine::ensure_window_events(size_t n) {
@@ -1014,7 +1026,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   } joiner{host_fill};
   tr.mark("place");
 
-  uint64_t windows = 0;
+  uint64_t windows = 0, verifies = 0;
   if (P.stream_len > 20) {
     upload_plan(E, P, E.s_pack);
     check_cuda(cudaEventRecord(E.ev_ready[0], E.s_pack), "event");
@@ -1023,6 +1035,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     if (stats) E.ensure_window_events(windows);
     check_cuda(cudaEventRecord(E.ev_c0, E.s_copy), "event");
     size_t spans_done = 0;
+    constexpr uint64_t kVerifyBatch = 8192;  // 512 MiB of 64 KiB chunks
     for (uint64_t w = 0; w < windows; ++w) {
       const int slot = int(w % DrainEngine::kSlots);
       uint8_t* buf = E.d_ring + slot * (DrainEngine::kWindow + 64);
@@ -1045,22 +1058,35 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
                  "scatter");
       if (stats) cudaEventRecord(E.ev_w1[w], E.s_pack);
       check_cuda(cudaEventRecord(E.ev_free[slot], E.s_pack), "event");
-      // verify as we go: re-hash every region whose last byte has landed
+      // verify as we go: re-hash the regions whose last byte has landed, in
+      // batches big enough to fill every SM (one 64 MiB region is only 64
+      // K1 CTAs, and a warp hashing a single chunk never reaches its stride)
       size_t done = spans_done;
       while (done < P.pay_spans.size() &&
              P.pay_rec_off[done] + P.pay_spans[done].len <= off + len)
         ++done;
-      if (done > spans_done) {
+      if (done > spans_done && (P.pay_first[done] - P.pay_first[spans_done] >= kVerifyBatch ||
+                                w + 1 == windows)) {
+        if (stats) {
+          E.ensure_verify_events(verifies + 1);
+          cudaEventRecord(E.ev_v0[verifies], E.s_pack);
+        }
         hash_payloads(E, P, P.pay_first[spans_done], P.pay_first[done], 0, E.s_pack);
-        if (stats) ++stats->hash_launches;
+        if (stats) cudaEventRecord(E.ev_v1[verifies], E.s_pack);
+        ++verifies;
         spans_done = done;
       }
     }
     check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
     host_fill.join();  // host-resident pages must be in place before their K1
     if (P.page_first.back()) {
+      if (stats) {
+        E.ensure_verify_events(verifies + 1);
+        cudaEventRecord(E.ev_v0[verifies], E.s_pack);
+      }
       hash_pages(E, P, 0, E.s_pack);
-      if (stats) ++stats->hash_launches;
+      if (stats) cudaEventRecord(E.ev_v1[verifies], E.s_pack);
+      ++verifies;
     }
     enqueue_fold(E, P, E.s_pack);
     tr.mark("enqueue");
@@ -1091,6 +1117,8 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       stats->pack_ms = median_window_ms(E, windows);
       stats->h2d_bytes = P.stream_len;
       stats->hash_bytes = hashed_bytes(P);
+      stats->hash_launches = verifies;
+      for (uint64_t v = 0; v < verifies; ++v) stats->hash_ms += elapsed(E.ev_v0[v], E.ev_v1[v]);
     }
     stats->image_bytes = raw.size();
     stats->total_chunks = P.pay_first.back() + P.page_first.back();

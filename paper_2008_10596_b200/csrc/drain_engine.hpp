@@ -91,6 +91,7 @@ struct DrainEngine {
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr, ev_h0 = nullptr, ev_h1 = nullptr;
   cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr;
   std::vector<cudaEvent_t> ev_w0, ev_w1;  // per-window kernel timing (stats only)
+  std::vector<cudaEvent_t> ev_v0, ev_v1;  // per refill-verify K1 launch (stats only)
   uint8_t* d_ring = nullptr;
 
   DevArray<crac_record_t> d_recs;
@@ -130,6 +131,7 @@ struct DrainEngine {
   DrainEngine(const DrainEngine&) = delete;
   DrainEngine& operator=(const DrainEngine&) = delete;
   void ensure_window_events(size_t n);
+  void ensure_verify_events(size_t n);
 };
 
 // Process-wide engine pool (Session construction / destruction).
