@@ -77,9 +77,7 @@ int crac_chunk_crc32_range(const crac_span_t* d_spans, const uint64_t* d_chunk_f
  * into d_crc; every chunk whose CRC differs from d_crc_prev is written by the
  * hashing warp straight into host_image + d_dst_off[span] + chunk offset
  * (pinned, UVA-mapped) and its d_crc_prev entry updated.  d_counters[0] +=
- * dirty chunks, d_counters[1] += dirty bytes (caller zeroes them).
- * d_crc_prev == NULL copies every chunk (hash + copy in one HBM read; the
- * destination may be device memory); d_counters may be NULL. */
+ * dirty chunks, d_counters[1] += dirty bytes (caller zeroes them). */
 int crac_hash_drain_range(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
                           uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
                           uint32_t* d_crc, uint32_t* d_crc_prev, const uint64_t* d_dst_off,
@@ -111,6 +109,16 @@ int crac_gather_chunks_to_host_dev(const crac_span_t* d_spans, const uint64_t* d
 int crac_fold_sections(const crac_record_t* d_recs, uint32_t n_recs, const uint64_t* d_pay_first,
                        const uint32_t* d_pay_crc, uint32_t n_pay, const uint32_t* d_page_crc,
                        uint64_t len3, uint64_t total_pay_chunks, uint32_t* d_out, void* stream);
+
+/* Hash + copy (stall-reduced snapshot): hashes chunks [c_lo, c_hi) into
+ * d_crc and writes every chunk to d_dst + d_dst_off[span] + chunk offset
+ * from the registers it was hashed from (one HBM read; d_dst is device or
+ * UVA memory).  dst_aligned = 1 promises every d_dst + d_dst_off[span] is
+ * 16-byte aligned (faster kernel); 0 accepts any alignment. */
+int crac_hash_copy_range(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
+                         uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
+                         uint32_t* d_crc, const uint64_t* d_dst_off, uint8_t* d_dst,
+                         int dst_aligned, void* stream);
 
 /* The frame bytes (frame_len <= 24) of records [0, n_recs) at
  * d_stream + out_off, with byte stores only, so a concurrent

@@ -701,10 +701,12 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   const uint32_t k1_ctas = uint32_t(std::max(1, E.sm_count - DrainEngine::kPackSMs));
   check_cuda(cudaEventRecord(E.ev_h0, E.s_hash), "event");
   if (fused) {
-    check_cuda(cudaError_t(crac_hash_drain_range(
+    const bool aligned = std::all_of(P.pay_rec_off.begin(), P.pay_rec_off.end(),
+                                     [](uint64_t o) { return o % 16 == 0; });
+    check_cuda(cudaError_t(crac_hash_copy_range(
                    E.d_pay_spans.ptr, E.d_pay_first.ptr, uint32_t(P.pay_spans.size()),
-                   DrainEngine::kChunk, 0, P.pay_first.back(), E.d_pay_crc.ptr, nullptr,
-                   E.d_pay_soff.ptr, E.d_shadow, nullptr, E.s_hash)),
+                   DrainEngine::kChunk, 0, P.pay_first.back(), E.d_pay_crc.ptr,
+                   E.d_pay_soff.ptr, E.d_shadow, aligned ? 1 : 0, E.s_hash)),
                "K1 hash+copy");
     check_cuda(cudaError_t(crac_write_frames(E.d_recs.ptr, uint32_t(P.pay_spans.size()),
                                              E.d_shadow, E.s_shadow)),

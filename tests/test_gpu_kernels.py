@@ -222,3 +222,37 @@ def test_pack_scatter_round_trip_random_records(eng):
         got = bytes(t[:e].cpu().numpy())
         assert got[:s] == want[sum(16 + x[1] for x in regions[:k]) + 16:][:s]
         assert got[s:e] == bytes(e - s)  # padding zero-filled
+
+
+@pytest.mark.parametrize("aligned", [1, 0])
+def test_hash_copy_writes_every_chunk_and_hashes(eng, aligned):
+    """crac_hash_copy_range: the stall-reduced snapshot's K1 (copy from the
+    hashing registers) against zlib and the source bytes, tails and odd
+    destination offsets included."""
+    L = eng.lib()
+    chunk = 65536
+    sizes = [chunk * 3, chunk * 2 + 512 * 7 + 33, 511, 512, chunk + 16, 4096 * 5]
+    bufs = [_rand(n, 40 + k).cuda() for k, n in enumerate(sizes)]
+    spans = _spans(bufs)
+    first_d, first = _first(bufs, chunk)
+    offs, pos = [], 0
+    for n in sizes:
+        pos += 16 if aligned else 16 + 7
+        offs.append(pos)
+        pos += (n + 15) // 16 * 16 if aligned else n
+    d_off = torch.tensor(offs, dtype=torch.int64).cuda()
+    dst = torch.full((pos + 64,), 0xAB, dtype=torch.uint8).cuda()
+    crc = torch.zeros(first[-1], dtype=torch.int32).cuda()
+    assert L.crac_hash_copy_range(_p(spans), _p(first_d), len(bufs), chunk, 0, first[-1], _p(crc),
+                                  _p(d_off), _p(dst), aligned, None) == 0
+    torch.cuda.synchronize()
+    out = bytes(dst.cpu().numpy())
+    want_crc = []
+    prev_end = 0
+    for b, o in zip(bufs, offs):
+        h = bytes(b.cpu().numpy())
+        assert out[o:o + len(h)] == h
+        assert out[prev_end:o] == b"\xAB" * (o - prev_end)  # nothing outside the payloads
+        prev_end = o + len(h)
+        want_crc += [zlib.crc32(h[i:i + chunk]) for i in range(0, len(h), chunk)]
+    assert [x & 0xFFFFFFFF for x in crc.cpu().tolist()] == want_crc
