@@ -337,7 +337,30 @@ def isolated_kernel_rates(torch, engine) -> dict:
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / N
         res[name] = {"avg_launch_ms": round(ms, 4), "GBps": round(2 * W / (ms * 1e-3) / 1e9, 1)}
-    del src, out
+    # the in-situ ceiling: the driver's own D2D copy of a 64 MiB window while
+    # a D2H of 16 MiB pieces runs on another stream (what the drain does);
+    # PCIe copy traffic slows every HBM copy, see profiles/r01/copy_interference.txt
+    host = torch.empty(256 * MIB, dtype=torch.uint8).pin_memory()
+    stage = torch.empty(256 * MIB, dtype=torch.uint8, device="cuda")
+    sc, sk = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(sc):
+        for i in range(120):
+            j = (i % 16) * 16 * MIB
+            host[j:j + 16 * MIB].copy_(stage[j:j + 16 * MIB], non_blocking=True)
+    times = []
+    with torch.cuda.stream(sk):
+        for w in range(1, N + 1):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(sk)
+            out[:W].copy_(src[W * w:W * (w + 1)], non_blocking=True)
+            e1.record(sk)
+            times.append((e0, e1))
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b in times)
+    res["d2d_copy_beside_d2h"] = {"avg_launch_ms": round(ms, 4),
+                                  "GBps": round(2 * W / (ms * 1e-3) / 1e9, 1)}
+    del src, out, host, stage
     return res
 
 
@@ -637,8 +660,9 @@ def main() -> None:
                          "isolated": {k: {**v, "frac": round(v["GBps"] / hbm, 4)}
                                       for k, v in isolated.items()},
                          "note": "in-situ launch times (timed region, median window) run "
-                                 "beside PCIe copy traffic, which slows this kernel ~2x "
-                                 "(profiles/r01/pack_insitu.txt); 'isolated' = the same kernel "
+                                 "beside PCIe copy traffic, which slows every HBM copy ~2x, "
+                                 "cudaMemcpy D2D included (isolated.d2d_copy_beside_d2h; "
+                                 "profiles/r01/copy_interference.txt); 'isolated' = the kernel "
                                  "back to back on one stream; traffic = ncu DRAM bytes per "
                                  "launch (writes still in L2 at kernel end are not counted)"},
             "pcie_roofline": {"d2h_GBps": round(d2h, 2), "h2d_GBps": round(h2d, 2),
