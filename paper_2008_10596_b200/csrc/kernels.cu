@@ -415,6 +415,158 @@ __global__ void __launch_bounds__(kK1Threads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K1-TMA: the same hash with rows staged through shared memory by the bulk
+// copy engine (cp.async.bulk + mbarrier) instead of register loads.  Kept as
+// the measured alternative the north star names (CRAC_K1_TMA=A|B|C selects
+// it for crac_chunk_crc32_range); DESIGN.md "K1 design" has the numbers.
+// The 128 KiB of lookup tables leave <= 99 KiB for staging, and every staged
+// word costs one extra LDS.128 on the shared-memory pipe the lookups already
+// keep busy.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+template <int kWarps, int kStages, int kStageRows>
+constexpr uint32_t k1_tma_smem() {
+  return kTabBytes + kWarps * kStages * kStageRows * 512 + kWarps * kStages * 8;
+}
+
+template <int kWarps, int kStages, int kStageRows>
+__global__ void __launch_bounds__(kWarps * 32, 1)
+    k1_chunk_crc_tma(const crac_span_t* __restrict__ spans, const uint64_t* __restrict__ chunk_first,
+                     uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
+                     uint32_t* __restrict__ out, uint32_t k_full) {
+  extern __shared__ __align__(128) uint32_t s_tab[];
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(g_tab);
+    uint4* dst = reinterpret_cast<uint4*>(s_tab);
+    for (uint32_t i = threadIdx.x; i < kTabWords / 4; i += kWarps * 32) dst[i] = src[i];
+  }
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t smem0 = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab));
+  constexpr uint32_t kStageBytes = kStageRows * 512;
+  const uint32_t stage0 = smem0 + kTabBytes + warp * kStages * kStageBytes;
+  const uint32_t bar0 = smem0 + kTabBytes + kWarps * kStages * kStageBytes + warp * kStages * 8;
+  if (lane == 0) {
+    for (int k = 0; k < kStages; ++k) mbar_init(bar0 + 8 * k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const LaneLut lut = make_lut(smem0, lane);
+  const uint64_t gw = blockIdx.x * uint64_t(kWarps) + warp;
+  const uint64_t tw = gridDim.x * uint64_t(kWarps);
+  const uint64_t total_chunks = c_hi - c_lo;
+  const uint64_t c_begin = c_lo + total_chunks * gw / tw, c_end = c_lo + total_chunks * (gw + 1) / tw;
+  if (c_begin >= c_end) return;
+
+  // producer cursor (lane 0 issues; all lanes track it): chunk pc, stage pst
+  uint64_t pc = c_begin;
+  uint32_t ps = find_span(chunk_first, n_spans, pc);
+  uint32_t pst = 0, issued = 0;
+  auto chunk_rows = [&](uint64_t c, uint32_t s) -> uint32_t {
+    const uint64_t off = (c - __ldg(chunk_first + s)) * chunk_bytes;
+    const uint64_t rem = spans[s].len - off;
+    return uint32_t((rem < chunk_bytes ? rem : chunk_bytes) >> 9);
+  };
+  auto issue = [&]() {  // next stage of the producer cursor, if any
+    while (pc < c_end) {
+      while (pc >= __ldg(chunk_first + ps + 1)) ++ps;
+      const uint32_t rows = chunk_rows(pc, ps);
+      if (pst * kStageRows < rows) {
+        const uint32_t nr = min(uint32_t(kStageRows), rows - pst * kStageRows);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(spans[ps].ptr) +
+                             (pc - __ldg(chunk_first + ps)) * chunk_bytes + pst * kStageBytes;
+        const uint32_t slot = issued % kStages;
+        if (lane == 0) {
+          mbar_expect_tx(bar0 + 8 * slot, nr * 512);
+          bulk_g2s(stage0 + slot * kStageBytes, src, nr * 512, bar0 + 8 * slot);
+        }
+        ++issued;
+        ++pst;
+        return;
+      }
+      ++pc;
+      pst = 0;
+    }
+  };
+  for (int k = 0; k < kStages; ++k) issue();
+
+  uint32_t consumed = 0;
+  uint32_t s = find_span(chunk_first, n_spans, c_begin);
+  for (uint64_t c = c_begin; c < c_end; ++c) {
+    while (c >= __ldg(chunk_first + s + 1)) ++s;
+    const crac_span_t sp = spans[s];
+    const uint64_t off = (c - __ldg(chunk_first + s)) * chunk_bytes;
+    const uint64_t rem_len = sp.len - off;
+    const uint32_t len = rem_len < chunk_bytes ? uint32_t(rem_len) : chunk_bytes;
+    const uint8_t* base = reinterpret_cast<const uint8_t*>(sp.ptr + off);
+    const uint32_t rows = len >> 9;
+    uint32_t acc = 0;
+    for (uint32_t r0 = 0; r0 < rows; r0 += kStageRows) {
+      const uint32_t slot = consumed % kStages, parity = (consumed / kStages) & 1;
+      mbar_wait(bar0 + 8 * slot, parity);
+      const uint32_t nr = min(uint32_t(kStageRows), rows - r0);
+      const uint32_t buf = stage0 + slot * kStageBytes + lane * 16;
+#pragma unroll
+      for (uint32_t k = 0; k < uint32_t(kStageRows); ++k) {
+        if (k < nr) {
+          const uint4 w = lds128(buf + k * 512);
+          acc = (r0 + k + 1 == rows) ? word16<false>(lut, acc, w) : word16<true>(lut, acc, w);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      ++consumed;
+      issue();
+    }
+    uint32_t L = rows ? warp_xor(crac::gf_mul(g_xp16[31 - lane], acc)) : 0u;
+    const uint32_t t = len & 511;
+    if (t) {
+      const uint32_t nt = t >> 4;
+      uint32_t part = 0;
+      if (lane < nt) {
+        const uint4 w = *reinterpret_cast<const uint4*>(base + rows * 512 + lane * 16);
+        part = crac::gf_mul(g_xp16[nt - 1 - lane], word16<false>(lut, 0u, w));
+      }
+      uint32_t lt = warp_xor(part);
+      if (lane == 0) {
+        const uint8_t* tb = base + rows * 512 + nt * 16;
+        for (uint32_t i = 0; i < (t & 15); ++i) lt = (lt >> 8) ^ g_t0[(lt ^ tb[i]) & 0xFFu];
+        L = crac::gf_mul(g_xpt[t], L) ^ lt;
+      }
+    }
+    if (lane == 0) out[c] = L ^ (len == chunk_bytes ? k_full : crac::crc_affine(len, g_pow2));
+  }
+}
+
 __device__ __forceinline__ void set_byte(uint4& v, uint32_t i, uint32_t b) {
   const uint32_t sh = (i & 3) * 8, keep = ~(0xFFu << sh), put = b << sh;
   switch (i >> 2) {  // register-resident (no local-memory indexing)
@@ -921,6 +1073,12 @@ int crac_gpu_init(void) {
     for (auto k : {k1_chunk_crc<4, 0>, k1_chunk_crc<8, 0>, k1_chunk_crc<16, 0>,
                    k1_chunk_crc<16, 1>, k1_chunk_crc<16, 2>, k1_chunk_crc<8, 3>})
       if (!e) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTabBytes));
+    if (!e) e = cudaFuncSetAttribute(k1_chunk_crc_tma<16, 3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(k1_tma_smem<16, 3, 4>()));
+    if (!e) e = cudaFuncSetAttribute(k1_chunk_crc_tma<8, 6, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(k1_tma_smem<8, 6, 4>()));
+    if (!e) e = cudaFuncSetAttribute(k1_chunk_crc_tma<8, 3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(k1_tma_smem<8, 3, 8>()));
     g_init_rc = int(e);
   });
   return g_init_rc;
@@ -949,6 +1107,26 @@ int crac_chunk_crc32_range(const crac_span_t* d_spans, const uint64_t* d_chunk_f
     const char* e = std::getenv("CRAC_K1_ROWS");
     return e ? std::atoi(e) : 0;
   }();
+  static const char tma = [] {
+    const char* e = std::getenv("CRAC_K1_TMA");
+    return e ? e[0] : '\0';
+  }();
+  if (tma) {  // measured alternative (see k1_chunk_crc_tma)
+    const uint64_t w = tma == 'A' ? 16 : 8;
+    const uint64_t b = std::min<uint64_t>((warps_needed + w - 1) / w, cap);
+    const cudaStream_t st = cudaStream_t(stream);
+    const uint32_t kf = k_full_for(chunk_bytes);
+    if (tma == 'A')
+      k1_chunk_crc_tma<16, 3, 4><<<unsigned(b), 512, k1_tma_smem<16, 3, 4>(), st>>>(
+          d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, kf);
+    else if (tma == 'B')
+      k1_chunk_crc_tma<8, 6, 4><<<unsigned(b), 256, k1_tma_smem<8, 6, 4>(), st>>>(
+          d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, kf);
+    else
+      k1_chunk_crc_tma<8, 3, 8><<<unsigned(b), 256, k1_tma_smem<8, 3, 8>(), st>>>(
+          d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, kf);
+    return int(cudaGetLastError());
+  }
   const int rows = forced ? forced : (chunk_bytes >= 32 * 512 ? 16 : chunk_bytes >= 8 * 512 ? 8 : 4);
   auto kern = rows == 4 ? k1_chunk_crc<4, 0>
               : rows == 16 ? k1_chunk_crc<16, 0> : k1_chunk_crc<8, 0>;
