@@ -669,12 +669,17 @@ def main() -> None:
                               "d2h_peak_GBps": pd, "h2d_peak_GBps": ph,
                               "peak_source": "measured in this run (16 MiB pinned copies)",
                               "binding_GBps": round(link, 2),
+                              "d2h_GBps_per_step": [round(d["d2h_bytes"] / (d["copy_ms"] * 1e6), 2)
+                                                    for d in drains if d["copy_ms"]],
+                              "h2d_GBps_per_step": [round(r["h2d_bytes"] / (r["copy_ms"] * 1e6), 2)
+                                                    for r in refills if r["copy_ms"]],
                               "value_frac": round(value / world / link, 4)},
             "e2e": {"value": round(e2e, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": refills[-1]["h2d_bytes"],
                     "d2h_bytes_per_step": drains[-1]["d2h_bytes"],
                     "wall_s": round(wall, 3)},
             "gpu_launches": launches,
+            "image_pages": image.pages(),
             "clocks": clk,
             "incremental": incremental,
             "stall_reduced": stall,

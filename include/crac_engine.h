@@ -76,6 +76,8 @@ int crac_set_app_state(crac_session_t* s, const void* src, uint64_t n);
 int crac_image_create(crac_image_t** out);
 void crac_image_destroy(crac_image_t* img);
 int crac_image_view(crac_image_t* img, const uint8_t** data, uint64_t* size);
+/* Capacity of the page-locked buffer and how much of it is 2 MiB-page backed. */
+int crac_image_pages(crac_image_t* img, uint64_t* capacity, uint64_t* huge_bytes);
 int crac_checkpoint(crac_session_t* s, crac_image_t* img, crac_stats_t* stats);
 int crac_checkpoint_incremental(crac_session_t* s, crac_image_t* img, crac_stats_t* stats);
 /* Stall-reduced drain (new): the app is quiesced only while the

@@ -82,6 +82,10 @@ class PinnedImage {
   // Ensures capacity for `size` bytes with (data() + align_at) % 4096 == 0.
   void prepare(uint64_t size, uint64_t align_at);
   void set_size(uint64_t n) { size_ = n; }
+  uint64_t capacity() const { return cap_; }
+  // Bytes of the buffer backed by 2 MiB pages (D2H into 4 KiB-backed memory
+  // is slower on the B200 box); from /proc/self/smaps.
+  uint64_t huge_page_bytes() const;
 
  private:
   uint8_t* base_ = nullptr;

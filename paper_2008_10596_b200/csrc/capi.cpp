@@ -200,6 +200,13 @@ int crac_image_view(crac_image_t* img, const uint8_t** data, uint64_t* size) {
   });
 }
 
+int crac_image_pages(crac_image_t* img, uint64_t* capacity, uint64_t* huge_bytes) {
+  return guard([&] {
+    *capacity = img->img.capacity();
+    *huge_bytes = img->img.huge_page_bytes();
+  });
+}
+
 int crac_checkpoint(crac_session_t* s, crac_image_t* img, crac_stats_t* stats) {
   return guard([&] {
     DrainStats d;

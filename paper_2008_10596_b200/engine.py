@@ -75,6 +75,7 @@ _SIGS = {
     "crac_image_create": (C.c_int, [C.POINTER(_P)]),
     "crac_image_destroy": (None, [_P]),
     "crac_image_view": (C.c_int, [_P, C.POINTER(_P), _PU64]),
+    "crac_image_pages": (C.c_int, [_P, _PU64, _PU64]),
     "crac_checkpoint": (C.c_int, [_P, _P, C.POINTER(Stats)]),
     "crac_checkpoint_incremental": (C.c_int, [_P, _P, C.POINTER(Stats)]),
     "crac_checkpoint_value": (C.c_int, [_P, C.POINTER(_P), _PU64]),
@@ -176,6 +177,12 @@ class Image:
 
     def tobytes(self) -> bytes:
         return bytes(self.view())
+
+    def pages(self) -> dict:
+        """Capacity of the page-locked buffer and its 2 MiB-page backed bytes."""
+        cap, huge = C.c_uint64(), C.c_uint64()
+        _check(lib().crac_image_pages(self._h, C.byref(cap), C.byref(huge)))
+        return {"capacity": cap.value, "huge_page_bytes": huge.value}
 
     def close(self):
         if getattr(self, "_h", None):
