@@ -50,7 +50,11 @@ def parse_args():
     ap.add_argument("--no-incremental", action="store_true")
     ap.add_argument("--no-stall", action="store_true",
                     help="skip the stall-reduced (checkpoint_begin/finish) measurement")
-    ap.add_argument("--workload", choices=["c4", "c2", "c3", "c5"], default="c4")
+    ap.add_argument("--workload", choices=["c4", "c2", "c3", "c5", "file"], default="c4")
+    ap.add_argument("--file-footprint-gib", type=float, default=16.0,
+                    help="state for --workload file (bounded by the disk: 2 images on it)")
+    ap.add_argument("--io-dir", default=None,
+                    help="directory of the image file (default: $CRAC_IO_DIR or /tmp)")
     ap.add_argument("--c2-calls", type=int, default=40000)
     ap.add_argument("--c3-footprint-gib", type=float, default=16.0)
     ap.add_argument("--c5-footprint-gib", type=float, default=64.0)
@@ -371,8 +375,9 @@ def build_workload(args, engine, rank: int, live_cap: int):
     import workloads
     region = args.region_mib * MIB
     seed = rank + 1
-    if args.workload in ("c4", "c5"):
-        want = args.footprint_gib if args.workload == "c4" else args.c5_footprint_gib
+    if args.workload in ("c4", "c5", "file"):
+        want = {"c4": args.footprint_gib, "c5": args.c5_footprint_gib,
+                "file": args.file_footprint_gib}[args.workload]
         footprint = min(int(want * GIB), live_cap) // region * region
         n = footprint // region
         sess = engine.Session(seed=seed, arena_bytes=footprint + 64 * MIB)
@@ -411,6 +416,8 @@ WORKLOAD_NAMES = {
     "c3": "C3: HPGMG-style cudaMallocManaged footprint with mixed residence, checkpoint + "
           "residency-restoring restart",
     "c5": "C5: incremental checkpoint sequence at 1/5/25 % dirty chunks, hash-only vs drain",
+    "file": "C4 shape through the file: checkpoint_to_file (drain + parallel O_DIRECT write + "
+            "fdatasync) then restart_from_file (parallel read + refill)",
 }
 
 
@@ -507,6 +514,135 @@ def run_c5(args, engine, sess, image, live, group, rank, world, peaks) -> None:
             "incremental": rows, "stall_reduced": stall}), flush=True)
 
 
+def dd_ceiling(path: Path, nbytes: int, streams: int = 8) -> dict:
+    """Storage ceiling measured with coreutils dd, independent of our writer:
+    `streams` concurrent O_DIRECT dd processes over disjoint 64 MiB-block
+    ranges of one file (write with fdatasync, then read)."""
+    bs = 64 * MIB
+    blocks = max(streams, nbytes // bs)
+    per = (blocks + streams - 1) // streams
+    out = {}
+    for mode in ("write", "read"):
+        cmds = []
+        for k in range(streams):
+            lo, cnt = k * per, max(0, min(per, blocks - k * per))
+            if not cnt:
+                continue
+            if mode == "write":
+                cmds.append(["dd", "if=/dev/zero", f"of={path}", f"bs={bs}", f"seek={lo}",
+                             f"count={cnt}", "oflag=direct", "conv=notrunc,fdatasync"])
+            else:
+                cmds.append(["dd", f"if={path}", "of=/dev/null", f"bs={bs}", f"skip={lo}",
+                             f"count={cnt}", "iflag=direct"])
+        t0 = time.perf_counter()
+        ps = [subprocess.Popen(c, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+              for c in cmds]
+        ok = all(p.wait() == 0 for p in ps)
+        dt = time.perf_counter() - t0
+        out[f"{mode}_GBps"] = round(blocks * bs / dt / 1e9, 3) if ok else None
+    try:
+        path.unlink()
+    except OSError:
+        pass
+    out["how"] = f"{streams} concurrent dd O_DIRECT streams, 64 MiB blocks, {blocks * bs // MIB} MiB"
+    return out
+
+
+def drop_cache(path: Path) -> None:
+    try:
+        fd = os.open(path, os.O_RDONLY)
+        try:
+            os.posix_fadvise(fd, 0, 0, os.POSIX_FADV_DONTNEED)
+        finally:
+            os.close(fd)
+    except OSError:
+        pass
+
+
+def run_file(args, engine, sess, live, group, rank, world, cfg_extra) -> None:
+    """Persistence: checkpoint_to_file then restart_from_file of
+    the C4-shaped state; wall time per phase, storage ceiling beside it."""
+    io_dir = Path(args.io_dir or os.environ.get("CRAC_IO_DIR", "/tmp"))
+    io_dir.mkdir(parents=True, exist_ok=True)
+    path = io_dir / f"crac_bench_rank{rank}.img"
+    img, staging = engine.Image(), engine.Image()
+    rows = []
+    for k in range(args.warmup + args.steps):
+        group.barrier()
+        t0 = time.perf_counter()
+        drain, wio = sess.checkpoint_to_file(path, img)
+        t1 = time.perf_counter()
+        sess.close()
+        drop_cache(path)  # a restart reads the device, not the page cache
+        t2 = time.perf_counter()
+        sess, refill, rio = engine.restart_from_file(path, staging)
+        t3 = time.perf_counter()
+        rows.append({"ckpt_s": t1 - t0, "restart_s": t3 - t2, "drain_ms": drain["total_ms"],
+                     "write_ms": wio["ms"], "read_ms": rio["ms"], "refill_ms": refill["total_ms"],
+                     "direct": wio["direct"] and rio["direct"], "bytes": wio["bytes"]})
+    rows = rows[args.warmup:]
+    ck = group.max(statistics.mean(r["ckpt_s"] for r in rows))
+    rs = group.max(statistics.mean(r["restart_s"] for r in rows))
+    nbytes = rows[-1]["bytes"]
+    sess.close()
+    img.close()
+    staging.close()
+    ceiling = dd_ceiling(path, min(nbytes, 16 * GIB)) if rank == 0 else None
+    try:
+        path.unlink()
+    except OSError:
+        pass
+    if rank != 0:
+        return
+    m = {k: round(statistics.mean(r[k] for r in rows), 3)
+         for k in ("drain_ms", "write_ms", "read_ms", "refill_ms")}
+    roof = None
+    if ceiling and ceiling.get("write_GBps") and ceiling.get("read_GBps"):
+        t_roof = nbytes / (ceiling["write_GBps"] * 1e9) + nbytes / (ceiling["read_GBps"] * 1e9)
+        roof = {"bound": "storage", "write_GBps": round(nbytes / (m["write_ms"] * 1e6), 3),
+                "read_GBps": round(nbytes / (m["read_ms"] * 1e6), 3),
+                "ceiling": ceiling, "frac": round(t_roof / (ck + rs), 4)}
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = cpu_baseline_file(args.cpu_sample_gib, args.region_mib * MIB, io_dir)
+    print(json.dumps({
+        "metric": "checkpoint & restart GB/s per GPU and whole box at 1/2/4/8 B200; % of roofline",
+        "value": round(2 * live * world / (ck + rs) / 1e9, 3), "unit": "GB/s (through the file)",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round((ck + rs) * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": WORKLOAD_NAMES["file"], "live_bytes_per_gpu": live,
+                   "file_bytes": nbytes, "io_dir": str(io_dir), **cfg_extra},
+        "per_gpu": {"checkpoint_to_file_GBps": round(live / ck / 1e9, 3),
+                    "restart_from_file_GBps": round(live / rs / 1e9, 3),
+                    "checkpoint_to_file_s": round(ck, 3), "restart_from_file_s": round(rs, 3),
+                    "phases_ms": m, "o_direct": all(r["direct"] for r in rows)},
+        "roofline": roof, "cpu_baseline": cpu}), flush=True)
+
+
+def cpu_baseline_file(sample_gib: float, region: int, io_dir: Path) -> dict:
+    """The reference's checkpoint_to_file / restart_from_file (ofstream /
+    ifstream), single-threaded, on a bounded sample."""
+    from oracle import ref
+    s, live = ref_make_session(int(sample_gib * GIB), region, seed=1)
+    path = io_dir / "crac_bench_ref.img"
+    t_ck = ref.ref_checkpoint_to_file(s, path)
+    s.close()
+    drop_cache(path)
+    r, t = ref.ref_restart_from_file(path)
+    r.close()
+    try:
+        path.unlink()
+    except OSError:
+        pass
+    return {"value": round(2 * live / (t_ck + t["total_s"]) / 1e9, 4), "unit": "GB/s",
+            "cores": 1, "kind": "reference",
+            "sample": f"{live // MIB} MiB ({live // region} x {region // MIB} MiB Device regions): "
+                      f"reference checkpoint_to_file then restart_from_file, single-threaded",
+            "phases_s": {"checkpoint_to_file_s": round(t_ck, 3),
+                         "restart_from_file_s": round(t["total_s"], 3)}}
+
+
 def main() -> None:
     args = parse_args()
     world, rank, local, local_world = dist_env()
@@ -534,6 +670,11 @@ def main() -> None:
     sess, live, cfg_extra = build_workload(args, engine, rank, min(host_cap, dev_cap))
     image = engine.Image()
     setup_s = time.perf_counter() - t_setup
+    if args.workload == "file":
+        image.close()
+        run_file(args, engine, sess, live, group, rank, world, cfg_extra)
+        group.close()
+        return
     if args.workload == "c5":
         run_c5(args, engine, sess, image, live, group, rank, world, peaks)
         sess.close()

@@ -93,6 +93,33 @@ int crac_checkpoint_finish(crac_session_t* s, crac_stats_t* stats);
  * released with crac_buffer_free (the reference-shaped value API). */
 int crac_checkpoint_value(crac_session_t* s, uint8_t** image, uint64_t* size);
 
+/* Image persistence — ref: src/ckpt_engine.cpp:63-65,173-177
+ * (checkpoint_to_file / restart_from_file) and src/image.cpp:432-451 (the
+ * whole-buffer ofstream / ifstream they use).  The drain lands in `img`; the
+ * file is written from it by parallel positional writes (O_DIRECT when the
+ * filesystem accepts it) and fdatasync'd; restart reads the file back into
+ * `img` the same way and refills from it.  Files are byte-identical to the
+ * reference's.  Write errors: InvalidArgument (1 + 0); unreadable file:
+ * ImageCorrupt (1 + 13). */
+typedef struct crac_io_stats {
+  double ms;          /* open .. fdatasync / close */
+  uint64_t bytes;     /* file bytes */
+  uint32_t threads;   /* I/O threads */
+  int32_t direct;     /* 1 if O_DIRECT */
+  uint64_t bounced;   /* bytes moved through an aligned bounce buffer */
+} crac_io_stats_t;
+int crac_checkpoint_to_file(crac_session_t* s, crac_image_t* img, const char* path, int compress,
+                            crac_stats_t* drain, crac_io_stats_t* io);
+int crac_restart_from_file(const char* path, crac_image_t* img, int mode, crac_session_t** out,
+                           crac_stats_t* refill, crac_io_stats_t* io);
+/* The parallel file transfer alone, on any host buffer (no GPU needed):
+ * threads / chunk_bytes 0 = defaults; flags bit 0 = O_DIRECT, bit 1 = fdatasync. */
+int crac_file_write(const char* path, const void* data, uint64_t n, uint32_t threads,
+                    uint64_t chunk_bytes, uint32_t flags, crac_io_stats_t* io);
+int crac_file_size(const char* path, uint64_t* n);
+int crac_file_read(const char* path, void* dst, uint64_t capacity, uint32_t threads,
+                   uint64_t chunk_bytes, uint32_t flags, uint64_t* n, crac_io_stats_t* io);
+
 /* Restart refill — ref: src/ckpt_engine.cpp:120-171 + src/image.cpp:280-345. */
 int crac_restart(const void* image, uint64_t size, int mode, crac_session_t** out,
                  crac_stats_t* stats);

@@ -24,6 +24,7 @@
 #include <memory>
 
 #include "cracsim/image.hpp"
+#include "cracsim/image_io.hpp"
 
 namespace cracsim {
 
@@ -83,6 +84,7 @@ class PinnedImage {
   void prepare(uint64_t size, uint64_t align_at);
   void set_size(uint64_t n) { size_ = n; }
   uint64_t capacity() const { return cap_; }
+  uint64_t room() const { return cap_ - off_; }  // bytes writable from data()
   // Bytes of the buffer backed by 2 MiB pages (D2H into 4 KiB-backed memory
   // is slower on the B200 box); from /proc/self/smaps.
   uint64_t huge_page_bytes() const;
@@ -128,6 +130,18 @@ Session restart_from_file(const std::filesystem::path& path, const KernelCatalog
                           TableMode mode = TableMode::Direct);
 
 // ---- B200 fast path ----
+// Persistence: the drain into a caller-owned pinned image, then
+// parallel O_DIRECT writes of it (image_io.hpp); restart reads the file into
+// the caller's pinned staging image in parallel and refills from it.  Same
+// files as the reference's checkpoint_to_file / restart_from_file.
+void checkpoint_to_file(Session& session, PinnedImage& image, const std::filesystem::path& path,
+                        bool compress, DrainStats* drain = nullptr, FileIoStats* io = nullptr);
+Session restart_from_file(const std::filesystem::path& path, PinnedImage& staging,
+                          const KernelCatalog& catalog, TableMode mode = TableMode::Direct,
+                          DrainStats* refill = nullptr, FileIoStats* io = nullptr);
+// Reads an image file into `staging` (4 KiB-aligned, page-locked).
+void read_image_into(const std::filesystem::path& path, PinnedImage& staging,
+                     FileIoStats* io = nullptr);
 void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats = nullptr);
 void checkpoint_incremental(Session& session, PinnedImage& image, DrainStats* stats = nullptr);
 // Stall-reduced drain.  checkpoint_begin quiesces, drains the

@@ -1,0 +1,58 @@
+// cracsim B200 build — image persistence.
+//
+// Replaces the reference's whole-buffer ofstream/ifstream file I/O
+// (ref: src/image.cpp:432-451 write_image_file / read_file_bytes) on the
+// checkpoint_to_file / restart_from_file path with parallel positional I/O:
+//   * the file is cut into `chunk` byte pieces written / read by a pool of
+//     host threads with pwrite / pread, each thread one contiguous run of
+//     pieces (CRAC_IO_LAYOUT=interleave hands them out round-robin instead);
+//   * the file's blocks are allocated with fallocate before the writes, so
+//     they all overwrite mapped blocks inside i_size and run concurrently;
+//   * O_DIRECT when the filesystem accepts it (no page-cache copy; the image
+//     is already in page-locked memory).  O_DIRECT needs 4 KiB-aligned memory,
+//     offsets and lengths: aligned pieces go straight from / to the image,
+//     the others through a per-thread aligned bounce buffer; the last piece
+//     is zero-padded to 4 KiB and the file truncated to its true length;
+//   * the write ends with fdatasync (a checkpoint is durable when the call
+//     returns; the reference only flushes the stream).
+// The bytes on disk are exactly the image bytes, so files interoperate with
+// the reference reader and writer.
+#pragma once
+
+#include <cstdint>
+#include <filesystem>
+#include <span>
+
+namespace cracsim {
+
+struct FileIoStats {
+  double ms = 0;          // wall time of the transfer (open .. fdatasync/close)
+  uint64_t bytes = 0;     // file bytes moved
+  uint32_t threads = 0;   // I/O threads used
+  bool direct = false;    // O_DIRECT was in effect
+  uint64_t bounced = 0;   // bytes that went through a bounce buffer
+};
+
+struct FileIoOptions {
+  uint32_t threads = 0;         // 0 = CRAC_IO_THREADS or min(16, hardware threads)
+  uint64_t chunk = 0;           // 0 = CRAC_IO_CHUNK_MIB or 64 MiB (multiple of 4 KiB)
+  bool direct = true;           // try O_DIRECT, fall back to buffered I/O if refused
+  bool sync = true;             // fdatasync before returning (writes)
+};
+
+// Writes `bytes` to `path` (created / truncated).  InvalidArgument on an I/O
+// error (the reference's "cannot write").
+void write_file_parallel(const std::filesystem::path& path, std::span<const uint8_t> bytes,
+                         FileIoStats* stats = nullptr, const FileIoOptions& opt = {});
+
+// Size of the file at `path`; ImageCorrupt if it cannot be opened (the
+// reference's "cannot read").
+uint64_t file_bytes(const std::filesystem::path& path);
+
+// Reads the whole file into dst[0, size).  `capacity` must be at least the
+// file size; with O_DIRECT, pieces land in place when dst is 4 KiB-aligned
+// and capacity >= size rounded up to 4 KiB.  Returns the file size.
+uint64_t read_file_parallel(const std::filesystem::path& path, uint8_t* dst, uint64_t capacity,
+                            FileIoStats* stats = nullptr, const FileIoOptions& opt = {});
+
+}  // namespace cracsim

@@ -57,6 +57,8 @@ _SIGS = {
     "ref_buffer_free": (None, [_P]),
     "ref_restart_image": (C.c_int, [_P, _U64, C.c_int, C.POINTER(_P), _PD, _PD]),
     "ref_decode_check": (C.c_int, [_P, _U64]),
+    "ref_checkpoint_to_file": (C.c_int, [_P, C.c_char_p, C.c_int, _PD]),
+    "ref_restart_from_file": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(_P), _PD]),
     "ref_summarize": (C.c_int, [_P, _U64, _PU64, _PU32, _PU64]),
     "ref_fixture_image": (C.c_int, [C.c_int, C.POINTER(_P), _PU64]),
     "ref_debug_dump": (C.c_int, [_P, C.POINTER(C.c_char_p)]),
@@ -301,6 +303,20 @@ def ref_restart(image, mode: int = 0):
     t1, t2 = C.c_double(), C.c_double()
     _check(ref_lib().ref_restart_image(p, n, mode, C.byref(h), C.byref(t1), C.byref(t2)))
     return RefSession(_handle=h), {"decode_s": t1.value, "restart_s": t2.value}
+
+
+def ref_checkpoint_to_file(session: "RefSession", path, compress: bool = False) -> float:
+    """The reference's checkpoint_to_file; returns its wall time in s."""
+    t = C.c_double()
+    _check(ref_lib().ref_checkpoint_to_file(session._h, str(path).encode(), int(compress),
+                                            C.byref(t)))
+    return t.value
+
+
+def ref_restart_from_file(path, mode: int = 0):
+    h, t = C.c_void_p(), C.c_double()
+    _check(ref_lib().ref_restart_from_file(str(path).encode(), mode, C.byref(h), C.byref(t)))
+    return RefSession(_handle=h), {"total_s": t.value}
 
 
 def ref_decode_check(image) -> None:

@@ -249,6 +249,26 @@ int ref_restart_image(const uint8_t* image, uint64_t size, int mode, void** out,
   });
 }
 
+// checkpoint_to_file / restart_from_file (ref: ckpt_engine.hpp:63-84), the
+// reference's own file path: whole-buffer ofstream / ifstream.
+int ref_checkpoint_to_file(void* h, const char* path, int compress, double* t_total) {
+  return guard([&] {
+    auto t0 = std::chrono::steady_clock::now();
+    checkpoint_to_file(static_cast<RefSession*>(h)->s, path, compress != 0);
+    if (t_total) *t_total = secs_since(t0);
+  });
+}
+
+int ref_restart_from_file(const char* path, int mode, void** out, double* t_total) {
+  return guard([&] {
+    auto t0 = std::chrono::steady_clock::now();
+    Session s = restart_from_file(path, standard_catalog(),
+                                  mode ? TableMode::Proxy : TableMode::Direct);
+    if (t_total) *t_total = secs_since(t0);
+    *out = new RefSession(std::move(s));
+  });
+}
+
 int ref_decode_check(const uint8_t* image, uint64_t size) {
   return guard([&] { (void)decode_image({image, size}); });
 }

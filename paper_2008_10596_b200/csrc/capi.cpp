@@ -63,6 +63,11 @@ void to_c(const DrainStats& d, crac_stats_t* o) {
   o->shadow_bytes = d.shadow_bytes;
 }
 
+void to_c(const FileIoStats& f, crac_io_stats_t* o) {
+  if (!o) return;
+  *o = crac_io_stats_t{f.ms, f.bytes, f.threads, f.direct ? 1 : 0, f.bounced};
+}
+
 template <typename T>
 T* heap_copy(const T* p, size_t n) {
   T* out = static_cast<T*>(std::malloc(n ? n * sizeof(T) : 1));
@@ -260,6 +265,55 @@ int crac_restart(const void* image, uint64_t size, int mode, crac_session_t** ou
                               std::chrono::milliseconds{30000}, stats ? &d : nullptr);
     to_c(d, stats);
     *out = new crac_session(std::move(r));
+  });
+}
+
+int crac_checkpoint_to_file(crac_session_t* s, crac_image_t* img, const char* path, int compress,
+                            crac_stats_t* drain, crac_io_stats_t* io) {
+  return guard([&] {
+    DrainStats d;
+    FileIoStats f;
+    checkpoint_to_file(s->s, img->img, path, compress != 0, drain ? &d : nullptr, &f);
+    to_c(d, drain);
+    to_c(f, io);
+  });
+}
+
+int crac_restart_from_file(const char* path, crac_image_t* img, int mode, crac_session_t** out,
+                           crac_stats_t* refill, crac_io_stats_t* io) {
+  return guard([&] {
+    DrainStats d;
+    FileIoStats f;
+    Session r = restart_from_file(path, img->img, standard_catalog(),
+                                  mode ? TableMode::Proxy : TableMode::Direct,
+                                  refill ? &d : nullptr, &f);
+    to_c(d, refill);
+    to_c(f, io);
+    *out = new crac_session(std::move(r));
+  });
+}
+
+int crac_file_write(const char* path, const void* data, uint64_t n, uint32_t threads,
+                    uint64_t chunk_bytes, uint32_t flags, crac_io_stats_t* io) {
+  return guard([&] {
+    FileIoStats f;
+    write_file_parallel(path, {static_cast<const uint8_t*>(data), n}, &f,
+                        FileIoOptions{threads, chunk_bytes, (flags & 1) != 0, (flags & 2) != 0});
+    to_c(f, io);
+  });
+}
+
+int crac_file_size(const char* path, uint64_t* n) {
+  return guard([&] { *n = file_bytes(path); });
+}
+
+int crac_file_read(const char* path, void* dst, uint64_t capacity, uint32_t threads,
+                   uint64_t chunk_bytes, uint32_t flags, uint64_t* n, crac_io_stats_t* io) {
+  return guard([&] {
+    FileIoStats f;
+    *n = read_file_parallel(path, static_cast<uint8_t*>(dst), capacity, &f,
+                            FileIoOptions{threads, chunk_bytes, (flags & 1) != 0, false});
+    to_c(f, io);
   });
 }
 

@@ -1,7 +1,5 @@
 // Session lifecycle, log replay, and the value-type (Snapshot) adapters over
 // the B200 drain/refill (drain.cu).
-#include <fstream>
-
 #include "drain_engine.hpp"
 #include "image_codec.hpp"
 
@@ -35,20 +33,27 @@ Snapshot checkpoint(Session& session) {
 }
 
 // ref: ckpt_engine.cpp:63-65 (the drain itself is the GPU path; the file is
-// written from the pinned image, compressed on request).
+// written from the pinned image by the parallel writer, compressed on request).
 void checkpoint_to_file(Session& session, const std::filesystem::path& path, bool compress) {
   PinnedImage img;
-  checkpoint_image(session, img);
-  std::vector<uint8_t> z;
-  std::span<const uint8_t> out = img.bytes();
+  checkpoint_to_file(session, img, path, compress);
+}
+
+void checkpoint_to_file(Session& session, PinnedImage& image, const std::filesystem::path& path,
+                        bool compress, DrainStats* drain, FileIoStats* io) {
+  checkpoint_image(session, image, drain);
   if (compress) {
-    z = compress_image(out);
-    out = z;
+    const std::vector<uint8_t> z = compress_image(image.bytes());
+    write_file_parallel(path, z, io);
+  } else {
+    write_file_parallel(path, image.bytes(), io);
   }
-  std::ofstream f(path, std::ios::binary | std::ios::trunc);
-  f.write(reinterpret_cast<const char*>(out.data()), static_cast<std::streamsize>(out.size()));
-  f.flush();
-  if (!f.good()) raise(Errc::InvalidArgument, "cannot write " + path.string());
+}
+
+void read_image_into(const std::filesystem::path& path, PinnedImage& staging, FileIoStats* io) {
+  const uint64_t n = file_bytes(path);
+  staging.prepare(n, 0);  // data() 4 KiB-aligned: O_DIRECT lands in place
+  staging.set_size(read_file_parallel(path, staging.mutable_data(), staging.room(), io));
 }
 
 // ref: ckpt_engine.cpp:67-118 — re-execute in seq order, verify every result.
@@ -110,8 +115,15 @@ Session restart(const Snapshot& snapshot, const KernelCatalog& catalog, TableMod
 
 Session restart_from_file(const std::filesystem::path& path, const KernelCatalog& catalog,
                           TableMode mode) {
-  const std::vector<uint8_t> bytes = read_file_bytes(path);
-  return restart_image(bytes, catalog, mode);
+  PinnedImage staging;
+  return restart_from_file(path, staging, catalog, mode);
+}
+
+Session restart_from_file(const std::filesystem::path& path, PinnedImage& staging,
+                          const KernelCatalog& catalog, TableMode mode, DrainStats* refill,
+                          FileIoStats* io) {
+  read_image_into(path, staging, io);
+  return restart_image(staging.bytes(), catalog, mode, std::chrono::milliseconds{30000}, refill);
 }
 
 }  // namespace cracsim

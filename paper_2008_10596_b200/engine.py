@@ -47,6 +47,17 @@ class Stats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
 
 
+class IoStats(C.Structure):
+    _fields_ = [("ms", C.c_double), ("bytes", C.c_uint64), ("threads", C.c_uint32),
+                ("direct", C.c_int32), ("bounced", C.c_uint64)]
+
+    def as_dict(self) -> dict:
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["direct"] = bool(d["direct"])
+        d["GBps"] = self.bytes / (self.ms * 1e6) if self.ms > 0 else 0.0
+        return d
+
+
 _LIB: Optional[C.CDLL] = None
 
 # name -> (restype, argtypes)
@@ -84,6 +95,14 @@ _SIGS = {
     "crac_checkpoint_finish": (C.c_int, [_P, C.POINTER(Stats)]),
     "crac_restart": (C.c_int, [_P, _U64, C.c_int, C.POINTER(_P), C.POINTER(Stats)]),
     "crac_decode_check": (C.c_int, [_P, _U64]),
+    "crac_checkpoint_to_file": (C.c_int, [_P, _P, C.c_char_p, C.c_int, C.POINTER(Stats),
+                                          C.POINTER(IoStats)]),
+    "crac_restart_from_file": (C.c_int, [C.c_char_p, _P, C.c_int, C.POINTER(_P),
+                                         C.POINTER(Stats), C.POINTER(IoStats)]),
+    "crac_file_write": (C.c_int, [C.c_char_p, _P, _U64, _U32, _U64, _U32, C.POINTER(IoStats)]),
+    "crac_file_size": (C.c_int, [C.c_char_p, _PU64]),
+    "crac_file_read": (C.c_int, [C.c_char_p, _P, _U64, _U32, _U64, _U32, _PU64,
+                                 C.POINTER(IoStats)]),
     "crac_summarize": (C.c_int, [_P, _U64, _PU64, _PU32, _PU64]),
     "crac_debug_dump": (C.c_int, [_P, C.POINTER(C.c_char_p)]),
     "crac_buffer_free": (None, [_P]),
@@ -296,6 +315,16 @@ class Session:
         _check(fn(self._h, image._h, C.byref(st)))
         return st.as_dict()
 
+    def checkpoint_to_file(self, path, image: Optional[Image] = None,
+                           compress: bool = False) -> tuple[dict, dict]:
+        """checkpoint_to_file: GPU drain into `image`, then the parallel
+        (O_DIRECT, fdatasync'd) file write.  Returns (drain stats, io stats)."""
+        img = image or Image()
+        st, io = Stats(), IoStats()
+        _check(lib().crac_checkpoint_to_file(self._h, img._h, str(path).encode(), int(compress),
+                                             C.byref(st), C.byref(io)))
+        return st.as_dict(), io.as_dict()
+
     def reserve_shadow(self, nbytes: int) -> None:
         """HBM the stall-reduced drain may stage the stream in (0 releases it)."""
         _check(lib().crac_reserve_shadow(self._h, nbytes))
@@ -407,6 +436,42 @@ def restart_from_address(addr: int, n: int, mode: int = DIRECT) -> tuple[Session
     h, st = C.c_void_p(), Stats()
     _check(lib().crac_restart(C.c_void_p(addr), n, mode, C.byref(h), C.byref(st)))
     return Session(_handle=h), st.as_dict()
+
+
+def restart_from_file(path, image: Optional[Image] = None,
+                      mode: int = DIRECT) -> tuple[Session, dict, dict]:
+    """restart_from_file: parallel read into the pinned `image`, then the GPU
+    refill.  Returns (session, refill stats, io stats)."""
+    img = image or Image()
+    h, st, io = C.c_void_p(), Stats(), IoStats()
+    _check(lib().crac_restart_from_file(str(path).encode(), img._h, mode, C.byref(h),
+                                        C.byref(st), C.byref(io)))
+    return Session(_handle=h), st.as_dict(), io.as_dict()
+
+
+def write_file(path, data, threads: int = 0, chunk_bytes: int = 0, direct: bool = True,
+               sync: bool = True) -> dict:
+    """The parallel image-file writer on any host buffer (no GPU involved)."""
+    p, n, keep = _buf(data)
+    io = IoStats()
+    _check(lib().crac_file_write(str(path).encode(), p, n, threads, chunk_bytes,
+                                 int(direct) | (int(sync) << 1), C.byref(io)))
+    return io.as_dict()
+
+
+def read_file(path, threads: int = 0, chunk_bytes: int = 0, direct: bool = True,
+              offset: int = 0) -> tuple[bytes, dict]:
+    """The parallel image-file reader into a host buffer that starts `offset`
+    bytes past a 4 KiB boundary (no GPU involved)."""
+    n = C.c_uint64()
+    _check(lib().crac_file_size(str(path).encode(), C.byref(n)))
+    cap = (n.value + 8191) // 4096 * 4096 + offset
+    raw = C.create_string_buffer(cap + 4096)
+    base = (C.addressof(raw) + 4095) // 4096 * 4096 + offset
+    got, io = C.c_uint64(), IoStats()
+    _check(lib().crac_file_read(str(path).encode(), C.c_void_p(base), cap - offset, threads,
+                                chunk_bytes, int(direct), C.byref(got), C.byref(io)))
+    return C.string_at(base, got.value), io.as_dict()
 
 
 def decode_check(image) -> None:
