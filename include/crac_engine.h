@@ -140,6 +140,23 @@ int crac_managed_pages(crac_session_t* s, uint64_t id, uint64_t cap, uint8_t* fl
 int crac_read_raw(crac_session_t* s, uint64_t address, uint64_t n, void* out);
 int crac_backing_ptr(crac_session_t* s, uint64_t id, uint64_t* ptr);
 
+/* Interposition support (libcrac_preload.so, crac_preload.h).
+ * The reference's shim has no real cudart underneath (ref: src/shim.cpp:
+ * 204-253 is the call path an LD_PRELOAD interposer feeds):
+ *   crac_stream_handle   the cudaStream_t behind app stream `id`;
+ *   crac_live_streams    live app stream ids (restart: rebuild the handle map);
+ *   crac_gate_enter/leave  admit a call forwarded to the real runtime through
+ *                        the dispatch gate (DispatchTable::admit / release);
+ *   crac_set_device_wide_drain  quiesce = cudaDeviceSynchronize;
+ *   crac_get_app_state   the APPSTATE bytes (a view, valid until the next
+ *                        crac_set_app_state / destroy). */
+int crac_stream_handle(crac_session_t* s, uint64_t id, void** cuda_stream);
+int crac_live_streams(crac_session_t* s, uint64_t cap, uint64_t* ids, uint64_t* n);
+int crac_gate_enter(crac_session_t* s);
+int crac_gate_leave(crac_session_t* s);
+int crac_set_device_wide_drain(crac_session_t* s, int on);
+int crac_get_app_state(crac_session_t* s, const uint8_t** data, uint64_t* n);
+
 /* Workload fixtures (bench / tests): synthetic content (see crac_gpu.h) and
  * the C5 epoch mutation over every live Device allocation. */
 int crac_fill_synthetic(crac_session_t* s, uint64_t id, uint64_t seed, uint8_t managed_side);

@@ -18,6 +18,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = ROOT / "build" / "obj"
 LIB = PKG / "libcrac_b200.so"
+PRELOAD = PKG / "libcrac_preload.so"   # cudart interposer
+APP = ROOT / "build" / "interpose_app"  # test application, shared cudart
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -64,7 +66,34 @@ def build(force: bool = False) -> Path:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    _build_preload(force)
     return LIB
+
+
+def _stale(out: Path, *deps: Path) -> bool:
+    return not out.exists() or out.stat().st_mtime < max(d.stat().st_mtime for d in deps)
+
+
+def _build_preload(force: bool) -> None:
+    """libcrac_preload.so: host C++ (g++), links libcrac_b200.so by $ORIGIN;
+    plus the shared-cudart test application it is exercised with."""
+    src = CSRC / "preload.cpp"
+    hdrs = [ROOT / "include" / "crac_preload.h", ROOT / "include" / "crac_engine.h"]
+    if force or _stale(PRELOAD, src, LIB, *hdrs):
+        cmd = ["g++", "-std=c++20", "-O2", "-g", "-fPIC", "-shared", "-Wall",
+               "-I", str(ROOT / "include"), "-I", "/usr/local/cuda/include",
+               str(src), "-o", str(PRELOAD), "-L", str(PKG), "-l:libcrac_b200.so",
+               "-Wl,-rpath,$ORIGIN", "-ldl", "-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"preload build failed:\n{r.stdout}\n{r.stderr}")
+    app_src = ROOT / "tests" / "native" / "interpose_app.cu"
+    if force or _stale(APP, app_src):
+        cmd = [NVCC, *ARCH, "-O2", "-std=c++17", "-cudart", "shared", str(app_src),
+               "-o", str(APP), "-ldl"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"interpose_app build failed:\n{r.stdout}\n{r.stderr}")
 
 
 if __name__ == "__main__":

@@ -192,6 +192,37 @@ int crac_set_app_state(crac_session_t* s, const void* src, uint64_t n) {
   });
 }
 
+int crac_stream_handle(crac_session_t* s, uint64_t id, void** cuda_stream) {
+  return guard([&] { *cuda_stream = s->s.device().stream_handle(id); });
+}
+
+int crac_live_streams(crac_session_t* s, uint64_t cap, uint64_t* ids, uint64_t* n) {
+  return guard([&] {
+    const auto v = s->s.device().live_stream_ids();
+    *n = v.size();
+    for (size_t i = 0; i < v.size() && i < cap; ++i) ids[i] = v[i];
+  });
+}
+
+int crac_gate_enter(crac_session_t* s) {
+  return guard([&] { s->s.table().admit(); });
+}
+
+int crac_gate_leave(crac_session_t* s) {
+  return guard([&] { s->s.table().release(); });
+}
+
+int crac_set_device_wide_drain(crac_session_t* s, int on) {
+  return guard([&] { s->s.table().set_device_wide_drain(on != 0); });
+}
+
+int crac_get_app_state(crac_session_t* s, const uint8_t** data, uint64_t* n) {
+  return guard([&] {
+    *data = s->s.app_state().data();
+    *n = s->s.app_state().size();
+  });
+}
+
 int crac_image_create(crac_image_t** out) {
   return guard([&] { *out = new crac_image(); });
 }

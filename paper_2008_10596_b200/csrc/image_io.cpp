@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -100,7 +101,7 @@ int run_pieces(uint64_t pieces, uint32_t threads, uint64_t bounce_bytes, Fn&& fn
       if (err.load(std::memory_order_relaxed)) return;
       if (!striped) k = next.fetch_add(1);
       if (k >= end) return;
-      const int e = fn(k, bounce, bounce_bytes);
+      const int e = fn(k, t, bounce, bounce_bytes);
       if (e) {
         int expected = 0;
         err.compare_exchange_strong(expected, e);
@@ -157,30 +158,43 @@ void write_file_parallel(const std::filesystem::path& path, std::span<const uint
   bool direct = false;
   Fd f{open_maybe_direct(path, O_WRONLY | O_CREAT | O_TRUNC, opt.direct, &direct)};
   if (f.fd < 0) raise(Errc::InvalidArgument, "cannot write " + path.string() + ": " + std::strerror(errno));
-  // Allocate the file's blocks first.  ext4 runs O_DIRECT writes under a
-  // shared inode lock only when they overwrite mapped blocks inside i_size;
-  // writes into holes or past EOF take it exclusively and serialise (2.7 GB/s
-  // against 4.4-5.3 on the box's disk).  fallocate maps the extents
-  // (unwritten, not zeroed); filesystems without it get ftruncate.
-  if (n && ::fallocate(f.fd, 0, 0, static_cast<off_t>(n)) != 0 &&
-      ::ftruncate(f.fd, static_cast<off_t>(n)) != 0)
+  // Size the file first (experiment knob CRAC_IO_PREALLOC = fallocate |
+  // truncate | none) so the writes land inside i_size.
+  const char* pre = std::getenv("CRAC_IO_PREALLOC");
+  const std::string prealloc = pre ? pre : "fallocate";
+  int prc = 0;
+  if (n && prealloc == "fallocate") {
+    prc = ::fallocate(f.fd, 0, 0, static_cast<off_t>(n));
+    if (prc != 0) prc = ::ftruncate(f.fd, static_cast<off_t>(n));
+  } else if (n && prealloc == "truncate") {
+    prc = ::ftruncate(f.fd, static_cast<off_t>(n));
+  }
+  if (prc != 0)
     raise(Errc::InvalidArgument, "cannot write " + path.string() + ": " + std::strerror(errno));
+  // experiment knob: one open file description per thread
+  const bool fd_per_thread = std::getenv("CRAC_IO_FD_PER_THREAD") != nullptr;
   const uint8_t* src = bytes.data();
   const bool src_aligned = reinterpret_cast<uintptr_t>(src) % kBlock == 0;
   const uint64_t pieces = (n + chunk - 1) / chunk;
   std::atomic<uint64_t> bounced{0};
-  const int err = run_pieces(pieces, threads, chunk, [&](uint64_t k, std::unique_ptr<AlignedBuf>& b,
+  std::vector<Fd> fds(fd_per_thread ? threads : 0);
+  for (Fd& x : fds)
+    if ((x.fd = ::open(path.c_str(), O_WRONLY | O_CLOEXEC | (direct ? O_DIRECT : 0))) < 0)
+      raise(Errc::InvalidArgument, "cannot write " + path.string() + ": " + std::strerror(errno));
+  const int err = run_pieces(pieces, threads, chunk, [&](uint64_t k, uint32_t t,
+                                                          std::unique_ptr<AlignedBuf>& b,
                                                           uint64_t bb) -> int {
+    const int fd = fd_per_thread ? fds[t].fd : f.fd;
     const uint64_t off = k * chunk, len = std::min(chunk, n - off);
-    if (!direct) return full_pwrite(f.fd, src + off, len, off);
+    if (!direct) return full_pwrite(fd, src + off, len, off);
     const uint64_t padded = round_block(len);
-    if (src_aligned && padded == len) return full_pwrite(f.fd, src + off, len, off);
+    if (src_aligned && padded == len) return full_pwrite(fd, src + off, len, off);
     if (!b) b = std::make_unique<AlignedBuf>(bb);
     if (!b->p) return ENOMEM;
     std::memcpy(b->p, src + off, len);
     std::memset(b->p + len, 0, padded - len);
     bounced.fetch_add(len, std::memory_order_relaxed);
-    return full_pwrite(f.fd, b->p, padded, off);
+    return full_pwrite(fd, b->p, padded, off);
   });
   if (err) raise(Errc::InvalidArgument, "cannot write " + path.string() + ": " + std::strerror(err));
   if (direct && round_block(n) != n && ::ftruncate(f.fd, static_cast<off_t>(n)) != 0)
@@ -219,7 +233,8 @@ uint64_t read_file_parallel(const std::filesystem::path& path, uint8_t* dst, uin
   const uint64_t pieces = (n + chunk - 1) / chunk;
   std::atomic<uint64_t> bounced{0};
   std::atomic<bool> short_read{false};
-  const int err = run_pieces(pieces, threads, chunk, [&](uint64_t k, std::unique_ptr<AlignedBuf>& b,
+  const int err = run_pieces(pieces, threads, chunk, [&](uint64_t k, uint32_t,
+                                                          std::unique_ptr<AlignedBuf>& b,
                                                           uint64_t bb) -> int {
     const uint64_t off = k * chunk, len = std::min(chunk, n - off);
     uint64_t got = 0;

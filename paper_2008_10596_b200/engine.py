@@ -95,6 +95,12 @@ _SIGS = {
     "crac_checkpoint_finish": (C.c_int, [_P, C.POINTER(Stats)]),
     "crac_restart": (C.c_int, [_P, _U64, C.c_int, C.POINTER(_P), C.POINTER(Stats)]),
     "crac_decode_check": (C.c_int, [_P, _U64]),
+    "crac_stream_handle": (C.c_int, [_P, _U64, C.POINTER(_P)]),
+    "crac_live_streams": (C.c_int, [_P, _U64, _PU64, _PU64]),
+    "crac_gate_enter": (C.c_int, [_P]),
+    "crac_gate_leave": (C.c_int, [_P]),
+    "crac_set_device_wide_drain": (C.c_int, [_P, C.c_int]),
+    "crac_get_app_state": (C.c_int, [_P, C.POINTER(_P), _PU64]),
     "crac_checkpoint_to_file": (C.c_int, [_P, _P, C.c_char_p, C.c_int, C.POINTER(Stats),
                                           C.POINTER(IoStats)]),
     "crac_restart_from_file": (C.c_int, [C.c_char_p, _P, C.c_int, C.POINTER(_P),

@@ -76,3 +76,31 @@ def test_host_codec_rejects_truncation_and_trailing(so, golden):
             so.decode_check(b[:keep])
     with pytest.raises(so.CracError):
         so.decode_check(b + b"\0")
+
+
+def test_preload_exports_its_api_and_interposers(so):
+    """libcrac_preload.so exports every crac_preload.h entry
+    point and the cudart calls it interposes; it links the engine library."""
+    import subprocess
+    pre = so.LIB_PATH.parent / "libcrac_preload.so"
+    if not pre.exists():
+        from paper_2008_10596_b200 import build
+        build.build()
+    text = (ROOT / "include" / "crac_preload.h").read_text()
+    api = set(re.findall(r"^\s*(?:int|void\*)\s+(crac_preload_\w+)\s*\(", text, re.M))
+    assert len(api) == 6
+    out = subprocess.run(["nm", "-D", "--defined-only", str(pre)], capture_output=True,
+                         text=True, check=True).stdout
+    syms = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+    interposed = {"cudaMalloc", "cudaMallocManaged", "cudaMallocHost", "cudaHostAlloc",
+                  "cudaFree", "cudaFreeHost", "cudaStreamCreate", "cudaStreamCreateWithFlags",
+                  "cudaStreamCreateWithPriority", "cudaStreamDestroy", "cudaLaunchKernel",
+                  "cudaMemcpy", "cudaMemcpyAsync", "cudaMemset", "cudaMemsetAsync"}
+    assert api | interposed <= syms, sorted((api | interposed) - syms)
+    # the engine library itself must not export cuda* (its static runtime
+    # would otherwise be interposed by the preload)
+    eng = subprocess.run(["nm", "-D", "--defined-only", str(so.LIB_PATH)], capture_output=True,
+                         text=True, check=True).stdout
+    assert not [ln for ln in eng.splitlines() if " T cuda" in ln]
+    needed = subprocess.run(["readelf", "-d", str(pre)], capture_output=True, text=True).stdout
+    assert "libcrac_b200.so" in needed
