@@ -6,8 +6,9 @@
 //   * the file is cut into `chunk` byte pieces written / read by a pool of
 //     host threads with pwrite / pread, each thread one contiguous run of
 //     pieces (CRAC_IO_LAYOUT=interleave hands them out round-robin instead);
-//   * the file's blocks are allocated with fallocate before the writes, so
-//     they all overwrite mapped blocks inside i_size and run concurrently;
+//   * an existing file is overwritten in place (no O_TRUNC) and cut to the
+//     image size at the end: overwriting mapped blocks is ext4's concurrent
+//     O_DIRECT path, and freeing them first queues discards under the writes;
 //   * O_DIRECT when the filesystem accepts it (no page-cache copy; the image
 //     is already in page-locked memory).  O_DIRECT needs 4 KiB-aligned memory,
 //     offsets and lengths: aligned pieces go straight from / to the image,
@@ -40,7 +41,7 @@ struct FileIoOptions {
   bool sync = true;             // fdatasync before returning (writes)
 };
 
-// Writes `bytes` to `path` (created / truncated).  InvalidArgument on an I/O
+// Writes `bytes` to `path` (created, or overwritten and cut to size).  InvalidArgument on an I/O
 // error (the reference's "cannot write").
 void write_file_parallel(const std::filesystem::path& path, std::span<const uint8_t> bytes,
                          FileIoStats* stats = nullptr, const FileIoOptions& opt = {});

@@ -172,6 +172,14 @@ void DrainEngine::ensure_verify_events(size_t n) {
   }
 }
 
+void DrainEngine::ensure_land_events(size_t n) {
+  while (ev_land.size() < n) {
+    cudaEvent_t a;
+    check_cuda(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "event");
+    ev_land.push_back(a);
+  }
+}
+
 void DrainEngine::ensure_window_events(size_t n) {
   while (ev_w0.size() < n) {
     cudaEvent_t a, b;
@@ -436,35 +444,49 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
     pos += 20;
   }
   tr.mark("payloads");
-  // managed allocations: lay out offsets first, then fill the page records of
-  // every allocation in parallel (C3 has millions of pages)
+  // managed allocations: lay out offsets and page-CRC indices first, then
+  // fill the page records of every allocation in parallel (C3 has millions of
+  // pages).  Device-resident pages are hashed by K1 as runs (page_spans);
+  // host-resident ones (flag bit0 clear) are moved and hashed by host
+  // threads, never by the SMs: pack emits zeros for them, scatter skips them.
   struct Slot {
     const BulkItem* it;
     size_t rec0;
-    uint64_t pos0, page0;
+    uint64_t pos0, dev0, host0;
   };
   std::vector<Slot> slots;
+  uint64_t n_dev = 0, n_host = 0;
   for (const BulkItem& it : items) {
     if (it.kind != AllocationKind::Managed) continue;
     const uint64_t pages = page_count_for(it.size);
-    slots.push_back(Slot{&it, P.recs.size() + 0, pos, P.page_first.back()});
-    P.recs.resize(P.recs.size() + 1 + pages);
-    pos += 16 + 16 * pages + it.size;
-    P.page_spans.push_back(crac_span_t{it.ptr, it.size});
-    P.page_first.push_back(P.page_first.back() + pages);
-  }
-  // host-resident pages (flag bit0 clear) are moved by host threads, not by
-  // the SMs: pack emits zeros for them, scatter skips them
-  std::vector<uint64_t> host_first(slots.size() + 1, 0);
-  for (size_t k = 0; k < slots.size(); ++k) {
-    const BulkItem& it = *slots[k].it;
     uint64_t h = 0;
     if (it.flags)
       for (uint8_t f : *it.flags) h += (f & 1) ? 0 : 1;
-    host_first[k + 1] = host_first[k] + h;
+    slots.push_back(Slot{&it, P.recs.size(), pos, n_dev, n_host});
+    P.recs.resize(P.recs.size() + 1 + pages);
+    pos += 16 + 16 * pages + it.size;
+    n_dev += pages - h;
+    n_host += h;
+  }
+  P.n_dev_pages = n_dev;
+  for (const Slot& sl : slots) {  // device-resident runs, in page-index order
+    const BulkItem& it = *sl.it;
+    const uint64_t pages = page_count_for(it.size);
+    for (uint64_t p = 0; p < pages;) {
+      if (it.flags && !((*it.flags)[p] & 1)) {
+        ++p;
+        continue;
+      }
+      uint64_t q = p + 1;
+      while (q < pages && !(it.flags && !((*it.flags)[q] & 1))) ++q;
+      const uint64_t lo = p * kPageSize, hi = std::min(it.size, q * kPageSize);
+      P.page_spans.push_back(crac_span_t{it.ptr + lo, hi - lo});
+      P.page_first.push_back(P.page_first.back() + (q - p));
+      p = q;
+    }
   }
   tr.mark("layout");
-  P.host_pages.assign(host_first.back(), HostPage{});
+  P.host_pages.assign(n_host, HostPage{});
   parallel_for(slots.size(), [&](uint64_t k) {
     const Slot& sl = slots[k];
     const BulkItem& it = *sl.it;
@@ -476,26 +498,27 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
     std::memcpy(h.frame, &it.id, 8);
     std::memcpy(h.frame + 8, &pages, 8);
     uint64_t at = sl.pos0 + 16;
-    uint64_t hp = host_first[k];
+    uint64_t dp = sl.dev0, hp = sl.host0;
     for (uint64_t p = 0; p < pages; ++p) {
       const uint64_t off = p * kPageSize;
       const uint32_t len = uint32_t(std::min<uint64_t>(kPageSize, it.size - off));
       const uint32_t fl = it.flags ? (*it.flags)[p] : 0;
+      const bool host = it.flags && !(fl & 1);
       crac_record_t& r = P.recs[sl.rec0 + 1 + p];
       r = crac_record_t{};
       r.out_off = at;
-      r.ptr = it.ptr + off;
+      r.ptr = host ? 0 : it.ptr + off;
       r.len = len;
       r.ext = p + 1 == pages ? padded - off : len;
       r.frame_len = 16;
-      r.reserved = uint32_t(sl.page0 + p);  // its page-CRC index
+      r.reserved = uint32_t(host ? n_dev + hp : dp);  // its page-CRC index
       std::memcpy(r.frame, &p, 8);
       std::memcpy(r.frame + 8, &fl, 4);
       std::memcpy(r.frame + 12, &len, 4);
-      if (it.flags && !((*it.flags)[p] & 1)) {
-        P.host_pages[hp++] = HostPage{at + 16, r.ptr, len, uint32_t(r.ext), sl.rec0 + 1 + p};
-        r.ptr = 0;
-      }
+      if (host)
+        P.host_pages[hp++] = HostPage{at + 16, it.ptr + off, len, uint32_t(r.ext), sl.rec0 + 1 + p};
+      else
+        ++dp;
       at += 16 + len;
     }
   });
@@ -527,7 +550,7 @@ void upload_plan(DrainEngine& E, const ImagePlan& P, cudaStream_t st) {
   upload(E.d_pay_first, P.pay_first, st);
   upload(E.d_page_spans, P.page_spans, st);
   upload(E.d_page_first, P.page_first, st);
-  const uint64_t n_pay = P.pay_first.back(), n_page = P.page_first.back();
+  const uint64_t n_pay = P.pay_first.back(), n_page = P.n_dev_pages + P.host_pages.size();
   E.d_pay_crc.ensure(std::max<uint64_t>(n_pay, 1));
   E.d_page_crc.ensure(std::max<uint64_t>(n_page, 1));
 }
@@ -571,6 +594,60 @@ void enqueue_fold(DrainEngine& E, const ImagePlan& P, cudaStream_t st) {
 void finish_fold(const DrainEngine& E, const ImagePlan& P, uint32_t& crc3, uint32_t& crc4) {
   crc3 = E.h_fold.ptr[0] ^ crac::crc_affine(P.len3, pow2_table());
   crc4 = E.h_fold.ptr[1] ^ crac::crc_affine(P.len4, pow2_table());
+}
+
+// Host-resident managed pages of a drain.  Each host thread takes a block of
+// pages in stream order, hashes every page (zlib CRC, into h_host_crc) and,
+// for pages of the ring part [0, head), copies it into the image once the
+// D2H of the window holding its last byte has landed (the windows carry
+// zeros there; windows land in order on s_copy).  The CPU reads pages that
+// live on its side: nothing migrates and no device mapping is needed.
+void host_pages_drain(DrainEngine& E, const ImagePlan& P, uint8_t* stream, uint64_t head) {
+  const uint64_t n = P.host_pages.size();
+  if (!n) return;
+  E.h_host_crc.ensure(n);
+  uint32_t* crc = E.h_host_crc.ptr;
+  constexpr uint64_t W = DrainEngine::kWindow;
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::atomic<uint64_t> next{0};
+  std::atomic<int> failed{0};
+  auto worker = [&] {
+    int64_t landed = -1;
+    for (uint64_t b; (b = next.fetch_add(512)) < n;)
+      for (uint64_t i = b; i < std::min(n, b + 512); ++i) {
+        const HostPage& h = P.host_pages[i];
+        const auto* src = reinterpret_cast<const uint8_t*>(h.ptr);
+        crc[i] = crc32_host(src, h.len);
+        if (h.stream_off + h.len > head) continue;  // shadow part: the pack reads it
+        const int64_t w = int64_t((h.stream_off + h.len - 1) / W);
+        if (w > landed) {
+          if (cudaEventSynchronize(E.ev_land[w]) != cudaSuccess) failed = 1;
+          landed = w;
+        }
+        std::memcpy(stream + h.stream_off, src, h.len);
+      }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < hw; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& t : pool) t.join();
+  if (failed) raise(Errc::DeviceFault, "D2H window failed under a host-page copy");
+}
+
+// Host-resident managed pages of a refill: image -> managed memory, then the
+// CRC of what landed (zero tail up to ext).
+void host_pages_refill(DrainEngine& E, const ImagePlan& P, const uint8_t* stream) {
+  const uint64_t n = P.host_pages.size();
+  if (!n) return;
+  E.h_host_crc.ensure(n);
+  uint32_t* crc = E.h_host_crc.ptr;
+  parallel_for(n, [&](uint64_t i) {
+    const HostPage& h = P.host_pages[i];
+    uint8_t* dst = reinterpret_cast<uint8_t*>(h.ptr);
+    std::memcpy(dst, stream + h.stream_off, h.len);
+    if (h.ext > h.len) std::memset(dst + h.len, 0, h.ext - h.len);
+    crc[i] = crc32_host(dst, h.len);
+  });
 }
 
 template <typename T>
@@ -705,19 +782,20 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   Q.head = head;
   // host-resident pages reaching into the shadow part are read by the pack
   // kernels over the link (the app may touch them once it resumes); pages
-  // wholly in the ring part keep the host-thread copy after its D2H
-  std::vector<HostPage> ring_pages;
-  for (const HostPage& h : P.host_pages) {
-    if (h.stream_off + h.len > head)
+  // wholly in the ring part are copied by host threads after their D2H.
+  // Either way their CRCs come from the host threads.
+  bool shadow_host_pages = false;
+  for (const HostPage& h : P.host_pages)
+    if (h.stream_off + h.len > head) {
       P.recs[h.rec].ptr = h.ptr;
-    else
-      ring_pages.push_back(h);
-  }
-
+      shadow_host_pages = true;
+    }
   std::vector<uint64_t> managed_ids;
-  for (const AllocationRecord& rec : active)
-    if (rec.kind == AllocationKind::Managed) managed_ids.push_back(rec.id);
+  if (shadow_host_pages)
+    for (const AllocationRecord& rec : active)
+      if (rec.kind == AllocationKind::Managed) managed_ids.push_back(rec.id);
   for (uint64_t id : managed_ids) ctx.managed_remote_access(id, true);
+  tr.mark("remote-access");
 
   // With the whole stream in the shadow, K1 copies every payload chunk to
   // its stream position right after hashing it: one HBM read of the state
@@ -745,11 +823,11 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   } else if (P.pay_first.back()) {
     hash_payloads(E, P, 0, P.pay_first.back(), k1_ctas, E.s_hash);
   }
-  // pages: host-resident ones are read over the link, so a modest grid
-  // saturates it and leaves the rest of the SMs to the pack
-  if (P.page_first.back()) hash_pages(E, P, std::min<uint32_t>(k1_ctas, 48), E.s_hash);
+  // pages: the device-resident runs (the host-resident ones are hashed by
+  // the host threads that move them)
+  if (P.n_dev_pages) hash_pages(E, P, k1_ctas, E.s_hash);
   check_cuda(cudaEventRecord(E.ev_h1, E.s_hash), "event");
-  enqueue_fold(E, P, E.s_hash);
+  tr.mark("k1-launch");
 
   // shadow windows: pack at HBM speed on their own stream, beside the ring
   // (fused: only from the 16-byte word holding crc3 on; the payload bytes
@@ -765,6 +843,8 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   const uint64_t windows = (head + W - 1) / W;
   Q.windows = windows;
   if (stats) E.ensure_window_events(windows);
+  const bool land_events = !P.host_pages.empty();
+  if (land_events) E.ensure_land_events(windows);
   check_cuda(cudaEventRecord(E.ev_c0, E.s_pack), "event");
   for (uint64_t w = 0; w < windows; ++w) {
     const int slot = int(w % DrainEngine::kSlots);
@@ -788,14 +868,24 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
                                  cudaMemcpyDeviceToHost, E.s_copy),
                  "D2H");
     check_cuda(cudaEventRecord(E.ev_free[slot], E.s_copy), "event");
+    if (land_events) check_cuda(cudaEventRecord(E.ev_land[w], E.s_copy), "event");
   }
+  tr.mark("enqueue");
+  // host-resident pages: hashed (all) and copied (ring part) by host threads
+  // while the windows drain; then K4 folds every CRC
+  host_pages_drain(E, P, img + s3, head);
+  if (!P.host_pages.empty())
+    check_cuda(cudaMemcpyAsync(E.d_page_crc.ptr + P.n_dev_pages, E.h_host_crc.ptr,
+                               P.host_pages.size() * 4, cudaMemcpyHostToDevice, E.s_hash),
+               "host page crcs");
+  enqueue_fold(E, P, E.s_hash);
+  tr.mark("host-pages");
   // snapshot complete = K1/K4, the shadow packs and the ring D2H have landed
   check_cuda(cudaEventRecord(E.ev_join[0], E.s_hash), "event");
   check_cuda(cudaEventRecord(E.ev_join[1], E.s_shadow), "event");
   check_cuda(cudaEventRecord(E.ev_join[2], E.s_copy), "event");
   for (cudaEvent_t e : E.ev_join) check_cuda(cudaStreamWaitEvent(E.s_pack, e, 0), "wait");
   check_cuda(cudaEventRecord(E.ev_s1, E.s_pack), "event");
-  tr.mark("enqueue");
   // the section CRCs are ready long before the D2H finishes
   check_cuda(cudaStreamSynchronize(E.s_hash), "hash sync");
   tr.mark("hash+fold");
@@ -810,14 +900,8 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   }
   check_cuda(cudaEventSynchronize(E.ev_s1), "snapshot sync");
   tr.mark("d2h-wait");
-  // host-resident pages of the ring part: managed memory -> image by host
-  // threads (the windows carried zeros there; their D2H has landed)
-  parallel_for(ring_pages.size(), [&](uint64_t i) {
-    const HostPage& h = ring_pages[i];
-    std::memcpy(img + s3 + h.stream_off, reinterpret_cast<const void*>(h.ptr), h.len);
-  });
-  tr.mark("host-pages");
   for (uint64_t id : managed_ids) ctx.managed_remote_access(id, false);
+  tr.mark("remote-access-off");
   for (const HostPage& h : P.host_pages) P.recs[h.rec].ptr = 0;  // the plan's invariant
 
   // the app may run from here on: the shadow -> image D2H reads only HBM
@@ -855,7 +939,7 @@ void drain_finish(Session& session, DrainStats* stats) {
     if (bulk) {
       stats->hash_ms = elapsed(E.ev_h0, E.ev_h1);
       stats->copy_ms = elapsed(E.ev_c0, E.ev_c1);
-      stats->hash_launches = (P.pay_first.back() ? 1 : 0) + (P.page_first.back() ? 1 : 0);
+      stats->hash_launches = (P.pay_first.back() ? 1 : 0) + (P.n_dev_pages ? 1 : 0);
       stats->hash_bytes = hashed_bytes(P);
       stats->pack_launches = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
       stats->pack_bytes = P.stream_len;
@@ -864,7 +948,7 @@ void drain_finish(Session& session, DrainStats* stats) {
       stats->shadow_bytes = P.stream_len - Q.head;
     }
     stats->image_bytes = P.image_bytes;
-    stats->total_chunks = P.pay_first.back() + P.page_first.back();
+    stats->total_chunks = P.pay_first.back() + P.n_dev_pages + P.host_pages.size();
     stats->dirty_chunks = stats->total_chunks;
   }
   Q = DrainEngine::Pending{};
@@ -930,14 +1014,14 @@ void hash_only(Session& session, DrainStats* stats) {
   upload_plan(E, P, E.s_hash);
   check_cuda(cudaEventRecord(E.ev_h0, E.s_hash), "event");
   if (P.pay_first.back()) hash_payloads(E, P, 0, P.pay_first.back(), 0, E.s_hash);
-  if (P.page_first.back()) hash_pages(E, P, 0, E.s_hash);
+  if (P.n_dev_pages) hash_pages(E, P, 0, E.s_hash);
   check_cuda(cudaEventRecord(E.ev_h1, E.s_hash), "event");
   check_cuda(cudaStreamSynchronize(E.s_hash), "hash sync");
   if (stats) {
     stats->hash_ms = stats->total_ms = elapsed(E.ev_h0, E.ev_h1);
     stats->hash_bytes = hashed_bytes(P);
-    stats->hash_launches = (P.pay_first.back() ? 1 : 0) + (P.page_first.back() ? 1 : 0);
-    stats->total_chunks = P.pay_first.back() + P.page_first.back();
+    stats->hash_launches = (P.pay_first.back() ? 1 : 0) + (P.n_dev_pages ? 1 : 0);
+    stats->total_chunks = P.pay_first.back() + P.n_dev_pages + P.host_pages.size();
   }
   E.plan.valid = false;  // the device tables now describe this pass, not an image
   E.prev_valid = false;
@@ -1032,25 +1116,14 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     raise(Errc::ImageCorrupt, "bulk sections do not match the log's active set");
   tr.mark("plan");
 
-  // managed pages: populate each run where the image says it lives, and let
-  // the scatter write host-resident pages over the link without migrating
   // managed pages land where they were: device-resident ones are first
-  // touched by the scatter kernel, host-resident ones by the host threads
-  // below, so no prefetch (or migration) is needed to restore residence
+  // touched by the scatter kernel (and verified by K1), host-resident ones
+  // are written and hashed by the host threads below, so nothing migrates
+  // and no prefetch or device mapping is needed to restore residence
   mi = 0;
   for (const AllocationRecord& rec : p.facts.active)
-    if (rec.kind == AllocationKind::Managed) {
-      ctx.set_managed_flags(rec.id, p.managed[mi++].flags);
-      ctx.managed_remote_access(rec.id, true);  // K1 verify reads host pages in place
-    }
-  std::thread host_fill([&] {
-    parallel_for(P.host_pages.size(), [&](uint64_t i) {
-      const HostPage& h = P.host_pages[i];
-      uint8_t* dst = reinterpret_cast<uint8_t*>(h.ptr);
-      std::memcpy(dst, raw.data() + s3 + h.stream_off, h.len);
-      if (h.ext > h.len) std::memset(dst + h.len, 0, h.ext - h.len);
-    });
-  });
+    if (rec.kind == AllocationKind::Managed) ctx.set_managed_flags(rec.id, p.managed[mi++].flags);
+  std::thread host_fill([&] { host_pages_refill(E, P, raw.data() + s3); });
   struct Joiner {
     std::thread& t;
     ~Joiner() {
@@ -1111,8 +1184,8 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       }
     }
     check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
-    host_fill.join();  // host-resident pages must be in place before their K1
-    if (P.page_first.back()) {
+    tr.mark("windows");
+    if (P.n_dev_pages) {
       if (stats) {
         E.ensure_verify_events(verifies + 1);
         cudaEventRecord(E.ev_v0[verifies], E.s_pack);
@@ -1121,6 +1194,12 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       if (stats) cudaEventRecord(E.ev_v1[verifies], E.s_pack);
       ++verifies;
     }
+    host_fill.join();  // the host-resident pages' CRCs
+    tr.mark("host-fill-join");
+    if (!P.host_pages.empty())
+      check_cuda(cudaMemcpyAsync(E.d_page_crc.ptr + P.n_dev_pages, E.h_host_crc.ptr,
+                                 P.host_pages.size() * 4, cudaMemcpyHostToDevice, E.s_pack),
+                 "host page crcs");
     enqueue_fold(E, P, E.s_pack);
     tr.mark("enqueue");
     check_cuda(cudaStreamSynchronize(E.s_pack), "refill sync");
@@ -1132,8 +1211,6 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   } else if (p.sec[2].crc != 0 || p.sec[3].crc != 0) {
     raise(Errc::ImageCorrupt, "crc mismatch in empty bulk section");
   }
-  for (const AllocationRecord& rec : p.facts.active)
-    if (rec.kind == AllocationKind::Managed) ctx.managed_remote_access(rec.id, false);
   check_cuda(cudaEventRecord(E.ev_t1, E.s_pack), "event");
   check_cuda(cudaEventSynchronize(E.ev_t1), "event sync");
   E.prev_valid = false;  // no pinned image of this session exists yet
@@ -1154,7 +1231,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       for (uint64_t v = 0; v < verifies; ++v) stats->hash_ms += elapsed(E.ev_v0[v], E.ev_v1[v]);
     }
     stats->image_bytes = raw.size();
-    stats->total_chunks = P.pay_first.back() + P.page_first.back();
+    stats->total_chunks = P.pay_first.back() + P.n_dev_pages + P.host_pages.size();
   }
   return session;
 }

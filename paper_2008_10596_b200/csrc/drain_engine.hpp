@@ -51,6 +51,8 @@ struct HostArray {  // pinned
 // Layout of the last image this session drained (enables incremental drains).
 // A host-resident managed page: its content is copied by host threads
 // between the managed allocation and the image (never crosses PCIe).
+// Its CRC is computed by the host thread that moves it (h_host_crc[k] for
+// host_pages[k]); K1 hashes device-resident pages only.
 struct HostPage {
   uint64_t stream_off;  // content offset in the bulk stream
   uint64_t ptr;         // managed address of the page
@@ -66,8 +68,11 @@ struct ImagePlan {
   uint64_t stream_len = 0;  // len3 + 20 + len4
   std::vector<crac_record_t> recs;
   std::vector<uint32_t> tile_rec;
-  std::vector<crac_span_t> pay_spans, page_spans;
+  std::vector<crac_span_t> pay_spans, page_spans;  // page_spans: device-resident runs
   std::vector<uint64_t> pay_first, page_first;
+  // page-CRC index space (record.reserved): device-resident pages [0, n_dev),
+  // in page_spans order; host-resident pages n_dev + k for host_pages[k]
+  uint64_t n_dev_pages = 0;
   std::vector<uint64_t> pay_rec_off;  // stream offset of each payload's first byte
   std::vector<uint64_t> log_sizes;    // signature: (id, size) of every bulk record
   std::vector<HostPage> host_pages;   // host-resident managed pages
@@ -103,6 +108,8 @@ struct DrainEngine {
   DevArray<unsigned long long> d_counters;
   DevArray<uint32_t> d_fold;   // linear parts of crc3 / crc4 (K4)
   HostArray<uint32_t> h_fold;
+  HostArray<uint32_t> h_host_crc;          // CRCs of host-resident pages (host threads)
+  std::vector<cudaEvent_t> ev_land;        // window w's D2H has landed (host-page copies)
   HostArray<uint64_t> h_count, h_dirty_idx;
 
   // Stall-reduced drain (checkpoint_begin/finish): the tail of the bulk
@@ -132,6 +139,7 @@ struct DrainEngine {
   DrainEngine& operator=(const DrainEngine&) = delete;
   void ensure_window_events(size_t n);
   void ensure_verify_events(size_t n);
+  void ensure_land_events(size_t n);
 };
 
 // Process-wide engine pool (Session construction / destruction).
