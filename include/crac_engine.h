@@ -167,6 +167,10 @@ int crac_mutate_device(crac_session_t* s, uint64_t seed, uint64_t epoch, uint64_
  * session, chunk CRCs left on the device; stats.hash_ms / hash_bytes. */
 int crac_hash_session(crac_session_t* s, crac_stats_t* stats);
 
+/* Host CRC-32 the engine uses for host-resident pages and small sections
+ * (zlib's crc32, bit-identical; PCLMUL folding).  No GPU needed. */
+uint32_t crac_crc32_host(const void* data, uint64_t n, uint32_t crc);
+
 /* Kernel-level entry for parity tests: CRC of every 64 KiB (chunk_bytes)
  * chunk of a host buffer, computed by K1 on the GPU. */
 int crac_hash_host_buffer(const void* data, uint64_t n, uint32_t chunk_bytes, uint32_t* crc_out);

@@ -33,7 +33,7 @@ EXTRA = {
     "kernels.cu": ["-Xptxas", "-v"] if os.environ.get("CRAC_PTXAS_V") else [],
 }
 SOURCES = ["kernels.cu", "device_core.cu", "drain.cu", "std_kernels.cu",
-           "shim.cpp", "image.cpp", "image_io.cpp", "ckpt_engine.cpp", "capi.cpp"]
+           "shim.cpp", "image.cpp", "image_io.cpp", "crc_host.cpp", "ckpt_engine.cpp", "capi.cpp"]
 
 
 def _headers_mtime() -> float:

@@ -348,6 +348,10 @@ int crac_file_read(const char* path, void* dst, uint64_t capacity, uint32_t thre
   });
 }
 
+uint32_t crac_crc32_host(const void* data, uint64_t n, uint32_t crc) {
+  return codec::crc32_fast(static_cast<const uint8_t*>(data), n, crc);
+}
+
 int crac_decode_check(const void* image, uint64_t size) {
   return guard([&] { (void)decode_image({static_cast<const uint8_t*>(image), size}); });
 }

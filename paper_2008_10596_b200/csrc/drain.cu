@@ -350,18 +350,20 @@ const uint32_t* pow2_table() {
 
 // fn(0..n-1) on up to 16 host threads (only worth it for big plans).
 template <typename Fn>
-void parallel_for(uint64_t n, Fn&& fn) {
+void parallel_for(uint64_t n, Fn&& fn, uint64_t min_parallel = 4096) {
   const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  if (n < 4096 || hw == 1) {
+  if (n < min_parallel || hw == 1) {
     for (uint64_t i = 0; i < n; ++i) fn(i);
     return;
   }
+  // blocks small enough that a few big items (managed allocations) spread
+  const uint64_t blk = std::max<uint64_t>(1, std::min<uint64_t>(1024, n / (4 * hw)));
   std::atomic<uint64_t> next{0};
   std::vector<std::thread> pool;
   for (unsigned t = 0; t < hw; ++t)
     pool.emplace_back([&] {
-      for (uint64_t b; (b = next.fetch_add(1024)) < n;)
-        for (uint64_t i = b; i < std::min(n, b + 1024); ++i) fn(i);
+      for (uint64_t b; (b = next.fetch_add(blk)) < n;)
+        for (uint64_t i = b; i < std::min(n, b + blk); ++i) fn(i);
     });
   for (auto& th : pool) th.join();
 }
@@ -454,37 +456,45 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
     size_t rec0;
     uint64_t pos0, dev0, host0;
   };
-  std::vector<Slot> slots;
-  uint64_t n_dev = 0, n_host = 0;
-  for (const BulkItem& it : items) {
-    if (it.kind != AllocationKind::Managed) continue;
+  std::vector<const BulkItem*> managed;
+  for (const BulkItem& it : items)
+    if (it.kind == AllocationKind::Managed) managed.push_back(&it);
+  // per allocation (in parallel): its device-resident runs and host count
+  std::vector<std::vector<crac_span_t>> runs(managed.size());
+  std::vector<uint64_t> host_n(managed.size(), 0);
+  parallel_for(managed.size(), [&](uint64_t k) {
+    const BulkItem& it = *managed[k];
     const uint64_t pages = page_count_for(it.size);
-    uint64_t h = 0;
-    if (it.flags)
-      for (uint8_t f : *it.flags) h += (f & 1) ? 0 : 1;
-    slots.push_back(Slot{&it, P.recs.size(), pos, n_dev, n_host});
-    P.recs.resize(P.recs.size() + 1 + pages);
-    pos += 16 + 16 * pages + it.size;
-    n_dev += pages - h;
-    n_host += h;
-  }
-  P.n_dev_pages = n_dev;
-  for (const Slot& sl : slots) {  // device-resident runs, in page-index order
-    const BulkItem& it = *sl.it;
-    const uint64_t pages = page_count_for(it.size);
+    const uint8_t* f = it.flags ? it.flags->data() : nullptr;
     for (uint64_t p = 0; p < pages;) {
-      if (it.flags && !((*it.flags)[p] & 1)) {
+      if (f && !(f[p] & 1)) {
+        ++host_n[k];
         ++p;
         continue;
       }
       uint64_t q = p + 1;
-      while (q < pages && !(it.flags && !((*it.flags)[q] & 1))) ++q;
+      while (q < pages && !(f && !(f[q] & 1))) ++q;
       const uint64_t lo = p * kPageSize, hi = std::min(it.size, q * kPageSize);
-      P.page_spans.push_back(crac_span_t{it.ptr + lo, hi - lo});
-      P.page_first.push_back(P.page_first.back() + (q - p));
+      runs[k].push_back(crac_span_t{it.ptr + lo, hi - lo});
       p = q;
     }
+  }, /*min_parallel=*/2);
+  std::vector<Slot> slots;
+  uint64_t n_dev = 0, n_host = 0;
+  for (size_t k = 0; k < managed.size(); ++k) {
+    const BulkItem& it = *managed[k];
+    const uint64_t pages = page_count_for(it.size);
+    slots.push_back(Slot{&it, P.recs.size(), pos, n_dev, n_host});
+    P.recs.resize(P.recs.size() + 1 + pages);
+    pos += 16 + 16 * pages + it.size;
+    n_dev += pages - host_n[k];
+    n_host += host_n[k];
+    for (const crac_span_t& r : runs[k]) {  // device-resident runs, in page-index order
+      P.page_spans.push_back(r);
+      P.page_first.push_back(P.page_first.back() + (r.len + kPageSize - 1) / kPageSize);
+    }
   }
+  P.n_dev_pages = n_dev;
   tr.mark("layout");
   P.host_pages.assign(n_host, HostPage{});
   parallel_for(slots.size(), [&](uint64_t k) {
@@ -521,7 +531,7 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
         ++dp;
       at += 16 + len;
     }
-  });
+  }, /*min_parallel=*/2);
   tr.mark("pages");
   P.stream_len = pos;
   const uint64_t tiles = (pos + CRAC_TILE_BYTES - 1) / CRAC_TILE_BYTES;
@@ -617,7 +627,7 @@ void host_pages_drain(DrainEngine& E, const ImagePlan& P, uint8_t* stream, uint6
       for (uint64_t i = b; i < std::min(n, b + 512); ++i) {
         const HostPage& h = P.host_pages[i];
         const auto* src = reinterpret_cast<const uint8_t*>(h.ptr);
-        crc[i] = crc32_host(src, h.len);
+        crc[i] = crc32_fast(src, h.len);
         if (h.stream_off + h.len > head) continue;  // shadow part: the pack reads it
         const int64_t w = int64_t((h.stream_off + h.len - 1) / W);
         if (w > landed) {
@@ -646,7 +656,7 @@ void host_pages_refill(DrainEngine& E, const ImagePlan& P, const uint8_t* stream
     uint8_t* dst = reinterpret_cast<uint8_t*>(h.ptr);
     std::memcpy(dst, stream + h.stream_off, h.len);
     if (h.ext > h.len) std::memset(dst + h.len, 0, h.ext - h.len);
-    crc[i] = crc32_host(dst, h.len);
+    crc[i] = crc32_fast(dst, h.len);
   });
 }
 

@@ -49,3 +49,25 @@ def test_reference_style_client_runs_on_b200(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.strip().endswith("ok")
+
+
+def test_host_crc_is_zlib():
+    """crac_crc32_host (PCLMUL folding, crc_host.cpp) == zlib.crc32 for every
+    length around the 16/64-byte fold boundaries, any alignment and seed."""
+    import ctypes
+    import os
+    import zlib
+
+    from paper_2008_10596_b200 import engine
+    if not engine.LIB_PATH.exists():
+        from paper_2008_10596_b200 import build
+        build.build()
+    lib = engine.lib()
+    buf = os.urandom(1 << 16)
+    cbuf = ctypes.create_string_buffer(buf, len(buf))
+    base = ctypes.addressof(cbuf)
+    for n in list(range(0, 300)) + [4095, 4096, 4097, 65536 - 16]:
+        for off in (0, 1, 5, 15):
+            for seed in (0, 0xDEADBEEF):
+                got = lib.crac_crc32_host(ctypes.c_void_p(base + off), n, seed)
+                assert got == zlib.crc32(buf[off:off + n], seed), (n, off, seed)
