@@ -606,6 +606,63 @@ void finish_fold(const DrainEngine& E, const ImagePlan& P, uint32_t& crc3, uint3
   crc4 = E.h_fold.ptr[1] ^ crac::crc_affine(P.len4, pow2_table());
 }
 
+// Host runs: maximal stream ranges made only of host-resident pages (frame +
+// content of consecutive pages), at least kSkipMin long and wholly below
+// `limit`.  The window D2H / H2D skips them -- they never cross PCIe -- and
+// the host threads write those pages' frames as well as their content.
+// Shorter runs travel as the pack's zeros and are overwritten after landing.
+constexpr uint64_t kSkipMin = 256ull << 10;
+
+void plan_host_runs(ImagePlan& P, uint64_t limit) {
+  P.host_runs.clear();
+  const size_t n = P.host_pages.size();
+  for (size_t i = 0; i < n;) {
+    const uint64_t lo = P.host_pages[i].stream_off - 16;
+    uint64_t hi = P.host_pages[i].stream_off + P.host_pages[i].len;
+    size_t j = i + 1;
+    while (j < n && P.host_pages[j].stream_off - 16 == hi) {
+      hi = P.host_pages[j].stream_off + P.host_pages[j].len;
+      ++j;
+    }
+    const bool skip = hi - lo >= kSkipMin && hi <= limit;
+    if (skip) P.host_runs.emplace_back(lo, hi);
+    for (size_t k = i; k < j; ++k) P.host_pages[k].own_frame = skip;
+    i = j;
+  }
+}
+
+uint64_t host_run_bytes(const ImagePlan& P) {
+  uint64_t b = 0;
+  for (const auto& r : P.host_runs) b += r.second - r.first;
+  return b;
+}
+
+// Enqueues the copy of stream bytes [off, end) between a window buffer
+// (`buf` holds stream offset `off`) and the image stream, minus the host runs,
+// in pieces of at most kCopyChunk.  `run` walks P.host_runs across calls.
+void copy_window(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, uint8_t* buf,
+                 uint8_t* stream, bool d2h, cudaStream_t st) {
+  const auto& R = P.host_runs;
+  for (uint64_t a = off; a < end;) {
+    while (run < R.size() && R[run].second <= a) ++run;
+    uint64_t b = end;
+    if (run < R.size() && R[run].first < end) {
+      if (R[run].first <= a) {
+        a = std::min(end, R[run].second);
+        continue;
+      }
+      b = R[run].first;
+    }
+    for (uint64_t c = a; c < b; c += DrainEngine::kCopyChunk) {
+      const uint64_t n = std::min(DrainEngine::kCopyChunk, b - c);
+      check_cuda(d2h ? cudaMemcpyAsync(stream + c, buf + (c - off), n, cudaMemcpyDeviceToHost, st)
+                     : cudaMemcpyAsync(buf + (c - off), stream + c, n, cudaMemcpyHostToDevice, st),
+                 d2h ? "D2H" : "H2D");
+    }
+    a = b;
+  }
+}
+
 // Host-resident managed pages of a drain.  Each host thread takes a block of
 // pages in stream order, hashes every page (zlib CRC, into h_host_crc) and,
 // for pages of the ring part [0, head), copies it into the image once the
@@ -628,6 +685,11 @@ void host_pages_drain(DrainEngine& E, const ImagePlan& P, uint8_t* stream, uint6
         const HostPage& h = P.host_pages[i];
         const auto* src = reinterpret_cast<const uint8_t*>(h.ptr);
         crc[i] = crc32_fast(src, h.len);
+        if (h.own_frame) {  // in a host run: no window copy touches these bytes
+          std::memcpy(stream + h.stream_off - 16, P.recs[h.rec].frame, 16);
+          std::memcpy(stream + h.stream_off, src, h.len);
+          continue;
+        }
         if (h.stream_off + h.len > head) continue;  // shadow part: the pack reads it
         const int64_t w = int64_t((h.stream_off + h.len - 1) / W);
         if (w > landed) {
@@ -794,6 +856,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   // kernels over the link (the app may touch them once it resumes); pages
   // wholly in the ring part are copied by host threads after their D2H.
   // Either way their CRCs come from the host threads.
+  plan_host_runs(P, head);
   bool shadow_host_pages = false;
   for (const HostPage& h : P.host_pages)
     if (h.stream_off + h.len > head) {
@@ -856,6 +919,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   const bool land_events = !P.host_pages.empty();
   if (land_events) E.ensure_land_events(windows);
   check_cuda(cudaEventRecord(E.ev_c0, E.s_pack), "event");
+  size_t run_i = 0;
   for (uint64_t w = 0; w < windows; ++w) {
     const int slot = int(w % DrainEngine::kSlots);
     uint8_t* buf = E.d_ring + slot * (W + 64);
@@ -872,11 +936,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
     check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_pack), "event");
     check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_ready[slot], 0), "wait");
     // the copy engine runs best on 16 MiB pieces; the pack on bigger windows
-    for (uint64_t c = 0; c < len; c += DrainEngine::kCopyChunk)
-      check_cuda(cudaMemcpyAsync(img + s3 + off + c, buf + c,
-                                 std::min(DrainEngine::kCopyChunk, len - c),
-                                 cudaMemcpyDeviceToHost, E.s_copy),
-                 "D2H");
+    copy_window(P, run_i, off, off + len, buf, img + s3, true, E.s_copy);
     check_cuda(cudaEventRecord(E.ev_free[slot], E.s_copy), "event");
     if (land_events) check_cuda(cudaEventRecord(E.ev_land[w], E.s_copy), "event");
   }
@@ -954,7 +1014,7 @@ void drain_finish(Session& session, DrainStats* stats) {
       stats->pack_launches = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
       stats->pack_bytes = P.stream_len;
       stats->pack_ms = Q.windows ? median_window_ms(E, Q.windows) : 0;  // per ring launch
-      stats->d2h_bytes = P.stream_len;
+      stats->d2h_bytes = P.stream_len - host_run_bytes(P);
       stats->shadow_bytes = P.stream_len - Q.head;
     }
     stats->image_bytes = P.image_bytes;
@@ -1119,6 +1179,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   tr.mark("items");
   ImagePlan& P = E.plan;
   build_plan(items, P);
+  plan_host_runs(P, P.stream_len);
   P.log_len = p.log.size();
   const uint64_t s3 = p.sec[2].payload_off;
   if (P.len3 != p.sec[2].length || P.len4 != p.sec[3].length ||
@@ -1150,7 +1211,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     windows = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
     if (stats) E.ensure_window_events(windows);
     check_cuda(cudaEventRecord(E.ev_c0, E.s_copy), "event");
-    size_t spans_done = 0;
+    size_t spans_done = 0, run_i = 0;
     constexpr uint64_t kVerifyBatch = 8192;  // 512 MiB of 64 KiB chunks
     for (uint64_t w = 0; w < windows; ++w) {
       const int slot = int(w % DrainEngine::kSlots);
@@ -1160,11 +1221,8 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       const uint64_t with_ahead = std::min(len + 16, P.stream_len - off);
       if (w >= uint64_t(DrainEngine::kSlots))
         check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_free[slot], 0), "wait");
-      for (uint64_t c = 0; c < with_ahead; c += DrainEngine::kCopyChunk)
-        check_cuda(cudaMemcpyAsync(buf + c, raw.data() + s3 + off + c,
-                                   std::min(DrainEngine::kCopyChunk, with_ahead - c),
-                                   cudaMemcpyHostToDevice, E.s_copy),
-                   "H2D");
+      copy_window(P, run_i, off, off + with_ahead, buf, const_cast<uint8_t*>(raw.data() + s3),
+                  false, E.s_copy);
       check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_copy), "event");
       check_cuda(cudaStreamWaitEvent(E.s_pack, E.ev_ready[slot], 0), "wait");
       if (stats) cudaEventRecord(E.ev_w0[w], E.s_pack);
@@ -1235,7 +1293,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       stats->pack_launches = windows;
       stats->pack_bytes = P.stream_len;
       stats->pack_ms = median_window_ms(E, windows);
-      stats->h2d_bytes = P.stream_len;
+      stats->h2d_bytes = P.stream_len - host_run_bytes(P);
       stats->hash_bytes = hashed_bytes(P);
       stats->hash_launches = verifies;
       for (uint64_t v = 0; v < verifies; ++v) stats->hash_ms += elapsed(E.ev_v0[v], E.ev_v1[v]);

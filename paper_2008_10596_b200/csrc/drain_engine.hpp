@@ -58,6 +58,7 @@ struct HostPage {
   uint64_t ptr;         // managed address of the page
   uint32_t len, ext;    // content bytes; bytes to write on refill (zero tail)
   uint64_t rec;         // its record in ImagePlan::recs (ptr zeroed there)
+  bool own_frame = false;  // in a skipped host run: the host writes its frame too
 };
 
 struct ImagePlan {
@@ -76,6 +77,9 @@ struct ImagePlan {
   std::vector<uint64_t> pay_rec_off;  // stream offset of each payload's first byte
   std::vector<uint64_t> log_sizes;    // signature: (id, size) of every bulk record
   std::vector<HostPage> host_pages;   // host-resident managed pages
+  // stream ranges of host-resident pages only (frames + content), long
+  // enough that the window copies skip them (plan_host_runs)
+  std::vector<std::pair<uint64_t, uint64_t>> host_runs;
   uint64_t log_len = 0;
   uint64_t tail_bytes = 0;  // STREAMS + APPSTATE + KERNEL_REGISTRY, framed
   bool valid = false;

@@ -344,6 +344,35 @@ def test_c3_managed_mixed_residence_matches_reference(eng):
     assert rs.checkpoint()[0] == img
 
 
+def test_c3_host_runs_skip_the_link_and_match_reference(eng):
+    """Host-resident runs >= 256 KiB never cross PCIe (the window copies skip
+    them; host threads write their frames and content).  Runs straddle the
+    64 MiB window boundaries, one ends at a partial last page, short runs
+    (< 256 KiB) ride along as zeros and are overwritten after landing."""
+    MIB = 1 << 20
+    s = eng.Session(seed=4, arena_bytes=256 * MIB)
+    r = ref.RefSession(seed=4, arena_bytes=256 * MIB)
+    sizes = [40 * MIB + 4096 * k + 77 * k for k in range(3)]
+    for api in (s, r):
+        for k, size in enumerate(sizes):
+            i, _ = api.alloc(workloads.MANAGED, size)
+            api.fill_synthetic(i, 9 + k, workloads.DEVICE_SIDE)
+            for off in range(MIB // 2, size - MIB, 2 * MIB):       # 1 MiB runs
+                api.page_read(i, off, MIB, workloads.HOST_SIDE)
+            for off in range(MIB // 4, 8 * MIB, 4 * MIB):          # 64 KiB runs
+                api.page_read(i, off, 64 << 10, workloads.HOST_SIDE)
+            api.page_read(i, size - 300 * 1024, 300 * 1024, workloads.HOST_SIDE)  # to the end
+        d, _ = api.alloc(workloads.DEVICE, 3 * MIB + 5)
+        api.fill_synthetic(d, 7)
+    img, st = s.checkpoint()
+    assert img == r.checkpoint()[0]
+    assert st["d2h_bytes"] < len(img) * 0.7  # the big host runs stayed off the link
+    rs, rst = eng.restart(img)
+    assert rst["h2d_bytes"] == st["d2h_bytes"]
+    assert _state(rs) == _state(s)
+    assert rs.checkpoint()[0] == img
+
+
 # ---------------------------------------------------------------------------
 # edge shapes and error parity (test_device_core.cpp / test_shim.cpp cases)
 # ---------------------------------------------------------------------------
