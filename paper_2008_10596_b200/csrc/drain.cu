@@ -672,6 +672,21 @@ void copy_window(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, ui
 void host_pages_drain(DrainEngine& E, const ImagePlan& P, uint8_t* stream, uint64_t head) {
   const uint64_t n = P.host_pages.size();
   if (!n) return;
+  // short-run pages of the shadow part: stashed now (the app may change them
+  // once it resumes), written after the shadow D2H (drain_finish)
+  DrainEngine::Pending& Q = E.pending;
+  Q.stash_at.clear();
+  std::vector<uint64_t> stash_of(n, ~0ull);
+  uint64_t stash_bytes = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const HostPage& h = P.host_pages[i];
+    if (!h.own_frame && h.stream_off + h.len > head) {
+      stash_of[i] = stash_bytes;
+      Q.stash_at.emplace_back(h.stream_off, h.len);
+      stash_bytes += h.len;
+    }
+  }
+  Q.stash.resize(stash_bytes);
   E.h_host_crc.ensure(n);
   uint32_t* crc = E.h_host_crc.ptr;
   constexpr uint64_t W = DrainEngine::kWindow;
@@ -690,7 +705,10 @@ void host_pages_drain(DrainEngine& E, const ImagePlan& P, uint8_t* stream, uint6
           std::memcpy(stream + h.stream_off, src, h.len);
           continue;
         }
-        if (h.stream_off + h.len > head) continue;  // shadow part: the pack reads it
+        if (stash_of[i] != ~0ull) {
+          std::memcpy(Q.stash.data() + stash_of[i], src, h.len);
+          continue;
+        }
         const int64_t w = int64_t((h.stream_off + h.len - 1) / W);
         if (w > landed) {
           if (cudaEventSynchronize(E.ev_land[w]) != cudaSuccess) failed = 1;
@@ -856,19 +874,10 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   // kernels over the link (the app may touch them once it resumes); pages
   // wholly in the ring part are copied by host threads after their D2H.
   // Either way their CRCs come from the host threads.
-  plan_host_runs(P, head);
-  bool shadow_host_pages = false;
-  for (const HostPage& h : P.host_pages)
-    if (h.stream_off + h.len > head) {
-      P.recs[h.rec].ptr = h.ptr;
-      shadow_host_pages = true;
-    }
-  std::vector<uint64_t> managed_ids;
-  if (shadow_host_pages)
-    for (const AllocationRecord& rec : active)
-      if (rec.kind == AllocationKind::Managed) managed_ids.push_back(rec.id);
-  for (uint64_t id : managed_ids) ctx.managed_remote_access(id, true);
-  tr.mark("remote-access");
+  // host-resident pages never go through the SMs (no device mapping of them
+  // is needed, nothing migrates): long runs are skipped by every window copy,
+  // ring and shadow alike, and written by host threads during the stall
+  plan_host_runs(P, P.stream_len);
 
   // With the whole stream in the shadow, K1 copies every payload chunk to
   // its stream position right after hashing it: one HBM read of the state
@@ -970,17 +979,11 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   }
   check_cuda(cudaEventSynchronize(E.ev_s1), "snapshot sync");
   tr.mark("d2h-wait");
-  for (uint64_t id : managed_ids) ctx.managed_remote_access(id, false);
-  tr.mark("remote-access-off");
-  for (const HostPage& h : P.host_pages) P.recs[h.rec].ptr = 0;  // the plan's invariant
 
   // the app may run from here on: the shadow -> image D2H reads only HBM
   // that belongs to the engine
-  for (uint64_t c = 0; head + c < P.stream_len; c += DrainEngine::kCopyChunk)
-    check_cuda(cudaMemcpyAsync(img + s3 + head + c, E.d_shadow + c,
-                               std::min(DrainEngine::kCopyChunk, P.stream_len - head - c),
-                               cudaMemcpyDeviceToHost, E.s_copy),
-               "D2H shadow");
+  if (head < P.stream_len)
+    copy_window(P, run_i, head, P.stream_len, E.d_shadow, img + s3, true, E.s_copy);
   check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
   Q.active = true;
 }
@@ -995,6 +998,11 @@ void drain_finish(Session& session, DrainStats* stats) {
   check_cuda(cudaStreamWaitEvent(E.s_pack, E.ev_c1, 0), "wait");
   check_cuda(cudaEventRecord(E.ev_t1, E.s_pack), "event");
   check_cuda(cudaEventSynchronize(E.ev_t1), "drain sync");
+  uint64_t at = 0;
+  for (const auto& [off, len] : Q.stash_at) {
+    std::memcpy(img + P.s3 + off, Q.stash.data() + at, len);
+    at += len;
+  }
   // crc3 lies inside the stream (the windows carried zeros there)
   put_at<uint32_t>(img + P.s3 + P.len3, Q.crc3);
   put_at<uint32_t>(img + P.s3 + P.stream_len, Q.crc4);

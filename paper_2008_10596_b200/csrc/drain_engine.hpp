@@ -131,6 +131,10 @@ struct DrainEngine {
     uint32_t crc3 = 0, crc4 = 0;
     uint64_t windows = 0;    // ring windows (stats)
     double stall_ms = 0;
+    // host-resident pages of short runs in the shadow part, copied while the
+    // app was stopped; written into the image after the shadow D2H lands
+    std::vector<uint8_t> stash;
+    std::vector<std::pair<uint64_t, uint32_t>> stash_at;  // (stream_off, len)
   } pending;
 
   ImagePlan plan;

@@ -473,6 +473,8 @@ def _big_state(api):
     api.fill_synthetic(m, 9, workloads.DEVICE_SIDE)
     for off in range(MIB, 80 * MIB, 2 * MIB):
         api.page_read(m, off, MIB, workloads.HOST_SIDE)
+    for off in range(MIB // 2, 80 * MIB, 8 * MIB):  # short (64 KiB) host runs
+        api.page_read(m, off, 64 << 10, workloads.HOST_SIDE)
     return m
 
 
@@ -504,6 +506,25 @@ def test_async_drain_is_the_image_at_begin(eng, shadow_mib):
     rs, _ = eng.restart(img.tobytes())
     assert rs.checkpoint()[0] == want
     assert s.checkpoint()[0] != want  # the mutations are live
+
+
+@pytest.mark.parametrize("shadow_mib", [64, 512])
+def test_async_drain_with_managed_runs_matches_reference(eng, shadow_mib):
+    """The stall-reduced drain over long and short host-resident runs equals
+    the reference's image; host pages change right after begin."""
+    s = eng.Session(seed=6, arena_bytes=512 * MIB)
+    r = ref.RefSession(seed=6, arena_bytes=512 * MIB)
+    m = _big_state(s)
+    _big_state(r)
+    want = r.checkpoint()[0]
+    s.reserve_shadow(shadow_mib * MIB)
+    img = eng.Image()
+    s.checkpoint_begin(img)
+    s.page_write(m, MIB // 2, b"\x11" * 4096, workloads.HOST_SIDE)   # a short-run page
+    s.page_write(m, 3 * MIB, b"\x22" * 8192, workloads.HOST_SIDE)    # a long-run page
+    s.checkpoint_finish()
+    assert img.tobytes() == want
+    s.reserve_shadow(0)
 
 
 def test_async_drain_matches_reference_small(eng):
