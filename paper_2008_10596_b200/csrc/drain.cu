@@ -31,6 +31,8 @@
 #include <cstring>
 #include <map>
 #include <atomic>
+#include <climits>
+#include <exception>
 #include <mutex>
 #include <set>
 #include <thread>
@@ -643,6 +645,11 @@ uint64_t host_run_bytes(const ImagePlan& P) {
 void copy_window(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, uint8_t* buf,
                  uint8_t* stream, bool d2h, cudaStream_t st) {
   const auto& R = P.host_runs;
+  thread_local std::vector<void*> dsts, srcs;
+  thread_local std::vector<size_t> sizes;
+  dsts.clear();
+  srcs.clear();
+  sizes.clear();
   for (uint64_t a = off; a < end;) {
     while (run < R.size() && R[run].second <= a) ++run;
     uint64_t b = end;
@@ -655,12 +662,30 @@ void copy_window(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, ui
     }
     for (uint64_t c = a; c < b; c += DrainEngine::kCopyChunk) {
       const uint64_t n = std::min(DrainEngine::kCopyChunk, b - c);
-      check_cuda(d2h ? cudaMemcpyAsync(stream + c, buf + (c - off), n, cudaMemcpyDeviceToHost, st)
-                     : cudaMemcpyAsync(buf + (c - off), stream + c, n, cudaMemcpyHostToDevice, st),
-                 d2h ? "D2H" : "H2D");
+      dsts.push_back(d2h ? static_cast<void*>(stream + c) : static_cast<void*>(buf + (c - off)));
+      srcs.push_back(d2h ? static_cast<void*>(buf + (c - off)) : static_cast<void*>(stream + c));
+      sizes.push_back(n);
     }
     a = b;
   }
+  static const int batch_env = [] {
+    const char* e = std::getenv("CRAC_COPY_BATCH");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (sizes.size() > 1 && (batch_env == 1 || (batch_env < 0 && !R.empty()))) {
+    // one call for the window's pieces (host runs cut C3 windows into ~32)
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t attr_idx = 0, fail = 0;
+    if (cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &attr,
+                             &attr_idx, 1, &fail, st) == cudaSuccess)
+      return;
+    cudaGetLastError();  // batch API unavailable: issue the pieces one by one
+  }
+  for (size_t i = 0; i < sizes.size(); ++i)
+    check_cuda(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i],
+                               d2h ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st),
+               d2h ? "D2H" : "H2D");
 }
 
 // Host-resident managed pages of a drain.  Each host thread takes a block of
@@ -669,7 +694,8 @@ void copy_window(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, ui
 // D2H of the window holding its last byte has landed (the windows carry
 // zeros there; windows land in order on s_copy).  The CPU reads pages that
 // live on its side: nothing migrates and no device mapping is needed.
-void host_pages_drain(DrainEngine& E, const ImagePlan& P, uint8_t* stream, uint64_t head) {
+void host_pages_drain(DrainEngine& E, const ImagePlan& P, uint8_t* stream, uint64_t head,
+                      const std::atomic<int64_t>& recorded) {
   const uint64_t n = P.host_pages.size();
   if (!n) return;
   // short-run pages of the shadow part: stashed now (the app may change them
@@ -711,6 +737,9 @@ void host_pages_drain(DrainEngine& E, const ImagePlan& P, uint8_t* stream, uint6
         }
         const int64_t w = int64_t((h.stream_off + h.len - 1) / W);
         if (w > landed) {
+          // the window loop runs beside this pass: an event not yet recorded
+          // would read as complete
+          while (recorded.load(std::memory_order_acquire) < w) std::this_thread::yield();
           if (cudaEventSynchronize(E.ev_land[w]) != cudaSuccess) failed = 1;
           landed = w;
         }
@@ -928,6 +957,25 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   const bool land_events = !P.host_pages.empty();
   if (land_events) E.ensure_land_events(windows);
   check_cuda(cudaEventRecord(E.ev_c0, E.s_pack), "event");
+  // host-resident pages: hashed (all) and copied by host threads beside the
+  // window loop (long runs at once; short ring-part runs after their window)
+  std::atomic<int64_t> recorded{-1};
+  std::exception_ptr host_err;
+  std::thread host_pass([&] {
+    try {
+      host_pages_drain(E, P, img + s3, head, recorded);
+    } catch (...) {
+      host_err = std::current_exception();
+    }
+  });
+  struct Joiner {
+    std::thread& t;
+    std::atomic<int64_t>& r;
+    ~Joiner() {
+      r.store(INT64_MAX);  // unblock waiters if the loop throws
+      if (t.joinable()) t.join();
+    }
+  } join_host{host_pass, recorded};
   size_t run_i = 0;
   for (uint64_t w = 0; w < windows; ++w) {
     const int slot = int(w % DrainEngine::kSlots);
@@ -948,11 +996,12 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
     copy_window(P, run_i, off, off + len, buf, img + s3, true, E.s_copy);
     check_cuda(cudaEventRecord(E.ev_free[slot], E.s_copy), "event");
     if (land_events) check_cuda(cudaEventRecord(E.ev_land[w], E.s_copy), "event");
+    recorded.store(int64_t(w), std::memory_order_release);
   }
   tr.mark("enqueue");
-  // host-resident pages: hashed (all) and copied (ring part) by host threads
-  // while the windows drain; then K4 folds every CRC
-  host_pages_drain(E, P, img + s3, head);
+  host_pass.join();
+  if (host_err) std::rethrow_exception(host_err);
+  // then K4 folds every CRC
   if (!P.host_pages.empty())
     check_cuda(cudaMemcpyAsync(E.d_page_crc.ptr + P.n_dev_pages, E.h_host_crc.ptr,
                                P.host_pages.size() * 4, cudaMemcpyHostToDevice, E.s_hash),

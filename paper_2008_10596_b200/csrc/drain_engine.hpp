@@ -14,6 +14,8 @@
 
 #include <cstdint>
 #include <memory>
+#include <new>
+#include <utility>
 #include <vector>
 
 #include "crac_gpu.h"
@@ -48,6 +50,35 @@ struct HostArray {  // pinned
   void release();
 };
 
+// Page-locked storage for big host tables that are uploaded every drain (the
+// record table: 268 MB for C3's 4 M pages), so the upload is a real async DMA
+// rather than a staged pageable copy; elements are default-initialised (a
+// resize does not zero memory the plan overwrites anyway).
+template <typename T>
+struct PinnedAlloc {
+  using value_type = T;
+  PinnedAlloc() = default;
+  template <typename U>
+  PinnedAlloc(const PinnedAlloc<U>&) {}
+  T* allocate(size_t n) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, n * sizeof(T), cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      throw std::bad_alloc();
+    }
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, size_t) { cudaFreeHost(p); }
+  template <typename U, typename... A>
+  void construct(U* p, A&&... a) {
+    if constexpr (sizeof...(A) == 0)
+      ::new (static_cast<void*>(p)) U;
+    else
+      ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+  bool operator==(const PinnedAlloc&) const { return true; }
+};
+
 // Layout of the last image this session drained (enables incremental drains).
 // A host-resident managed page: its content is copied by host threads
 // between the managed allocation and the image (never crosses PCIe).
@@ -67,7 +98,7 @@ struct ImagePlan {
   uint64_t s3 = 0;          // file offset of the ALLOC_PAYLOADS payload (= stream start)
   uint64_t len3 = 0, len4 = 0;
   uint64_t stream_len = 0;  // len3 + 20 + len4
-  std::vector<crac_record_t> recs;
+  std::vector<crac_record_t, PinnedAlloc<crac_record_t>> recs;
   std::vector<uint32_t> tile_rec;
   std::vector<crac_span_t> pay_spans, page_spans;  // page_spans: device-resident runs
   std::vector<uint64_t> pay_first, page_first;
