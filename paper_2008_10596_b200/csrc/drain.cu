@@ -837,16 +837,21 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
 
   const SnapshotMeta meta{ctx.seed(), ctx.arena_bytes(), kEngineVersion};
   const std::vector<CallLogEntry> log = session.log().snapshot();
+  tr.mark("log-snapshot");
   const std::vector<AllocationRecord> active = active_set(log);
+  tr.mark("active-set");
   const std::vector<uint8_t> sec1 = meta_bytes(meta);
   const std::vector<uint8_t> sec2 = log_bytes(log);
   const std::vector<uint8_t> sec5 = streams_bytes(ctx.live_stream_ids());
   const std::vector<uint8_t>& sec6 = session.app_state();
   const std::vector<uint8_t> sec7 = registry_bytes(ctx.registered_binaries());
+  tr.mark("sections");
 
   std::vector<std::vector<uint8_t>> flags;
   ImagePlan& P = E.plan;
-  build_plan(live_items(ctx, active, flags, true), P);
+  std::vector<BulkItem> items = live_items(ctx, active, flags, true);
+  tr.mark("live-items");
+  build_plan(items, P);
   P.log_len = log.size();
   tr.mark("plan");
 
@@ -1209,59 +1214,33 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     if (run_hi) ctx.premap(run_lo, run_hi - run_lo);
   }
   tr.mark("premap");
-  ctx.begin_replay(std::move(live));
-  try {
-    replay_log(ctx, p.log, &binaries);
-  } catch (...) {
-    ctx.end_replay();
-    throw;
-  }
-  ctx.end_replay();
-  tr.mark("replay");
-  if (ctx.live_stream_ids() != p.streams)
-    raise(Errc::ReplayDivergence, "live streams after replay do not match the snapshot");
 
-  // destinations of every framed record, in image order
-  std::vector<BulkItem> items;
-  size_t mi = 0;
-  for (const AllocationRecord& rec : p.facts.active) {
-    const auto replayed = ctx.find_record(rec.id);
-    if (!replayed || replayed->size != rec.size || replayed->kind != rec.kind)
-      raise(Errc::ReplayDivergence,
-            "record " + std::to_string(rec.id) + " does not match a replayed allocation");
-    BulkItem it{rec.id, rec.kind, rec.size, ctx.backing_ptr(rec.id), nullptr};
-    if (rec.kind == AllocationKind::Managed) it.flags = &p.managed[mi++].flags;
-    items.push_back(it);
-  }
-  tr.mark("items");
+  // With the arena at its logged VA and only Device allocations live, every
+  // destination is the logged address itself: the H2D / scatter / verify
+  // pipeline starts before the replay and the replay (host bookkeeping only,
+  // the extents are pre-mapped) runs beside it, then vouches for the
+  // addresses.  Otherwise the data path waits for the replayed backings.
+  const bool early = ctx.fixed_va() && !p.facts.active.empty() &&
+                     std::all_of(p.facts.active.begin(), p.facts.active.end(),
+                                 [](const AllocationRecord& r) {
+                                   return r.kind == AllocationKind::Device;
+                                 });
   ImagePlan& P = E.plan;
-  build_plan(items, P);
-  plan_host_runs(P, P.stream_len);
-  P.log_len = p.log.size();
   const uint64_t s3 = p.sec[2].payload_off;
-  if (P.len3 != p.sec[2].length || P.len4 != p.sec[3].length ||
-      s3 + P.stream_len != p.sec[3].payload_off + p.sec[3].length)
-    raise(Errc::ImageCorrupt, "bulk sections do not match the log's active set");
-  tr.mark("plan");
-
-  // managed pages land where they were: device-resident ones are first
-  // touched by the scatter kernel (and verified by K1), host-resident ones
-  // are written and hashed by the host threads below, so nothing migrates
-  // and no prefetch or device mapping is needed to restore residence
-  mi = 0;
-  for (const AllocationRecord& rec : p.facts.active)
-    if (rec.kind == AllocationKind::Managed) ctx.set_managed_flags(rec.id, p.managed[mi++].flags);
-  std::thread host_fill([&] { host_pages_refill(E, P, raw.data() + s3); });
-  struct Joiner {
-    std::thread& t;
-    ~Joiner() {
-      if (t.joinable()) t.join();
-    }
-  } joiner{host_fill};
-  tr.mark("place");
-
+  auto plan = [&](const std::vector<BulkItem>& items) {
+    build_plan(items, P);
+    plan_host_runs(P, P.stream_len);
+    P.log_len = p.log.size();
+    if (P.len3 != p.sec[2].length || P.len4 != p.sec[3].length ||
+        s3 + P.stream_len != p.sec[3].payload_off + p.sec[3].length)
+      raise(Errc::ImageCorrupt, "bulk sections do not match the log's active set");
+    tr.mark("plan");
+  };
   uint64_t windows = 0, verifies = 0;
-  if (P.stream_len > 20) {
+  // enqueues H2D windows -> scatter -> K1 verify (payloads as their regions
+  // complete, then the device-resident pages); nothing here waits
+  auto enqueue_data_path = [&] {
+    if (P.stream_len <= 20) return;
     upload_plan(E, P, E.s_pack);
     check_cuda(cudaEventRecord(E.ev_ready[0], E.s_pack), "event");
     check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_ready[0], 0), "wait");
@@ -1309,7 +1288,6 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       }
     }
     check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
-    tr.mark("windows");
     if (P.n_dev_pages) {
       if (stats) {
         E.ensure_verify_events(verifies + 1);
@@ -1319,6 +1297,73 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       if (stats) cudaEventRecord(E.ev_v1[verifies], E.s_pack);
       ++verifies;
     }
+    tr.mark("windows");
+  };
+  // the engine streams must be idle before an error unwinds the session
+  // (the arena they write into is unmapped with it)
+  auto quiet = [&] {
+    cudaStreamSynchronize(E.s_copy);
+    cudaStreamSynchronize(E.s_pack);
+  };
+
+  if (early) {
+    std::vector<BulkItem> items;
+    for (const AllocationRecord& rec : p.facts.active)
+      items.push_back(BulkItem{rec.id, rec.kind, rec.size, rec.address, nullptr});
+    plan(items);
+    enqueue_data_path();
+  }
+  ctx.begin_replay(std::move(live));
+  try {
+    replay_log(ctx, p.log, &binaries);
+  } catch (...) {
+    ctx.end_replay();
+    quiet();
+    throw;
+  }
+  ctx.end_replay();
+  tr.mark("replay");
+  if (ctx.live_stream_ids() != p.streams) {
+    quiet();
+    raise(Errc::ReplayDivergence, "live streams after replay do not match the snapshot");
+  }
+
+  // destinations of every framed record, in image order
+  std::vector<BulkItem> items;
+  size_t mi = 0;
+  for (const AllocationRecord& rec : p.facts.active) {
+    const auto replayed = ctx.find_record(rec.id);
+    if (!replayed || replayed->size != rec.size || replayed->kind != rec.kind ||
+        (early && ctx.backing_ptr(rec.id) != rec.address)) {
+      quiet();
+      raise(Errc::ReplayDivergence,
+            "record " + std::to_string(rec.id) + " does not match a replayed allocation");
+    }
+    BulkItem it{rec.id, rec.kind, rec.size, ctx.backing_ptr(rec.id), nullptr};
+    if (rec.kind == AllocationKind::Managed) it.flags = &p.managed[mi++].flags;
+    items.push_back(it);
+  }
+  tr.mark("items");
+  if (!early) plan(items);
+
+  // managed pages land where they were: device-resident ones are first
+  // touched by the scatter kernel (and verified by K1), host-resident ones
+  // are written and hashed by the host threads below, so nothing migrates
+  // and no prefetch or device mapping is needed to restore residence
+  mi = 0;
+  for (const AllocationRecord& rec : p.facts.active)
+    if (rec.kind == AllocationKind::Managed) ctx.set_managed_flags(rec.id, p.managed[mi++].flags);
+  std::thread host_fill([&] { host_pages_refill(E, P, raw.data() + s3); });
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } joiner{host_fill};
+  tr.mark("place");
+
+  if (!early) enqueue_data_path();
+  if (P.stream_len > 20) {
     host_fill.join();  // the host-resident pages' CRCs
     tr.mark("host-fill-join");
     if (!P.host_pages.empty())

@@ -237,6 +237,38 @@ def test_tampered_log_address_is_replay_divergence(eng, golden):
     assert e.value.errc == e2.value.errc
 
 
+@pytest.mark.parametrize("which", ["live_last", "live_first", "freed"])
+def test_tampered_device_only_log_while_data_path_runs(eng, which):
+    """Device-only images at the fixed VA refill before the replay has run
+    (the destinations are the logged addresses); a log whose replay diverges
+    must still be refused with the reference's error, with the engine
+    streams drained before the session unwinds, and the next restart works."""
+    s = eng.Session(seed=5, arena_bytes=1 << 30)
+    ids = workloads.build_regions(s, 12, lambda k: (3 << 20) + 4096 * k + 5 * k, seed=5)
+    s.free(ids[3])
+    s.free(ids[7])
+    i, _ = s.alloc(workloads.DEVICE, 5000)
+    s.fill_synthetic(i, 5)
+    good, _ = s.checkpoint()
+    snap = io.decode_image(good)
+    allocs = [k for k, e in enumerate(snap.log) if e[1] == 1]
+    freed = {e[4] for e in snap.log if e[1] == 2}
+    live = [k for k in allocs if snap.log[k][4] not in freed]
+    k = {"live_last": live[-1], "live_first": live[0],
+         "freed": [a for a in allocs if snap.log[a][4] in freed][0]}[which]
+    seq, op, kind, size, ident, addr = snap.log[k]
+    snap.log[k] = (seq, op, kind, size, ident, addr + 256)
+    bad = io.encode_image(snap)
+    with pytest.raises(eng.CracError) as e:
+        eng.restart(bad)
+    with pytest.raises(ref.RefError) as e2:
+        ref.ref_restart(bad)
+    assert e.value.errc in ("ReplayDivergence", "ImageCorrupt")
+    assert e.value.errc == e2.value.errc
+    r, _ = eng.restart(good)
+    assert r.checkpoint()[0] == good
+
+
 def test_unknown_kernel_body_refused(eng, golden):
     _, images = golden
     # "scale"/"probe" and the random gen_k* kernels are not in the standard catalog
