@@ -123,6 +123,10 @@ void checkpoint_to_file(Session& session, const std::filesystem::path& path, boo
 std::map<uint64_t, uint64_t> replay_log(
     DeviceContext& ctx, std::span<const CallLogEntry> log,
     const std::map<uint64_t, std::vector<KernelDescriptor>>* binaries = nullptr);
+// replay_log without building the returned map (placed_out may be null).
+void replay_log_into(DeviceContext& ctx, std::span<const CallLogEntry> log,
+                     const std::map<uint64_t, std::vector<KernelDescriptor>>* binaries,
+                     std::map<uint64_t, uint64_t>* placed_out);
 Session restart(const Snapshot& snapshot, const KernelCatalog& catalog,
                 TableMode mode = TableMode::Direct,
                 std::chrono::milliseconds quiesce_timeout = std::chrono::milliseconds{30000});

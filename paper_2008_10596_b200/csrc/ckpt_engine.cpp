@@ -61,6 +61,14 @@ std::map<uint64_t, uint64_t> replay_log(
     DeviceContext& ctx, std::span<const CallLogEntry> log,
     const std::map<uint64_t, std::vector<KernelDescriptor>>* binaries) {
   std::map<uint64_t, uint64_t> placed;
+  replay_log_into(ctx, log, binaries, &placed);
+  return placed;
+}
+
+// The restart path does not need the seq -> address map (C2: 28 k inserts).
+void replay_log_into(DeviceContext& ctx, std::span<const CallLogEntry> log,
+                     const std::map<uint64_t, std::vector<KernelDescriptor>>* binaries,
+                     std::map<uint64_t, uint64_t>* placed_out) {
   auto diverged = [](const CallLogEntry& e, const std::string& what) {
     raise(Errc::ReplayDivergence, "seq " + std::to_string(e.seq) + ": " + what);
   };
@@ -72,7 +80,7 @@ std::map<uint64_t, uint64_t> replay_log(
           diverged(e, "id " + std::to_string(rec.id) + " != logged " + std::to_string(e.id));
         if (rec.address != e.address)
           diverged(e, "address mismatch for allocation " + std::to_string(e.id));
-        placed.emplace_hint(placed.end(), e.seq, rec.address);  // seq ascends
+        if (placed_out) placed_out->emplace_hint(placed_out->end(), e.seq, rec.address);  // seq ascends
         break;
       }
       case LogOp::Free: ctx.free(e.id); break;
@@ -92,7 +100,6 @@ std::map<uint64_t, uint64_t> replay_log(
       case LogOp::UnregisterBinary: ctx.unregister_fat_binary(e.id); break;
     }
   }
-  return placed;
 }
 
 // ref: ckpt_engine.cpp:120-171, via the GPU refill.

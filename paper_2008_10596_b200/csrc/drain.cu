@@ -1315,7 +1315,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   }
   ctx.begin_replay(std::move(live));
   try {
-    replay_log(ctx, p.log, &binaries);
+    replay_log_into(ctx, p.log, &binaries, nullptr);
   } catch (...) {
     ctx.end_replay();
     quiet();
