@@ -833,8 +833,13 @@ std::vector<BulkItem> live_items(DeviceContext& ctx, const std::vector<Allocatio
   std::vector<BulkItem> items;
   flags.clear();
   flags.reserve(active.size());
-  for (const AllocationRecord& rec : active) {
-    BulkItem it{rec.id, rec.kind, rec.size, ctx.backing_ptr(rec.id), nullptr};
+  items.reserve(active.size());
+  std::vector<uint64_t> ptrs;
+  if (!ctx.match_records(active, ptrs))
+    raise(Errc::InvalidArgument, "the log's active set does not match the live allocations");
+  for (size_t k = 0; k < active.size(); ++k) {
+    const AllocationRecord& rec = active[k];
+    BulkItem it{rec.id, rec.kind, rec.size, ptrs[k], nullptr};
     if (with_flags && rec.kind == AllocationKind::Managed) {
       const auto pages = ctx.managed_pages(rec.id);
       std::vector<uint8_t> f(pages.size());
@@ -1368,16 +1373,19 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
 
   // destinations of every framed record, in image order
   std::vector<BulkItem> items;
+  std::vector<uint64_t> ptrs;
+  bool match = ctx.match_records(p.facts.active, ptrs);
+  for (size_t k = 0; match && early && k < ptrs.size(); ++k)
+    match = ptrs[k] == p.facts.active[k].address;
+  if (!match) {
+    quiet();
+    raise(Errc::ReplayDivergence, "the active set does not match the replayed allocations");
+  }
   size_t mi = 0;
-  for (const AllocationRecord& rec : p.facts.active) {
-    const auto replayed = ctx.find_record(rec.id);
-    if (!replayed || replayed->size != rec.size || replayed->kind != rec.kind ||
-        (early && ctx.backing_ptr(rec.id) != rec.address)) {
-      quiet();
-      raise(Errc::ReplayDivergence,
-            "record " + std::to_string(rec.id) + " does not match a replayed allocation");
-    }
-    BulkItem it{rec.id, rec.kind, rec.size, ctx.backing_ptr(rec.id), nullptr};
+  items.reserve(ptrs.size());
+  for (size_t k = 0; k < ptrs.size(); ++k) {
+    const AllocationRecord& rec = p.facts.active[k];
+    BulkItem it{rec.id, rec.kind, rec.size, ptrs[k], nullptr};
     if (rec.kind == AllocationKind::Managed) it.flags = &p.managed[mi++].flags;
     items.push_back(it);
   }
