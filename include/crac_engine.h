@@ -87,6 +87,10 @@ int crac_checkpoint_incremental(crac_session_t* s, crac_image_t* img, crac_stats
  * instant of begin.  crac_reserve_shadow(s, 0) releases the reservation;
  * OutOfArena (1 + 8) if the HBM is not available. */
 int crac_reserve_shadow(crac_session_t* s, uint64_t bytes);
+/* The shadow in another GPU's HBM (SURVEY §8f.3 buddy copy): reachable by
+ * peer access (InvalidArgument otherwise); `device` = this session's GPU is
+ * crac_reserve_shadow. */
+int crac_reserve_shadow_on(crac_session_t* s, uint64_t bytes, int device);
 int crac_checkpoint_begin(crac_session_t* s, crac_image_t* img, crac_stats_t* stats);
 int crac_checkpoint_finish(crac_session_t* s, crac_stats_t* stats);
 /* checkpoint(Session&) -> Snapshot -> encode_image, into a malloc'd buffer

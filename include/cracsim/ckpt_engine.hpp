@@ -155,7 +155,10 @@ void checkpoint_incremental(Session& session, PinnedImage& image, DrainStats* st
 // and completes `out`: the bytes equal checkpoint_image's at the instant of
 // checkpoint_begin, whatever the app does in between.  With no shadow this is
 // checkpoint_image.  Any other drain first finishes a pending one.
-void reserve_shadow(Session& session, uint64_t bytes);
+// `device` >= 0 places the shadow in that GPU's HBM (a buddy GPU reachable by
+// peer access): the snapshot crosses NVLink during the stall and
+// the buddy's copy engine drains it over the buddy's PCIe link afterwards.
+void reserve_shadow(Session& session, uint64_t bytes, int device = -1);
 void checkpoint_begin(Session& session, PinnedImage& out, DrainStats* stats = nullptr);
 void checkpoint_finish(Session& session, DrainStats* stats = nullptr);
 // K1 over every live allocation (hash-only timing; no drain).

@@ -255,6 +255,10 @@ int crac_reserve_shadow(crac_session_t* s, uint64_t bytes) {
   return guard([&] { reserve_shadow(s->s, bytes); });
 }
 
+int crac_reserve_shadow_on(crac_session_t* s, uint64_t bytes, int device) {
+  return guard([&] { reserve_shadow(s->s, bytes, device); });
+}
+
 int crac_checkpoint_begin(crac_session_t* s, crac_image_t* img, crac_stats_t* stats) {
   return guard([&] {
     DrainStats d;

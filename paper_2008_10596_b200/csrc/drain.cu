@@ -140,7 +140,9 @@ DrainEngine::~DrainEngine() {
   for (cudaEvent_t e : ev_v1) cudaEventDestroy(e);
   for (cudaEvent_t e : {ev_t0, ev_t1, ev_h0, ev_h1, ev_c0, ev_c1}) cudaEventDestroy(e);
   cudaFree(d_ring);
-  if (d_shadow) cudaFree(d_shadow);
+  free_shadow(*this);
+  if (s_peer) cudaStreamDestroy(s_peer);
+  if (ev_peer) cudaEventDestroy(ev_peer);
   cudaEventDestroy(ev_s1);
   for (cudaEvent_t e : ev_join) cudaEventDestroy(e);
   cudaStreamDestroy(s_shadow);
@@ -217,6 +219,23 @@ std::unique_ptr<DrainEngine> acquire_engine(int device) {
   return std::make_unique<DrainEngine>(device);
 }
 
+// Frees the shadow on the device that holds it.
+void free_shadow(DrainEngine& E) {
+  if (E.d_shadow) {
+    if (E.shadow_device >= 0) {
+      cudaStreamSynchronize(E.s_peer);
+      cudaSetDevice(E.shadow_device);
+      cudaFree(E.d_shadow);
+      cudaSetDevice(E.device);
+    } else {
+      cudaFree(E.d_shadow);
+    }
+  }
+  E.d_shadow = nullptr;
+  E.shadow_cap = 0;
+  E.shadow_device = -1;
+}
+
 void release_engine(std::unique_ptr<DrainEngine> e) {
   if (!e) return;
   if (cudaStreamSynchronize(e->s_pack) != cudaSuccess ||
@@ -225,9 +244,7 @@ void release_engine(std::unique_ptr<DrainEngine> e) {
       cudaStreamSynchronize(e->s_shadow) != cudaSuccess)
     return;  // a broken engine is dropped (and leaked), never pooled
   e->pending = DrainEngine::Pending{};  // an unfinished async drain is abandoned
-  if (e->d_shadow) cudaFree(e->d_shadow);  // the shadow belongs to its session
-  e->d_shadow = nullptr;
-  e->shadow_cap = 0;
+  free_shadow(*e);  // the shadow belongs to its session
   e->plan.valid = false;  // keep the vectors' capacity for the next session
   e->plan.image_ptr = 0;
   e->prev_valid = false;
@@ -1079,8 +1096,16 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
 
   // the app may run from here on: the shadow -> image D2H reads only HBM
   // that belongs to the engine
-  if (head < P.stream_len)
-    copy_window(P, run_i, head, P.stream_len, E.d_shadow, img + s3, true, E.s_copy);
+  if (head < P.stream_len) {
+    if (E.shadow_device >= 0) {  // the buddy GPU drains its copy over its own link
+      check_cuda(cudaStreamWaitEvent(E.s_peer, E.ev_s1, 0), "wait");
+      copy_window(P, run_i, head, P.stream_len, E.d_shadow, img + s3, true, E.s_peer);
+      check_cuda(cudaEventRecord(E.ev_peer, E.s_peer), "event");
+      check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_peer, 0), "wait");
+    } else {
+      copy_window(P, run_i, head, P.stream_len, E.d_shadow, img + s3, true, E.s_copy);
+    }
+  }
   check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
   Q.active = true;
 }
@@ -1144,23 +1169,43 @@ void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
   drain_finish(session, stats);
 }
 
-void reserve_shadow(Session& session, uint64_t bytes) {
+void reserve_shadow(Session& session, uint64_t bytes, int device) {
   finish_pending(session);
   DrainEngine& E = session.drain_engine();
+  const int own = E.device;
+  if (device < 0) device = own;
   bytes = (bytes + DrainEngine::kWindow - 1) / DrainEngine::kWindow * DrainEngine::kWindow;
-  if (bytes == E.shadow_cap) return;
-  if (E.d_shadow) check_cuda(cudaFree(E.d_shadow), "free shadow");
-  E.d_shadow = nullptr;
-  E.shadow_cap = 0;
+  if (bytes == E.shadow_cap && device == (E.shadow_device < 0 ? own : E.shadow_device)) return;
+  if (bytes && device != own) {
+    int n = 0, can = 0;
+    check_cuda(cudaGetDeviceCount(&n), "device count");
+    if (device >= n) raise(Errc::InvalidArgument, "reserve_shadow: no device " + std::to_string(device));
+    check_cuda(cudaDeviceCanAccessPeer(&can, own, device), "peer query");
+    if (!can)
+      raise(Errc::InvalidArgument, "reserve_shadow: device " + std::to_string(device) +
+                                       " is not reachable from device " + std::to_string(own) +
+                                       " by peer access");
+    const cudaError_t pe = cudaDeviceEnablePeerAccess(device, 0);
+    if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) check_cuda(pe, "peer access");
+    cudaGetLastError();
+  }
+  free_shadow(E);
   if (!bytes) return;
   // +64: the pack of the last window writes whole 16-byte words
+  check_cuda(cudaSetDevice(device), "set device");
   const cudaError_t e = cudaMalloc(&E.d_shadow, bytes + 64);
+  if (e == cudaSuccess && device != own && !E.s_peer) {
+    check_cuda(cudaStreamCreateWithFlags(&E.s_peer, cudaStreamNonBlocking), "peer stream");
+    check_cuda(cudaEventCreateWithFlags(&E.ev_peer, cudaEventDisableTiming), "peer event");
+  }
+  check_cuda(cudaSetDevice(own), "set device");
   if (e != cudaSuccess) {
     cudaGetLastError();
     E.d_shadow = nullptr;
     raise(Errc::OutOfArena, "reserve_shadow: " + std::to_string(bytes) + " bytes of HBM unavailable");
   }
   E.shadow_cap = bytes;
+  E.shadow_device = device == own ? -1 : device;
 }
 
 void checkpoint_begin(Session& session, PinnedImage& out, DrainStats* stats) {

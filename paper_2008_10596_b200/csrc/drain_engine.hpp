@@ -155,6 +155,12 @@ struct DrainEngine {
   cudaEvent_t ev_s1 = nullptr, ev_join[3] = {};
   uint8_t* d_shadow = nullptr;
   uint64_t shadow_cap = 0;
+  // Buddy shadow: the shadow may live in a peer GPU's HBM,
+  // written over NVLink by this GPU's kernels (peer access) and drained to
+  // the host by the peer's own copy engine on the peer's PCIe link.
+  int shadow_device = -1;           // -1: this device
+  cudaStream_t s_peer = nullptr;    // on shadow_device
+  cudaEvent_t ev_peer = nullptr;    // on shadow_device: the shadow D2H is done
   struct Pending {
     bool active = false;
     PinnedImage* out = nullptr;
@@ -180,6 +186,9 @@ struct DrainEngine {
   void ensure_verify_events(size_t n);
   void ensure_land_events(size_t n);
 };
+
+// Frees the (possibly buddy-GPU) shadow of an engine.
+void free_shadow(DrainEngine& E);
 
 // Process-wide engine pool (Session construction / destruction).
 std::unique_ptr<DrainEngine> acquire_engine(int device);

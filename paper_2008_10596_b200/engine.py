@@ -95,6 +95,7 @@ _SIGS = {
     "crac_checkpoint_finish": (C.c_int, [_P, C.POINTER(Stats)]),
     "crac_restart": (C.c_int, [_P, _U64, C.c_int, C.POINTER(_P), C.POINTER(Stats)]),
     "crac_decode_check": (C.c_int, [_P, _U64]),
+    "crac_reserve_shadow_on": (C.c_int, [_P, _U64, C.c_int]),
     "crac_crc32_host": (C.c_uint32, [_P, _U64, _U32]),
     "crac_stream_handle": (C.c_int, [_P, _U64, C.POINTER(_P)]),
     "crac_live_streams": (C.c_int, [_P, _U64, _PU64, _PU64]),
@@ -332,9 +333,13 @@ class Session:
                                              C.byref(st), C.byref(io)))
         return st.as_dict(), io.as_dict()
 
-    def reserve_shadow(self, nbytes: int) -> None:
-        """HBM the stall-reduced drain may stage the stream in (0 releases it)."""
-        _check(lib().crac_reserve_shadow(self._h, nbytes))
+    def reserve_shadow(self, nbytes: int, device: Optional[int] = None) -> None:
+        """HBM the stall-reduced drain may stage the stream in (0 releases it);
+        `device` puts it on a buddy GPU reachable by peer access (§8f.3)."""
+        if device is None:
+            _check(lib().crac_reserve_shadow(self._h, nbytes))
+        else:
+            _check(lib().crac_reserve_shadow_on(self._h, nbytes, device))
 
     def checkpoint_begin(self, image: Image) -> dict:
         """Quiesce, snapshot into the shadow, resume; the D2H keeps running."""

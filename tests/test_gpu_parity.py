@@ -559,6 +559,34 @@ def test_async_drain_with_managed_runs_matches_reference(eng, shadow_mib):
     s.reserve_shadow(0)
 
 
+def test_buddy_shadow_placement(eng):
+    """reserve_shadow on a device: this GPU's own ordinal is
+    the ordinary shadow; an ordinal with no peer route is refused with
+    InvalidArgument and leaves the session able to drain."""
+    import torch
+    s = eng.Session(seed=2, arena_bytes=1 << 22)
+    r = ref.RefSession(seed=2, arena_bytes=1 << 22)
+    for api in (s, r):
+        workloads.drive_small(api, seed=6)
+    want = r.checkpoint()[0]
+    s.reserve_shadow(64 * MIB, device=0)
+    img = eng.Image()
+    s.checkpoint_begin(img)
+    s.checkpoint_finish()
+    assert img.tobytes() == want
+    n = torch.cuda.device_count()
+    with pytest.raises(eng.CracError) as e:
+        s.reserve_shadow(64 * MIB, device=n + 3)
+    assert e.value.errc == "InvalidArgument"
+    assert s.checkpoint()[0] == want
+    if n > 1:  # a real buddy: the snapshot crosses NVLink
+        s.reserve_shadow(64 * MIB, device=1)
+        s.checkpoint_begin(img)
+        s.checkpoint_finish()
+        assert img.tobytes() == want
+    s.reserve_shadow(0)
+
+
 def test_async_drain_matches_reference_small(eng):
     s = eng.Session(seed=2, arena_bytes=1 << 22)
     r = ref.RefSession(seed=2, arena_bytes=1 << 22)
