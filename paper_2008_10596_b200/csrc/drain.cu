@@ -459,6 +459,7 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
   P.pay_first.assign(1, 0);
   P.page_first.assign(1, 0);
   P.pay_rec_off.clear();
+  P.pay_kind.clear();
   P.log_sizes.clear();
   {  // one allocation for the whole record table
     uint64_t n = 1;
@@ -487,6 +488,7 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
     P.pay_first.push_back(P.pay_first.back() +
                           (it.size + DrainEngine::kChunk - 1) / DrainEngine::kChunk);
     P.pay_rec_off.push_back(pos + 16);
+    P.pay_kind.push_back(uint8_t(it.kind));
     pos += 16 + it.size;
   }
   P.len3 = pos;
@@ -686,6 +688,90 @@ void plan_host_runs(ImagePlan& P, uint64_t limit) {
     for (size_t k = i; k < j; ++k) P.host_pages[k].own_frame = skip;
     i = j;
   }
+  P.direct_runs.clear();
+  P.skip_runs = P.host_runs;
+}
+
+// Direct runs: the interior of every Device payload of at least
+// kDirectMinTiles + 2 tiles, cut to whole stream tiles 64 bytes clear of the
+// payload's ends, wholly below `limit`.  The copy engines move them straight
+// between the allocation and the image (a D2H from a misaligned device
+// address into a 4 KiB-aligned host address runs at full PCIe speed,
+// profiles/r01d/direct_copy2.txt); the pack / scatter kernels only handle
+// the tiles around them (frames, payload edges, small payloads, pages).
+// Host runs and direct runs are disjoint (UVM_PAGES vs ALLOC_PAYLOADS).
+constexpr uint64_t kTile = CRAC_TILE_BYTES;
+constexpr uint64_t kDirectMinTiles = 4;
+
+void plan_direct_runs(ImagePlan& P, uint64_t limit) {
+  P.direct_runs.clear();
+  static const bool enabled = [] {
+    const char* e = std::getenv("CRAC_DIRECT");
+    return !(e && !std::strcmp(e, "0"));
+  }();
+  if (enabled)
+    for (size_t k = 0; k < P.pay_spans.size(); ++k) {
+      if (P.pay_kind[k] != uint8_t(AllocationKind::Device)) continue;
+      const uint64_t a = P.pay_rec_off[k], b = std::min(a + P.pay_spans[k].len, limit);
+      if (b < a + 64 + (kDirectMinTiles + 2) * kTile) continue;
+      const uint64_t lo = (a + 64 + kTile - 1) / kTile * kTile, hi = (b - 64) / kTile * kTile;
+      if (hi < lo + kDirectMinTiles * kTile) continue;
+      P.direct_runs.push_back(ImagePlan::DirectRun{lo, hi, P.pay_spans[k].ptr + (lo - a)});
+    }
+  P.skip_runs.clear();
+  P.skip_runs.reserve(P.host_runs.size() + P.direct_runs.size());
+  for (const auto& d : P.direct_runs) P.skip_runs.emplace_back(d.lo, d.hi);
+  P.skip_runs.insert(P.skip_runs.end(), P.host_runs.begin(), P.host_runs.end());
+  std::sort(P.skip_runs.begin(), P.skip_runs.end());
+}
+
+uint64_t direct_run_bytes(const ImagePlan& P) {
+  uint64_t b = 0;
+  for (const auto& d : P.direct_runs) b += d.hi - d.lo;
+  return b;
+}
+
+// The kernel (pack / scatter) ranges of window [off, end): the window minus
+// its direct runs, each starting on a tile boundary.  `run` walks
+// P.direct_runs across calls.
+void kernel_ranges(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end,
+                   std::vector<std::pair<uint64_t, uint64_t>>& out) {
+  out.clear();
+  const auto& D = P.direct_runs;
+  for (uint64_t a = off; a < end;) {
+    while (run < D.size() && D[run].hi <= a) ++run;
+    uint64_t b = end;
+    if (run < D.size() && D[run].lo < end) {
+      if (D[run].lo <= a) {
+        a = std::min(end, D[run].hi);
+        continue;
+      }
+      b = D[run].lo;
+    }
+    out.emplace_back(a, b);
+    a = b;
+  }
+}
+
+// Enqueues the direct copies of every direct run starting in [off, end).
+void copy_direct(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, uint8_t* stream,
+                 bool d2h, cudaStream_t st) {
+  constexpr uint64_t kPiece = 64ull << 20;  // the copy engine's best piece (direct_copy2.txt)
+  const auto& D = P.direct_runs;
+  while (run < D.size() && D[run].lo < off) ++run;
+  for (; run < D.size() && D[run].lo < end; ++run) {
+    const auto& d = D[run];
+    // refill: through the end of the destination word straddling `hi` (the
+    // scatter writes only words that start outside the run)
+    const uint64_t hi = d2h ? d.hi : d.hi + 15;
+    for (uint64_t c = d.lo; c < hi; c += kPiece) {
+      const uint64_t n = std::min(kPiece, hi - c);
+      uint8_t* dev = reinterpret_cast<uint8_t*>(d.dev + (c - d.lo));
+      check_cuda(d2h ? cudaMemcpyAsync(stream + c, dev, n, cudaMemcpyDeviceToHost, st)
+                     : cudaMemcpyAsync(dev, stream + c, n, cudaMemcpyHostToDevice, st),
+                 d2h ? "D2H direct" : "H2D direct");
+    }
+  }
 }
 
 uint64_t host_run_bytes(const ImagePlan& P) {
@@ -699,7 +785,7 @@ uint64_t host_run_bytes(const ImagePlan& P) {
 // in pieces of at most kCopyChunk.  `run` walks P.host_runs across calls.
 void copy_window(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, uint8_t* buf,
                  uint8_t* stream, bool d2h, cudaStream_t st) {
-  const auto& R = P.host_runs;
+  const auto& R = P.skip_runs;
   thread_local std::vector<void*> dsts, srcs;
   thread_local std::vector<size_t> sizes;
   dsts.clear();
@@ -715,8 +801,11 @@ void copy_window(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, ui
       }
       b = R[run].first;
     }
-    for (uint64_t c = a; c < b; c += DrainEngine::kCopyChunk) {
-      const uint64_t n = std::min(DrainEngine::kCopyChunk, b - c);
+    // H2D: 16 bytes past a gap that a skip run ends, for the scatter's
+    // straddling last word (ring bytes under a skip run are never read else)
+    const uint64_t bc = d2h ? b : std::min(end, b + 16);
+    for (uint64_t c = a; c < bc; c += DrainEngine::kCopyChunk) {
+      const uint64_t n = std::min(DrainEngine::kCopyChunk, bc - c);
       dsts.push_back(d2h ? static_cast<void*>(stream + c) : static_cast<void*>(buf + (c - off)));
       srcs.push_back(d2h ? static_cast<void*>(buf + (c - off)) : static_cast<void*>(stream + c));
       sizes.push_back(n);
@@ -972,6 +1061,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   // is needed, nothing migrates): long runs are skipped by every window copy,
   // ring and shadow alike, and written by host threads during the stall
   plan_host_runs(P, P.stream_len);
+  plan_direct_runs(P, head);  // only where the app stays stopped until they land
 
   // With the whole stream in the shadow, K1 copies every payload chunk to
   // its stream position right after hashing it: one HBM read of the state
@@ -1041,7 +1131,8 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
       if (t.joinable()) t.join();
     }
   } join_host{host_pass, recorded};
-  size_t run_i = 0;
+  size_t run_i = 0, krun_i = 0, drun_i = 0;
+  std::vector<std::pair<uint64_t, uint64_t>> kr;
   for (uint64_t w = 0; w < windows; ++w) {
     const int slot = int(w % DrainEngine::kSlots);
     uint8_t* buf = E.d_ring + slot * (W + 64);
@@ -1050,15 +1141,20 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
     if (w >= uint64_t(DrainEngine::kSlots))
       check_cuda(cudaStreamWaitEvent(E.s_pack, E.ev_free[slot], 0), "wait");
     if (stats) cudaEventRecord(E.ev_w0[w], E.s_pack);
-    check_cuda(cudaError_t(crac_pack_records(E.d_recs.ptr, uint32_t(P.recs.size()),
-                                             E.d_tile_rec.ptr + off / CRAC_TILE_BYTES, off, len,
-                                             buf, E.s_pack)),
-               "pack");
+    kernel_ranges(P, krun_i, off, off + len, kr);
+    for (const auto& [g0, g1] : kr) {
+      check_cuda(cudaError_t(crac_pack_records(E.d_recs.ptr, uint32_t(P.recs.size()),
+                                               E.d_tile_rec.ptr + g0 / CRAC_TILE_BYTES, g0, g1 - g0,
+                                               buf + (g0 - off), E.s_pack)),
+                 "pack");
+      Q.packed += g1 - g0;
+    }
     if (stats) cudaEventRecord(E.ev_w1[w], E.s_pack);
     check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_pack), "event");
     check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_ready[slot], 0), "wait");
     // the copy engine runs best on 16 MiB pieces; the pack on bigger windows
     copy_window(P, run_i, off, off + len, buf, img + s3, true, E.s_copy);
+    copy_direct(P, drun_i, off, off + len, img + s3, true, E.s_copy);
     check_cuda(cudaEventRecord(E.ev_free[slot], E.s_copy), "event");
     if (land_events) check_cuda(cudaEventRecord(E.ev_land[w], E.s_copy), "event");
     recorded.store(int64_t(w), std::memory_order_release);
@@ -1142,8 +1238,8 @@ void drain_finish(Session& session, DrainStats* stats) {
       stats->hash_launches = (P.pay_first.back() ? 1 : 0) + (P.n_dev_pages ? 1 : 0);
       stats->hash_bytes = hashed_bytes(P);
       stats->pack_launches = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
-      stats->pack_bytes = P.stream_len;
-      stats->pack_ms = Q.windows ? median_window_ms(E, Q.windows) : 0;  // per ring launch
+      stats->pack_bytes = Q.packed + (P.stream_len - Q.head);  // ring windows + shadow
+      stats->pack_ms = Q.windows ? median_window_ms(E, Q.windows) : 0;  // per ring window
       stats->d2h_bytes = P.stream_len - host_run_bytes(P);
       stats->shadow_bytes = P.stream_len - Q.head;
     }
@@ -1318,13 +1414,14 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   auto plan = [&](const std::vector<BulkItem>& items) {
     build_plan(items, P);
     plan_host_runs(P, P.stream_len);
+    plan_direct_runs(P, P.stream_len);
     P.log_len = p.log.size();
     if (P.len3 != p.sec[2].length || P.len4 != p.sec[3].length ||
         s3 + P.stream_len != p.sec[3].payload_off + p.sec[3].length)
       raise(Errc::ImageCorrupt, "bulk sections do not match the log's active set");
     tr.mark("plan");
   };
-  uint64_t windows = 0, verifies = 0;
+  uint64_t windows = 0, verifies = 0, scattered = 0;
   // enqueues H2D windows -> scatter -> K1 verify (payloads as their regions
   // complete, then the device-resident pages); nothing here waits
   auto enqueue_data_path = [&] {
@@ -1335,7 +1432,8 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     windows = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
     if (stats) E.ensure_window_events(windows);
     check_cuda(cudaEventRecord(E.ev_c0, E.s_copy), "event");
-    size_t spans_done = 0, run_i = 0;
+    size_t spans_done = 0, run_i = 0, krun_i = 0, drun_i = 0;
+    std::vector<std::pair<uint64_t, uint64_t>> kr;
     constexpr uint64_t kVerifyBatch = 8192;  // 512 MiB of 64 KiB chunks
     for (uint64_t w = 0; w < windows; ++w) {
       const int slot = int(w % DrainEngine::kSlots);
@@ -1347,13 +1445,19 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
         check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_free[slot], 0), "wait");
       copy_window(P, run_i, off, off + with_ahead, buf, const_cast<uint8_t*>(raw.data() + s3),
                   false, E.s_copy);
+      copy_direct(P, drun_i, off, off + len, const_cast<uint8_t*>(raw.data() + s3), false,
+                  E.s_copy);
       check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_copy), "event");
       check_cuda(cudaStreamWaitEvent(E.s_pack, E.ev_ready[slot], 0), "wait");
       if (stats) cudaEventRecord(E.ev_w0[w], E.s_pack);
-      check_cuda(cudaError_t(crac_scatter_records(E.d_recs.ptr, uint32_t(P.recs.size()),
-                                                  E.d_tile_rec.ptr + off / CRAC_TILE_BYTES, buf,
-                                                  off, len, E.s_pack)),
-                 "scatter");
+      kernel_ranges(P, krun_i, off, off + len, kr);
+      for (const auto& [g0, g1] : kr) {
+        check_cuda(cudaError_t(crac_scatter_records(E.d_recs.ptr, uint32_t(P.recs.size()),
+                                                    E.d_tile_rec.ptr + g0 / CRAC_TILE_BYTES,
+                                                    buf + (g0 - off), g0, g1 - g0, E.s_pack)),
+                   "scatter");
+        scattered += g1 - g0;
+      }
       if (stats) cudaEventRecord(E.ev_w1[w], E.s_pack);
       check_cuda(cudaEventRecord(E.ev_free[slot], E.s_pack), "event");
       // verify as we go: re-hash the regions whose last byte has landed, in
@@ -1484,7 +1588,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     if (windows) {
       stats->copy_ms = elapsed(E.ev_c0, E.ev_c1);
       stats->pack_launches = windows;
-      stats->pack_bytes = P.stream_len;
+      stats->pack_bytes = scattered;
       stats->pack_ms = median_window_ms(E, windows);
       stats->h2d_bytes = P.stream_len - host_run_bytes(P);
       stats->hash_bytes = hashed_bytes(P);

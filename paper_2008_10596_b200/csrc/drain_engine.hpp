@@ -111,6 +111,16 @@ struct ImagePlan {
   // stream ranges of host-resident pages only (frames + content), long
   // enough that the window copies skip them (plan_host_runs)
   std::vector<std::pair<uint64_t, uint64_t>> host_runs;
+  // Direct runs (plan_direct_runs): tile-aligned interiors of big Device
+  // payloads, copied by the copy engine straight between the allocation and
+  // the image -- no pack / scatter, no HBM staging.  `dev` = device address
+  // of stream byte `lo`.
+  struct DirectRun {
+    uint64_t lo, hi, dev;
+  };
+  std::vector<DirectRun> direct_runs;
+  std::vector<std::pair<uint64_t, uint64_t>> skip_runs;  // host ∪ direct, sorted
+  std::vector<uint8_t> pay_kind;  // AllocationKind of each payload record
   uint64_t log_len = 0;
   uint64_t tail_bytes = 0;  // STREAMS + APPSTATE + KERNEL_REGISTRY, framed
   bool valid = false;
@@ -167,6 +177,7 @@ struct DrainEngine {
     uint64_t head = 0;       // stream bytes drained through the ring (stall)
     uint32_t crc3 = 0, crc4 = 0;
     uint64_t windows = 0;    // ring windows (stats)
+    uint64_t packed = 0;     // stream bytes the ring windows' pack kernels produced
     double stall_ms = 0;
     // host-resident pages of short runs in the shadow part, copied while the
     // app was stopped; written into the image after the shadow D2H lands
