@@ -703,13 +703,18 @@ void plan_host_runs(ImagePlan& P, uint64_t limit) {
 constexpr uint64_t kTile = CRAC_TILE_BYTES;
 constexpr uint64_t kDirectMinTiles = 4;
 
-void plan_direct_runs(ImagePlan& P, uint64_t limit) {
+void plan_direct_runs(ImagePlan& P, uint64_t limit, bool drain) {
   P.direct_runs.clear();
-  static const bool enabled = [] {
+  // CRAC_DIRECT = 0 | drain | refill | both (default): measurement knob
+  static const int enabled = [] {
     const char* e = std::getenv("CRAC_DIRECT");
-    return !(e && !std::strcmp(e, "0"));
+    if (!e) return 3;
+    if (!std::strcmp(e, "0")) return 0;
+    if (!std::strcmp(e, "drain")) return 1;
+    if (!std::strcmp(e, "refill")) return 2;
+    return 3;
   }();
-  if (enabled)
+  if (enabled & (drain ? 1 : 2))
     for (size_t k = 0; k < P.pay_spans.size(); ++k) {
       if (P.pay_kind[k] != uint8_t(AllocationKind::Device)) continue;
       const uint64_t a = P.pay_rec_off[k], b = std::min(a + P.pay_spans[k].len, limit);
@@ -756,7 +761,10 @@ void kernel_ranges(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end,
 // Enqueues the direct copies of every direct run starting in [off, end).
 void copy_direct(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, uint8_t* stream,
                  bool d2h, cudaStream_t st) {
-  constexpr uint64_t kPiece = 64ull << 20;  // the copy engine's best piece (direct_copy2.txt)
+  static const uint64_t kPiece = [] {  // the copy engine's best piece (direct_copy2.txt)
+    const char* e = std::getenv("CRAC_DIRECT_PIECE_MIB");
+    return uint64_t(e ? std::max(1, std::atoi(e)) : 64) << 20;
+  }();
   const auto& D = P.direct_runs;
   while (run < D.size() && D[run].lo < off) ++run;
   for (; run < D.size() && D[run].lo < end; ++run) {
@@ -1061,7 +1069,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   // is needed, nothing migrates): long runs are skipped by every window copy,
   // ring and shadow alike, and written by host threads during the stall
   plan_host_runs(P, P.stream_len);
-  plan_direct_runs(P, head);  // only where the app stays stopped until they land
+  plan_direct_runs(P, head, true);  // only where the app stays stopped until they land
 
   // With the whole stream in the shadow, K1 copies every payload chunk to
   // its stream position right after hashing it: one HBM read of the state
@@ -1414,7 +1422,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   auto plan = [&](const std::vector<BulkItem>& items) {
     build_plan(items, P);
     plan_host_runs(P, P.stream_len);
-    plan_direct_runs(P, P.stream_len);
+    plan_direct_runs(P, P.stream_len, false);
     P.log_len = p.log.size();
     if (P.len3 != p.sec[2].length || P.len4 != p.sec[3].length ||
         s3 + P.stream_len != p.sec[3].payload_off + p.sec[3].length)
