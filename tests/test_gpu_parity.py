@@ -376,6 +376,33 @@ def test_c3_managed_mixed_residence_matches_reference(eng):
     assert rs.checkpoint()[0] == img
 
 
+def test_direct_runs_edges_match_reference(eng):
+    """Device payloads around the direct-run threshold (6 stream tiles plus
+    the 64-byte margins), payloads that straddle 64 MiB window boundaries,
+    odd sizes on every word phase, a big Pinned payload (never direct) and a
+    managed one between them: the image equals the reference's, and the
+    refill (direct H2D + edge scatter) restores every byte."""
+    MIB, T = 1 << 20, 65536
+    sizes = [6 * T + 127, 6 * T + 128, 6 * T + 129, 7 * T, 7 * T + 15, 64 * MIB + 1,
+             30 * MIB + 3, 30 * MIB + 5, 30 * MIB + 7, 5 * T - 1]
+    s = eng.Session(seed=11, arena_bytes=512 * MIB)
+    r = ref.RefSession(seed=11, arena_bytes=512 * MIB)
+    for api in (s, r):
+        for k, size in enumerate(sizes):
+            i, _ = api.alloc(workloads.DEVICE, size)
+            api.fill_synthetic(i, 40 + k)
+            if k == 4:
+                p_, _ = api.alloc(workloads.PINNED, 2 * MIB + 9)
+                api.fill_synthetic(p_, 3)
+                m, _ = api.alloc(workloads.MANAGED, MIB + 77)
+                api.fill_synthetic(m, 4, workloads.DEVICE_SIDE)
+    img, st = s.checkpoint()
+    assert img == r.checkpoint()[0]
+    rs, _ = eng.restart(img)
+    assert _state(rs) == _state(s)
+    assert rs.checkpoint()[0] == img
+
+
 def test_c3_host_runs_skip_the_link_and_match_reference(eng):
     """Host-resident runs >= 256 KiB never cross PCIe (the window copies skip
     them; host threads write their frames and content).  Runs straddle the
