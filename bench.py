@@ -423,7 +423,9 @@ WORKLOAD_NAMES = {
 
 def ncu_traffic(kernel):
     """DRAM bytes (read + write) per launch of `kernel` from the newest
-    committed `ncu --set full` summary (profiles/*/ncu_full.json)."""
+    committed `ncu --set full` summary (profiles/*/ncu_full.json).  Where
+    ncu_meta.json gives the profiled launch's algorithmic bytes, returns the
+    ratio instead (DRAM bytes per algorithmic byte) for the caller to scale."""
     if not kernel:
         return None, None
     name = kernel.split(" ")[0]
@@ -433,6 +435,9 @@ def ncu_traffic(kernel):
             full = json.loads(path.read_text())
         except (OSError, ValueError):
             continue
+        meta = {}
+        if (path.parent / "ncu_meta.json").exists():
+            meta = json.loads((path.parent / "ncu_meta.json").read_text())
         for key, m in full.items():
             if name not in key:
                 continue
@@ -440,7 +445,11 @@ def ncu_traffic(kernel):
             for metric in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 val, unit = m[metric].split()
                 total += float(val) * units[unit]
-            return int(total), f"{path.parent.name}/{path.name}: {key}"
+            src = f"{path.parent.name}/{path.name}: {key}"
+            alg = (meta.get(key) or {}).get("algorithmic_bytes")
+            if alg:  # DRAM bytes per algorithmic byte of the profiled launch
+                return total / alg, src + f" ({total / 1e9:.3f} GB for {alg / 1e9:.3f} GB algorithmic)"
+            return int(total), src
     return None, None
 
 
@@ -747,6 +756,8 @@ def main() -> None:
     dom_ms, dom_bytes, _ = kernels[dom] if dom else (0.0, 0, 0)
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
     traffic, traffic_src = ncu_traffic(dom)
+    if traffic is not None and traffic < 16:  # a ratio: scale to this launch
+        traffic = int(traffic * dom_bytes)
 
     # incremental (C5 shape on the resident state): hash-only and a 1 % dirty drain
     incremental = None
