@@ -82,6 +82,17 @@ int crac_hash_drain_range(const crac_span_t* d_spans, const uint64_t* d_chunk_fi
                           uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
                           uint32_t* d_crc, uint32_t* d_crc_prev, const uint64_t* d_dst_off,
                           uint8_t* host_image, unsigned long long* d_counters, void* stream);
+/* Split form of crac_hash_drain_range: the first n_writers CTAs only write
+ * dirty chunks to the image, the others hash and hand each dirty chunk over
+ * through d_queue (>= c_hi - c_lo + 16 * n_writers + 1 u64, zeroed here), so
+ * the hashing never waits on PCIe.  d_counters needs 5 u64 ([0] dirty chunks,
+ * [1] dirty bytes, [2..4] queue control; zeroed by the caller).  n_writers
+ * <= SMs / 4. */
+int crac_hash_drain_split(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
+                          uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
+                          uint32_t* d_crc, uint32_t* d_crc_prev, const uint64_t* d_dst_off,
+                          uint8_t* host_image, unsigned long long* d_counters,
+                          unsigned long long* d_queue, uint32_t n_writers, void* stream);
 
 /* Incremental drain straight to the host image: dirty chunk k (index
  * d_dirty_idx[first + k]) of payload span s is written by the SMs to

@@ -1640,13 +1640,31 @@ void incremental_locked(Session& session, PinnedImage& image, DrainStats* stats)
     upload(E.d_pay_dst, dst, E.s_pack);
     E.dst_for_image = P.image_ptr;
   }
-  check_cuda(cudaMemsetAsync(E.d_counters.ptr, 0, 16, E.s_pack), "counters");
+  // Split by default: writer CTAs stream the dirty chunks over PCIe while the
+  // other SMs hash at HBM speed (CRAC_INCR_SPLIT=0: every hashing warp writes
+  // its own dirty chunks, the fused form)
+  static const bool split = [] {
+    const char* e = std::getenv("CRAC_INCR_SPLIT");
+    return !(e && !std::strcmp(e, "0"));
+  }();
+  const uint32_t writers = uint32_t(std::max(1, std::min(16, E.sm_count / 8)));
+  E.d_counters.ensure(5);
+  check_cuda(cudaMemsetAsync(E.d_counters.ptr, 0, 40, E.s_pack), "counters");
+  if (split) E.d_dirty_idx.ensure(n + uint64_t(writers) * 16 + 1);
   check_cuda(cudaEventRecord(E.ev_h0, E.s_pack), "event");
-  check_cuda(cudaError_t(crac_hash_drain_range(
-                 E.d_pay_spans.ptr, E.d_pay_first.ptr, uint32_t(P.pay_spans.size()),
-                 DrainEngine::kChunk, 0, n, E.d_pay_crc.ptr, E.d_prev_crc.ptr, E.d_pay_dst.ptr, img,
-                 E.d_counters.ptr, E.s_pack)),
-             "hash+drain");
+  if (split)
+    check_cuda(cudaError_t(crac_hash_drain_split(
+                   E.d_pay_spans.ptr, E.d_pay_first.ptr, uint32_t(P.pay_spans.size()),
+                   DrainEngine::kChunk, 0, n, E.d_pay_crc.ptr, E.d_prev_crc.ptr, E.d_pay_dst.ptr,
+                   img, E.d_counters.ptr,
+                   reinterpret_cast<unsigned long long*>(E.d_dirty_idx.ptr), writers, E.s_pack)),
+               "hash+drain split");
+  else
+    check_cuda(cudaError_t(crac_hash_drain_range(
+                   E.d_pay_spans.ptr, E.d_pay_first.ptr, uint32_t(P.pay_spans.size()),
+                   DrainEngine::kChunk, 0, n, E.d_pay_crc.ptr, E.d_prev_crc.ptr, E.d_pay_dst.ptr,
+                   img, E.d_counters.ptr, E.s_pack)),
+               "hash+drain");
   check_cuda(cudaEventRecord(E.ev_h1, E.s_pack), "event");
   check_cuda(cudaMemcpyAsync(E.h_count.ptr, E.d_counters.ptr, 16, cudaMemcpyDeviceToHost, E.s_pack),
              "counters");

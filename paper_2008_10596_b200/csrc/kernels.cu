@@ -286,7 +286,14 @@ struct HashDrain {
   const uint64_t* dst_off;       // per span: image offset of its first payload byte
   uint8_t* host;                 // pinned image (UVA)
   unsigned long long* counters;  // [0] dirty chunks, [1] dirty bytes
+  // kMode 4 (split drain): the first n_writers CTAs write the dirty chunks the
+  // others push into `queue` (chunk index + 1, 0 = not yet); qctl[0] pushed,
+  // qctl[1] claimed by writers, qctl[2] hasher warps finished
+  unsigned long long* queue;
+  unsigned long long* qctl;
+  uint32_t n_writers;
 };
+
 
 __device__ __forceinline__ void chunk_to_host(uint8_t* dst, const uint8_t* src, uint32_t len,
                                               uint32_t lane) {
@@ -315,9 +322,53 @@ __device__ __forceinline__ void chunk_to_host(uint8_t* dst, const uint8_t* src, 
   for (uint32_t i = h + 16 * body + lane; i < len; i += 32) dst[i] = src[i];
 }
 
+// Split-drain writer warp: claims queue slots in order and copies each dirty
+// chunk into the image; exits once every hasher warp has finished and no
+// pushed slot is left.  Hashers never wait for writers, so the kernel cannot
+// deadlock as long as n_writers < the CTAs the GPU can hold at once.
+__device__ void drain_writer(const crac_span_t* __restrict__ spans,
+                             const uint64_t* __restrict__ chunk_first, uint32_t n_spans,
+                             uint32_t chunk_bytes, const HashDrain& hd, uint32_t hasher_warps,
+                             uint32_t lane) {
+  for (;;) {
+    unsigned long long slot = 0;
+    if (lane == 0) slot = atomicAdd(&hd.qctl[1], 1ull);
+    slot = __shfl_sync(0xFFFFFFFFu, slot, 0);
+    unsigned long long v = 0;
+    for (;;) {
+      if (lane == 0) {
+        v = *reinterpret_cast<volatile unsigned long long*>(&hd.queue[slot]);
+        if (!v) {
+          const unsigned long long done = *reinterpret_cast<volatile unsigned long long*>(&hd.qctl[2]);
+          if (done == hasher_warps) {
+            __threadfence();
+            const unsigned long long tail =
+                *reinterpret_cast<volatile unsigned long long*>(&hd.qctl[0]);
+            v = *reinterpret_cast<volatile unsigned long long*>(&hd.queue[slot]);
+            if (!v && slot >= tail) v = ~0ull;
+          }
+        }
+      }
+      v = __shfl_sync(0xFFFFFFFFu, v, 0);
+      if (v) break;
+      __nanosleep(256);
+    }
+    if (v == ~0ull) return;
+    const uint64_t c = v - 1;
+    const uint32_t s = find_span(chunk_first, n_spans, c);
+    const crac_span_t sp = spans[s];
+    const uint64_t off = (c - __ldg(chunk_first + s)) * chunk_bytes;
+    const uint64_t rem = sp.len - off;
+    const uint32_t len = rem < chunk_bytes ? uint32_t(rem) : chunk_bytes;
+    chunk_to_host(hd.host + hd.dst_off[s] + off, reinterpret_cast<const uint8_t*>(sp.ptr + off), len,
+                  lane);
+  }
+}
+
 // kMode: 0 hash only; 1 fused incremental drain (dirty chunks to the image);
 // 2 hash + copy every chunk from registers (stall-reduced snapshot), every
-// destination 16-byte aligned; 3 the same for any destination alignment.
+// destination 16-byte aligned; 3 the same for any destination alignment;
+// 4 split incremental drain (hashers push dirty chunks, writer CTAs copy).
 template <int kRows, int kMode>
 __global__ void __launch_bounds__(kK1Threads, 1)
     k1_chunk_crc(const crac_span_t* __restrict__ spans, const uint64_t* __restrict__ chunk_first,
@@ -332,12 +383,23 @@ __global__ void __launch_bounds__(kK1Threads, 1)
   __syncthreads();
 
   const uint32_t lane = threadIdx.x & 31;
+  const uint32_t n_wr = kMode == 4 ? hd.n_writers : 0;
+  if (kMode == 4 && blockIdx.x < n_wr) {
+    drain_writer(spans, chunk_first, n_spans, chunk_bytes, hd, (gridDim.x - n_wr) * kK1Warps, lane);
+    return;
+  }
   const LaneLut lut = make_lut(static_cast<uint32_t>(__cvta_generic_to_shared(s_tab)), lane);
-  const uint64_t gw = blockIdx.x * uint64_t(kK1Warps) + (threadIdx.x >> 5);
-  const uint64_t tw = gridDim.x * uint64_t(kK1Warps);
+  const uint64_t gw = (blockIdx.x - n_wr) * uint64_t(kK1Warps) + (threadIdx.x >> 5);
+  const uint64_t tw = (gridDim.x - n_wr) * uint64_t(kK1Warps);
   const uint64_t total_chunks = c_hi - c_lo;
   const uint64_t c_begin = c_lo + total_chunks * gw / tw, c_end = c_lo + total_chunks * (gw + 1) / tw;
-  if (c_begin >= c_end) return;
+  if (c_begin >= c_end) {
+    if (kMode == 4 && lane == 0) {
+      __threadfence();
+      atomicAdd(&hd.qctl[2], 1ull);
+    }
+    return;
+  }
 
   uint32_t s = find_span(chunk_first, n_spans, c_begin);
   uint64_t s_next = __ldg(chunk_first + s + 1);
@@ -409,9 +471,18 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         hd.prev[c] = crc;
         atomicAdd(&hd.counters[0], 1ull);
         atomicAdd(&hd.counters[1], (unsigned long long)len);
+        if (kMode == 4) {  // hand the chunk to the writers and keep hashing
+          const unsigned long long slot = atomicAdd(&hd.qctl[0], 1ull);
+          *reinterpret_cast<volatile unsigned long long*>(&hd.queue[slot]) = c + 1;
+          __threadfence();
+        }
       }
-      chunk_to_host(hd.host + hd.dst_off[s] + off, base, len, lane);
+      if (kMode != 4) chunk_to_host(hd.host + hd.dst_off[s] + off, base, len, lane);
     }
+  }
+  if (kMode == 4 && lane == 0) {
+    __threadfence();
+    atomicAdd(&hd.qctl[2], 1ull);
   }
 }
 
@@ -1148,7 +1219,31 @@ int crac_hash_drain_range(const crac_span_t* d_spans, const uint64_t* d_chunk_fi
   if (!d_crc_prev || !d_counters) return int(cudaErrorInvalidValue);
   k1_chunk_crc<16, 1><<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
       d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, k_full_for(chunk_bytes),
-      HashDrain{d_crc_prev, d_dst_off, host_image, d_counters});
+      HashDrain{d_crc_prev, d_dst_off, host_image, d_counters, nullptr, nullptr, 0});
+  return int(cudaGetLastError());
+}
+
+int crac_hash_drain_split(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
+                          uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
+                          uint32_t* d_crc, uint32_t* d_crc_prev, const uint64_t* d_dst_off,
+                          uint8_t* host_image, unsigned long long* d_counters,
+                          unsigned long long* d_queue, uint32_t n_writers, void* stream) {
+  if (c_hi <= c_lo) return 0;
+  if (chunk_bytes == 0 || chunk_bytes % 512) return int(cudaErrorInvalidValue);
+  if (!d_crc_prev || !d_counters || !d_queue || n_writers == 0) return int(cudaErrorInvalidValue);
+  if (int rc = crac_gpu_init()) return rc;
+  // one CTA per SM (128 KiB of tables each): every CTA of the grid is resident
+  // at once, writers included, and hashers get all the other SMs
+  const uint32_t sms = uint32_t(sm_count());
+  if (n_writers * 4 > sms) return int(cudaErrorInvalidValue);
+  uint64_t hashers = (c_hi - c_lo + kK1Warps - 1) / kK1Warps;
+  if (hashers > sms - n_writers) hashers = sms - n_writers;
+  cudaStream_t st = cudaStream_t(stream);
+  const uint64_t q = c_hi - c_lo + uint64_t(n_writers) * kK1Warps + 1;
+  if (cudaError_t e = cudaMemsetAsync(d_queue, 0, q * 8, st); e != cudaSuccess) return int(e);
+  k1_chunk_crc<16, 4><<<unsigned(hashers + n_writers), kK1Threads, kTabBytes, st>>>(
+      d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, k_full_for(chunk_bytes),
+      HashDrain{d_crc_prev, d_dst_off, host_image, d_counters, d_queue, d_counters + 2, n_writers});
   return int(cudaGetLastError());
 }
 

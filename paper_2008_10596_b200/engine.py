@@ -134,6 +134,8 @@ _SIGS = {
     "crac_diff_compact_range": (C.c_int, [_P, _P, _U64, _U64, _P, _P, _P, _P]),
     "crac_fold_sections": (C.c_int, [_P, _U32, _P, _P, _U32, _P, _U64, _U64, _P, _P]),
     "crac_hash_drain_range": (C.c_int, [_P, _P, _U32, _U32, _U64, _U64, _P, _P, _P, _P, _P, _P]),
+    "crac_hash_drain_split": (C.c_int, [_P, _P, _U32, _U32, _U64, _U64, _P, _P, _P, _P, _P, _P,
+                                        _U32, _P]),
     "crac_pack_records": (C.c_int, [_P, _U32, _P, _U64, _U64, _P, _P]),
     "crac_scatter_records": (C.c_int, [_P, _U32, _P, _P, _U64, _U64, _P]),
     "crac_diff_compact": (C.c_int, [_P, _P, _U64, _P, _P, _P, _P]),

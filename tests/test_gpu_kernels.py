@@ -160,6 +160,54 @@ def test_fused_hash_drain_writes_only_changed_chunks(eng):
     assert img[16:16 + 2 * chunk] == bytes(2 * chunk)
 
 
+@pytest.mark.parametrize("writers", [1, 4, 16])
+def test_split_hash_drain_writes_only_changed_chunks(eng, writers):
+    """crac_hash_drain_split: writer CTAs copy the chunks the hashers hand over
+    (more chunks than hashing warps, ragged last chunk, odd offsets)."""
+    L = eng.lib()
+    chunk = 65536
+    bufs = [_rand(chunk * 300 + 1000, 5).cuda(), _rand(chunk * 41 + 3, 6).cuda()]
+    spans = _spans(bufs)
+    first_d, first = _first(bufs, chunk)
+    n = first[-1]
+    crc = torch.zeros(n, dtype=torch.int32).cuda()
+    prev = torch.zeros(n, dtype=torch.int32).cuda()
+    total = sum(b.numel() for b in bufs)
+    image = torch.zeros(total + 64, dtype=torch.uint8).pin_memory()
+    offs = [16, 16 + bufs[0].numel() + 16]
+    d_off = torch.tensor(offs, dtype=torch.int64).cuda()
+    counters = torch.zeros(5, dtype=torch.int64).cuda()
+    queue = torch.zeros(n + 16 * writers + 1, dtype=torch.int64).cuda()
+    args = lambda: (_p(spans), _p(first_d), 2, chunk, 0, n, _p(crc), _p(prev), _p(d_off),
+                    _p(image), _p(counters), _p(queue), writers, None)
+    assert L.crac_hash_drain_split(*args()) == 0  # everything dirty
+    torch.cuda.synchronize()
+    img = bytes(image.numpy())
+    for b, o in zip(bufs, offs):
+        data = bytes(b.cpu().numpy())
+        assert img[o:o + len(data)] == data
+    assert counters.cpu().tolist()[:2] == [n, total]
+    # a few chunks change, spread over both buffers
+    image.zero_()
+    counters.zero_()
+    for c in (0, 7, 299, 300):
+        bufs[0][c * chunk + 11] ^= 0x5A
+    bufs[1][41 * chunk + 1] ^= 0x01  # the 3-byte last chunk
+    assert L.crac_hash_drain_split(*args()) == 0
+    torch.cuda.synchronize()
+    img = bytes(image.numpy())
+    assert counters.cpu().tolist()[:2] == [5, 3 * chunk + 1000 + 3]
+    d0, d1 = bytes(bufs[0].cpu().numpy()), bytes(bufs[1].cpu().numpy())
+    for c in (0, 7, 299):
+        assert img[16 + c * chunk:16 + (c + 1) * chunk] == d0[c * chunk:(c + 1) * chunk]
+    assert img[16 + 300 * chunk:16 + len(d0)] == d0[300 * chunk:]
+    assert img[offs[1] + 41 * chunk:offs[1] + len(d1)] == d1[41 * chunk:]
+    assert img[offs[1]:offs[1] + 41 * chunk] == bytes(41 * chunk)
+    assert img[16 + chunk:16 + 2 * chunk] == bytes(chunk)  # clean chunks untouched
+    assert L.crac_hash_drain_split(_p(spans), _p(first_d), 2, chunk, 0, n, _p(crc), _p(prev),
+                                   _p(d_off), _p(image), _p(counters), _p(queue), 0, None) != 0
+
+
 def test_pack_scatter_round_trip_random_records(eng):
     """K2a then K3 over a random framed stream, across window boundaries."""
     L = eng.lib()
