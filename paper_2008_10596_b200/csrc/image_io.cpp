@@ -236,20 +236,27 @@ uint64_t read_file_parallel(const std::filesystem::path& path, uint8_t* dst, uin
   const uint32_t threads = io_threads(opt);
   const bool in_place = reinterpret_cast<uintptr_t>(dst) % kBlock == 0 && capacity >= round_block(n);
   const uint64_t pieces = (n + chunk - 1) / chunk;
+  // experiment knob: one open file description per thread (as dd runs)
+  const bool fd_per_thread = std::getenv("CRAC_IO_FD_PER_THREAD") != nullptr;
+  std::vector<Fd> fds(fd_per_thread ? std::min<uint64_t>(threads, std::max<uint64_t>(pieces, 1)) : 0);
+  for (Fd& x : fds)
+    if ((x.fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC | (direct ? O_DIRECT : 0))) < 0)
+      raise(Errc::ImageCorrupt, "cannot read " + path.string());
   std::atomic<uint64_t> bounced{0};
   std::atomic<bool> short_read{false};
-  const int err = run_pieces(pieces, threads, chunk, [&](uint64_t k, uint32_t,
+  const int err = run_pieces(pieces, threads, chunk, [&](uint64_t k, uint32_t t,
                                                           std::unique_ptr<AlignedBuf>& b,
                                                           uint64_t bb) -> int {
+    const int fd = fd_per_thread ? fds[t].fd : f.fd;
     const uint64_t off = k * chunk, len = std::min(chunk, n - off);
     uint64_t got = 0;
     int e;
     if (!direct || in_place) {
-      e = full_pread(f.fd, dst + off, direct ? round_block(len) : len, off, len, &got);
+      e = full_pread(fd, dst + off, direct ? round_block(len) : len, off, len, &got);
     } else {
       if (!b) b = std::make_unique<AlignedBuf>(bb);
       if (!b->p) return ENOMEM;
-      e = full_pread(f.fd, b->p, round_block(len), off, len, &got);
+      e = full_pread(fd, b->p, round_block(len), off, len, &got);
       if (!e) std::memcpy(dst + off, b->p, std::min(got, len));
       bounced.fetch_add(len, std::memory_order_relaxed);
     }
