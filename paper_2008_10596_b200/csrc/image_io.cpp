@@ -234,7 +234,10 @@ uint64_t read_file_parallel(const std::filesystem::path& path, uint8_t* dst, uin
   if (n > capacity) raise(Errc::InvalidArgument, "buffer too small for " + path.string());
   const uint64_t chunk = io_chunk(opt);
   const uint32_t threads = io_threads(opt);
-  const bool in_place = reinterpret_cast<uintptr_t>(dst) % kBlock == 0 && capacity >= round_block(n);
+  // experiment knob CRAC_IO_BOUNCE_READ: read through the per-thread bounce
+  // buffer (a reused, cache-hot 64 MiB like dd's) even when dst is aligned
+  const bool in_place = reinterpret_cast<uintptr_t>(dst) % kBlock == 0 && capacity >= round_block(n) &&
+                        std::getenv("CRAC_IO_BOUNCE_READ") == nullptr;
   const uint64_t pieces = (n + chunk - 1) / chunk;
   // experiment knob: one open file description per thread (as dd runs)
   const bool fd_per_thread = std::getenv("CRAC_IO_FD_PER_THREAD") != nullptr;

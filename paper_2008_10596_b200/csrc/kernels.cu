@@ -1142,7 +1142,7 @@ int crac_gpu_init(void) {
     if (!e) e = cudaMemcpyToSymbol(g_xpt, h.xpt.data(), 512 * 4);
     if (!e) e = cudaMemcpyToSymbol(g_pow2, h.pow2.data(), 64 * 4);
     for (auto k : {k1_chunk_crc<4, 0>, k1_chunk_crc<8, 0>, k1_chunk_crc<16, 0>,
-                   k1_chunk_crc<16, 1>, k1_chunk_crc<16, 2>, k1_chunk_crc<8, 3>})
+                   k1_chunk_crc<16, 1>, k1_chunk_crc<16, 2>, k1_chunk_crc<8, 3>, k1_chunk_crc<16, 4>})
       if (!e) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTabBytes));
     if (!e) e = cudaFuncSetAttribute(k1_chunk_crc_tma<16, 3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(k1_tma_smem<16, 3, 4>()));

@@ -40,15 +40,15 @@ def main():
     for rep in range(2):
         drop(p)
         print(f"dd read 8 streams: {dd_read(p, n):.2f} GB/s", flush=True)
-        for fdpt in (False, True):
-            for threads, chunk in ((8, 64), (16, 64), (8, 16), (32, 16), (4, 256)):
-                if fdpt:
-                    os.environ["CRAC_IO_FD_PER_THREAD"] = "1"
+        for bounce in (False, True):
+            for threads, chunk in ((8, 64), (16, 64), (8, 16), (32, 16)):
+                if bounce:
+                    os.environ["CRAC_IO_BOUNCE_READ"] = "1"
                 else:
-                    os.environ.pop("CRAC_IO_FD_PER_THREAD", None)
+                    os.environ.pop("CRAC_IO_BOUNCE_READ", None)
                 drop(p)
                 _, r = engine.read_file(p, threads=threads, chunk_bytes=chunk * MIB)
-                print(f"reader threads {threads:2d} piece {chunk:3d} MiB fd_per_thread={int(fdpt)}: "
+                print(f"reader threads {threads:2d} piece {chunk:3d} MiB bounce={int(bounce)}: "
                       f"{r['GBps']:.2f} GB/s", flush=True)
     p.unlink()
 
