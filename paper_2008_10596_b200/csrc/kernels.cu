@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     // ---- main body: rows of 512 B, kRows-deep double-buffered loads ----
     uint32_t acc;
     uint8_t* dst = nullptr;
-    if (kMode >= 2) {
+    if ((kMode == 2 || kMode == 3)) {
       dst = hd.host + hd.dst_off[s] + off;
       const uint32_t m = uint32_t(reinterpret_cast<uint64_t>(dst) & 15);
       acc = k1_rows<kRows>(lut, base + lane * 16, rows,
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       if (lane == 0) out[c] = L;
       continue;
     }
-    if (kMode >= 2) {
+    if ((kMode == 2 || kMode == 3)) {
       if (lane == 0) out[c] = L;
       // byte-exact edges the register copy left: the head word (misaligned
       // destination), the m bytes of the last main row's straddling word,
