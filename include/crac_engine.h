@@ -93,6 +93,13 @@ int crac_reserve_shadow(crac_session_t* s, uint64_t bytes);
 int crac_reserve_shadow_on(crac_session_t* s, uint64_t bytes, int device);
 int crac_checkpoint_begin(crac_session_t* s, crac_image_t* img, crac_stats_t* stats);
 int crac_checkpoint_finish(crac_session_t* s, crac_stats_t* stats);
+/* Pre-copy drain (new): begin copies the state into `img`
+ * while the application runs; finish quiesces it and re-sends only the chunks
+ * that changed since (stats.stall_ms = the quiesced phase).  Bytes equal
+ * crac_checkpoint's at the instant of finish.  Device-only sessions; others
+ * drain synchronously in begin. */
+int crac_checkpoint_precopy_begin(crac_session_t* s, crac_image_t* img, crac_stats_t* stats);
+int crac_checkpoint_precopy_finish(crac_session_t* s, crac_stats_t* stats);
 /* checkpoint(Session&) -> Snapshot -> encode_image, into a malloc'd buffer
  * released with crac_buffer_free (the reference-shaped value API). */
 int crac_checkpoint_value(crac_session_t* s, uint8_t** image, uint64_t* size);

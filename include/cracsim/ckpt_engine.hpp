@@ -161,6 +161,15 @@ void checkpoint_incremental(Session& session, PinnedImage& image, DrainStats* st
 void reserve_shadow(Session& session, uint64_t bytes, int device = -1);
 void checkpoint_begin(Session& session, PinnedImage& out, DrainStats* stats = nullptr);
 void checkpoint_finish(Session& session, DrainStats* stats = nullptr);
+// Pre-copy drain (no spare HBM needed): begin copies the whole
+// state into `out` while the application keeps running (K1 hashes each chunk
+// and writes the bytes it hashed); finish stops the application and re-sends
+// only the chunks that changed since (an incremental drain), so the stall is
+// one hash pass plus the changed bytes.  The bytes equal checkpoint_image's at
+// the instant of finish.  Device-only sessions; others drain synchronously in
+// begin.  finish's stats: stall_ms = the gated phase, total_ms = both phases.
+void checkpoint_precopy_begin(Session& session, PinnedImage& out, DrainStats* stats = nullptr);
+void checkpoint_precopy_finish(Session& session, DrainStats* stats = nullptr);
 // K1 over every live allocation (hash-only timing; no drain).
 void hash_only(Session& session, DrainStats* stats);
 Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catalog,

@@ -259,6 +259,22 @@ int crac_reserve_shadow_on(crac_session_t* s, uint64_t bytes, int device) {
   return guard([&] { reserve_shadow(s->s, bytes, device); });
 }
 
+int crac_checkpoint_precopy_begin(crac_session_t* s, crac_image_t* img, crac_stats_t* stats) {
+  return guard([&] {
+    DrainStats d;
+    checkpoint_precopy_begin(s->s, img->img, stats ? &d : nullptr);
+    to_c(d, stats);
+  });
+}
+
+int crac_checkpoint_precopy_finish(crac_session_t* s, crac_stats_t* stats) {
+  return guard([&] {
+    DrainStats d;
+    checkpoint_precopy_finish(s->s, stats ? &d : nullptr);
+    to_c(d, stats);
+  });
+}
+
 int crac_checkpoint_begin(crac_session_t* s, crac_image_t* img, crac_stats_t* stats) {
   return guard([&] {
     DrainStats d;

@@ -1258,7 +1258,13 @@ void drain_finish(Session& session, DrainStats* stats) {
   Q = DrainEngine::Pending{};
 }
 
+void precopy_wait(Session& session, double* phase1_ms);
+
 void finish_pending(Session& session) {
+  if (session.drain_engine().pending.precopy) {
+    precopy_wait(session, nullptr);
+    return;
+  }
   if (session.drain_engine().pending.active) drain_finish(session, nullptr);
 }
 
@@ -1737,6 +1743,146 @@ void checkpoint_incremental(Session& session, PinnedImage& image, DrainStats* st
     if (!raced) incremental_locked(session, image, stats);
   }
   if (raced) checkpoint_image(session, image, stats);
+}
+
+}  // namespace cracsim
+
+// ---------------------------------------------------------------------------
+// pre-copy drain (SURVEY §8f.3 stall reduction without spare HBM)
+// ---------------------------------------------------------------------------
+// Phase 1 runs while the application keeps running: K1 hashes every payload
+// chunk and writes the very bytes it hashed (from its registers) straight into
+// the pinned image, so every chunk's CRC describes exactly the bytes the image
+// holds, however the application changes the memory meanwhile.  Phase 2 is an
+// ordinary incremental drain under the gate: every chunk whose content moved
+// since phase 1 hashed it is written again, so the image is the state at the
+// instant of phase 2 and the application stops only for a hash pass plus the
+// changed bytes.  Device-only sessions (a freed Device extent stays mapped,
+// so reading it mid-free is harmless; pinned / managed backings are released
+// on free) with at least one payload; anything else is a synchronous drain.
+namespace cracsim {
+namespace {
+
+void precopy_wait(Session& session, double* phase1_ms) {
+  DrainEngine& E = session.drain_engine();
+  DrainEngine::Pending& Q = E.pending;
+  if (!Q.precopy) return;
+  check_cuda(cudaStreamSynchronize(E.s_hash), "pre-copy sync");
+  if (phase1_ms) *phase1_ms = elapsed(E.ev_t0, E.ev_h1);
+  ImagePlan& P = E.plan;
+  // the image now holds, chunk by chunk, the bytes whose CRCs K1 left in
+  // d_pay_crc: they seed the incremental pass
+  const uint64_t n_pay = P.pay_first.back();
+  E.d_prev_crc.ensure(n_pay);
+  check_cuda(cudaMemcpyAsync(E.d_prev_crc.ptr, E.d_pay_crc.ptr, n_pay * 4, cudaMemcpyDeviceToDevice,
+                             E.s_hash),
+             "seed prev crc");
+  check_cuda(cudaStreamSynchronize(E.s_hash), "pre-copy seed");
+  P.valid = true;
+  P.image_ptr = reinterpret_cast<uint64_t>(Q.out->data());
+  E.prev_valid = true;
+  E.dst_for_image = 0;  // rebuild the image-offset table for this image
+  Q = DrainEngine::Pending{};
+}
+
+}  // namespace
+
+void checkpoint_precopy_begin(Session& session, PinnedImage& out, DrainStats* stats) {
+  finish_pending(session);
+  DeviceContext& ctx = session.device();
+  DrainEngine& E = session.drain_engine();
+  ImagePlan& P = E.plan;
+  bool eligible = true;
+  uint8_t* img = nullptr;
+  {
+    QuiesceScope q(session.table(), session.config().quiesce_timeout);
+    if (stats) *stats = DrainStats{};
+    const SnapshotMeta meta{ctx.seed(), ctx.arena_bytes(), kEngineVersion};
+    const std::vector<CallLogEntry> log = session.log().snapshot();
+    const std::vector<AllocationRecord> active = active_set(log);
+    eligible = !active.empty() && std::all_of(active.begin(), active.end(), [](const AllocationRecord& r) {
+      return r.kind == AllocationKind::Device;
+    });
+    if (eligible) {
+      const std::vector<uint8_t> sec1 = meta_bytes(meta);
+      const std::vector<uint8_t> sec2 = log_bytes(log);
+      const std::vector<uint8_t> sec5 = streams_bytes(ctx.live_stream_ids());
+      const std::vector<uint8_t>& sec6 = session.app_state();
+      const std::vector<uint8_t> sec7 = registry_bytes(ctx.registered_binaries());
+      std::vector<std::vector<uint8_t>> flags;
+      build_plan(live_items(ctx, active, flags, false), P);
+      P.log_len = log.size();
+      const uint64_t s3 = 16 + (20 + sec1.size()) + (20 + sec2.size()) + 16;
+      const uint64_t total = s3 + P.stream_len + 4 + (20 + sec5.size()) + (20 + sec6.size()) +
+                             (20 + sec7.size());
+      out.prepare(total, s3);
+      P.s3 = s3;
+      P.image_bytes = total;
+      P.tail_bytes = (20 + sec5.size()) + (20 + sec6.size()) + (20 + sec7.size());
+      P.valid = false;
+      E.prev_valid = false;
+      img = out.mutable_data();
+      std::memcpy(img, kImageMagic, 8);
+      put_at<uint32_t>(img + 8, kImageVersion);
+      put_at<uint32_t>(img + 12, kSectionCount);
+      uint64_t at = 16;
+      at += write_section(img + at, 1, sec1);
+      at += write_section(img + at, 2, sec2);
+      put_at<uint32_t>(img + at, 3);
+      put_at<uint32_t>(img + at + 4, 0);
+      put_at<uint64_t>(img + at + 8, P.len3);
+      // crc3 (patched by phase 2) and the empty UVM_PAGES header
+      put_at<uint32_t>(img + s3 + P.len3, 0);
+      put_at<uint32_t>(img + s3 + P.len3 + 4, 4);
+      put_at<uint32_t>(img + s3 + P.len3 + 8, 0);
+      put_at<uint64_t>(img + s3 + P.len3 + 12, 0);
+      at = s3 + P.stream_len + 4;
+      at += write_section(img + at, 5, sec5);
+      at += write_section(img + at, 6, sec6);
+      at += write_section(img + at, 7, sec7);
+      if (at != total) raise(Errc::DeviceFault, "image layout mismatch");
+      upload_plan(E, P, E.s_hash);
+      upload(E.d_pay_soff, P.pay_rec_off, E.s_hash);
+      check_cuda(cudaEventRecord(E.ev_t0, E.s_hash), "event");
+    }
+  }  // the application runs from here on
+  if (!eligible) {
+    checkpoint_image(session, out, stats);
+    return;
+  }
+  const bool aligned = std::all_of(P.pay_rec_off.begin(), P.pay_rec_off.end(),
+                                   [](uint64_t o) { return o % 16 == 0; });
+  uint8_t* stream = img + P.s3;  // page-locked host memory, written by the SMs over PCIe
+  check_cuda(cudaError_t(crac_hash_copy_range(E.d_pay_spans.ptr, E.d_pay_first.ptr,
+                                              uint32_t(P.pay_spans.size()), DrainEngine::kChunk, 0,
+                                              P.pay_first.back(), E.d_pay_crc.ptr, E.d_pay_soff.ptr,
+                                              stream, aligned ? 1 : 0, E.s_hash)),
+             "pre-copy hash+copy");
+  check_cuda(cudaError_t(crac_write_frames(E.d_recs.ptr, uint32_t(P.pay_spans.size()), stream,
+                                           E.s_hash)),
+             "pre-copy frames");
+  check_cuda(cudaEventRecord(E.ev_h1, E.s_hash), "event");
+  DrainEngine::Pending& Q = E.pending;
+  Q = DrainEngine::Pending{};
+  Q.precopy = true;
+  Q.out = &out;
+}
+
+void checkpoint_precopy_finish(Session& session, DrainStats* stats) {
+  DrainEngine& E = session.drain_engine();
+  if (!E.pending.precopy) {  // nothing in flight (or a synchronous fallback ran)
+    if (stats && E.pending.active) drain_finish(session, stats);
+    return;
+  }
+  PinnedImage& out = *E.pending.out;
+  double phase1 = 0;
+  precopy_wait(session, &phase1);
+  checkpoint_incremental(session, out, stats);
+  if (stats) {
+    stats->stall_ms = stats->total_ms;  // phase 2 runs with the gate held
+    stats->total_ms += phase1;
+    stats->shadow_bytes = 0;
+  }
 }
 
 }  // namespace cracsim

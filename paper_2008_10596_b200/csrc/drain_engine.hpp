@@ -183,6 +183,7 @@ struct DrainEngine {
     // app was stopped; written into the image after the shadow D2H lands
     std::vector<uint8_t> stash;
     std::vector<std::pair<uint64_t, uint32_t>> stash_at;  // (stream_off, len)
+    bool precopy = false;  // a pre-copy pass (checkpoint_precopy_begin) is in flight
   } pending;
 
   ImagePlan plan;

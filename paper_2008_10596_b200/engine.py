@@ -95,6 +95,8 @@ _SIGS = {
     "crac_checkpoint_finish": (C.c_int, [_P, C.POINTER(Stats)]),
     "crac_restart": (C.c_int, [_P, _U64, C.c_int, C.POINTER(_P), C.POINTER(Stats)]),
     "crac_decode_check": (C.c_int, [_P, _U64]),
+    "crac_checkpoint_precopy_begin": (C.c_int, [_P, _P, C.POINTER(Stats)]),
+    "crac_checkpoint_precopy_finish": (C.c_int, [_P, C.POINTER(Stats)]),
     "crac_reserve_shadow_on": (C.c_int, [_P, _U64, C.c_int]),
     "crac_crc32_host": (C.c_uint32, [_P, _U64, _U32]),
     "crac_stream_handle": (C.c_int, [_P, _U64, C.POINTER(_P)]),
@@ -334,6 +336,18 @@ class Session:
         _check(lib().crac_checkpoint_to_file(self._h, img._h, str(path).encode(), int(compress),
                                              C.byref(st), C.byref(io)))
         return st.as_dict(), io.as_dict()
+
+    def checkpoint_precopy_begin(self, image: Image) -> dict:
+        """Pre-copy the state into `image` while the application keeps running."""
+        st = Stats()
+        _check(lib().crac_checkpoint_precopy_begin(self._h, image._h, C.byref(st)))
+        return st.as_dict()
+
+    def checkpoint_precopy_finish(self) -> dict:
+        """Quiesce and re-send the chunks changed since the pre-copy."""
+        st = Stats()
+        _check(lib().crac_checkpoint_precopy_finish(self._h, C.byref(st)))
+        return st.as_dict()
 
     def reserve_shadow(self, nbytes: int, device: Optional[int] = None) -> None:
         """HBM the stall-reduced drain may stage the stream in (0 releases it);

@@ -614,6 +614,50 @@ def test_buddy_shadow_placement(eng):
     s.reserve_shadow(0)
 
 
+def test_precopy_drain_is_the_image_at_finish(eng):
+    """Pre-copy: the state changes while phase 1 copies it (a
+    device kernel rewriting ~10 % of the chunks, a host copy); the image is the
+    state at finish, and only the changed chunks were sent again."""
+    s = eng.Session(seed=9, arena_bytes=1 << 30)
+    workloads.build_regions(s, 6, lambda k: 24 * MIB + 4096 * k + 3 * k, seed=9)
+    img = eng.Image()
+    s.checkpoint_precopy_begin(img)
+    mutated = s.mutate(seed=2, epoch=1, threshold=(1 << 64) // 10)
+    first = s.live_records()[0].id
+    s.copy_h2d(first, 1000, b"\x42" * 5000)
+    st = s.checkpoint_precopy_finish()
+    assert st["incremental"] == 1
+    assert 0 < st["dirty_chunks"] < st["total_chunks"]
+    assert st["dirty_chunks"] <= mutated + 2
+    assert st["stall_ms"] <= st["total_ms"]
+    want = s.checkpoint()[0]
+    assert img.tobytes() == want
+    rs, _ = eng.restart(want)
+    assert rs.checkpoint()[0] == want
+
+
+def test_precopy_layout_change_and_ineligible_sessions(eng):
+    # an allocation during phase 1: finish falls back to a full drain
+    s = eng.Session(seed=3, arena_bytes=1 << 28)
+    workloads.build_regions(s, 3, lambda k: 8 * MIB + k, seed=3)
+    img = eng.Image()
+    s.checkpoint_precopy_begin(img)
+    i, _ = s.alloc(workloads.DEVICE, 3 * MIB)
+    s.fill_synthetic(i, 4)
+    st = s.checkpoint_precopy_finish()
+    assert st["incremental"] == 0
+    assert img.tobytes() == s.checkpoint()[0]
+    # pinned / managed allocations: begin drains synchronously, like the reference
+    s2 = eng.Session(seed=2, arena_bytes=1 << 22)
+    r2 = ref.RefSession(seed=2, arena_bytes=1 << 22)
+    for api in (s2, r2):
+        workloads.drive_small(api, seed=8)
+    img2 = eng.Image()
+    s2.checkpoint_precopy_begin(img2)
+    s2.checkpoint_precopy_finish()
+    assert img2.tobytes() == r2.checkpoint()[0]
+
+
 def test_async_drain_matches_reference_small(eng):
     s = eng.Session(seed=2, arena_bytes=1 << 22)
     r = ref.RefSession(seed=2, arena_bytes=1 << 22)
