@@ -705,10 +705,13 @@ constexpr uint64_t kDirectMinTiles = 4;
 
 void plan_direct_runs(ImagePlan& P, uint64_t limit, bool drain) {
   P.direct_runs.clear();
-  // CRAC_DIRECT = 0 | drain | refill | both (default): measurement knob
+  // CRAC_DIRECT = 0 | drain | refill (default) | both.  Measured on C4
+  // (tools/ab_direct2.sh, 3 rounds): the refill gains with direct H2D (55.0
+  // against 54.3 GB/s through the ring), the drain loses with direct D2H (54.0
+  // against 55.0), so only the refill uses them by default.
   static const int enabled = [] {
     const char* e = std::getenv("CRAC_DIRECT");
-    if (!e) return 3;
+    if (!e) return 2;
     if (!std::strcmp(e, "0")) return 0;
     if (!std::strcmp(e, "drain")) return 1;
     if (!std::strcmp(e, "refill")) return 2;
