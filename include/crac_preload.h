@@ -19,6 +19,8 @@
  *   CRAC_RESTART_FROM  image file: the session is restart_from_file'd at the
  *                      first intercepted call instead of created empty
  *   CRAC_CKPT_PATH     where SIGUSR2 writes a checkpoint (asynchronous trigger)
+ *   CRAC_PRECOPY       0: stop the application for the whole drain (default:
+ *                      a pre-copy drain stops it only to re-send what changed)
  *   CRAC_PRELOAD_VERBOSE  1: counters on stderr at exit
  *
  * Applications may call the functions below through dlsym(RTLD_DEFAULT, ...)

@@ -139,10 +139,25 @@ void rebuild_maps(State& g) {
   }
 }
 
+// The application is stopped only for the drain's gated phase: a pre-copy
+// (the state is copied while the application runs, then only what changed is
+// re-sent under the gate; sessions with pinned / managed memory drain
+// synchronously instead), then the file is written from the pinned image
+// while the application runs again.  CRAC_PRECOPY=0: a plain drain.
 int checkpoint_locked(State& g, const char* path) {
   const std::vector<uint8_t> wrapped = wrap_app_state(g);
   int rc = crac_set_app_state(g.s, wrapped.data(), wrapped.size());
-  if (rc == 0) rc = crac_checkpoint_to_file(g.s, g.img, path, 0, nullptr, nullptr);
+  const char* pc = std::getenv("CRAC_PRECOPY");
+  if (pc && !std::strcmp(pc, "0")) {
+    if (rc == 0) rc = crac_checkpoint_to_file(g.s, g.img, path, 0, nullptr, nullptr);
+  } else {
+    if (rc == 0) rc = crac_checkpoint_precopy_begin(g.s, g.img, nullptr);
+    if (rc == 0) rc = crac_checkpoint_precopy_finish(g.s, nullptr);
+    const uint8_t* data = nullptr;
+    uint64_t n = 0;
+    if (rc == 0) rc = crac_image_view(g.img, &data, &n);
+    if (rc == 0) rc = crac_file_write(path, data, n, 0, 0, 3, nullptr);  // O_DIRECT + fdatasync
+  }
   if (rc == 0) ++g.n_ckpt;
   return rc;
 }

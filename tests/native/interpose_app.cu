@@ -134,6 +134,52 @@ int spin(long ms) {
   return 0;
 }
 
+// Device memory only (the pre-copy path of the preload's checkpoint): a and
+// b rewritten with their own values on two streams for `ms` milliseconds.
+int devspin(long ms) {
+  cudaStream_t s1, s2;
+  CK(cudaStreamCreate(&s1));
+  CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  Saved sv{0x4445564f4e4cull, nullptr, nullptr, nullptr, nullptr, 43};
+  CK(cudaMalloc(&sv.a, kA * sizeof(float)));
+  CK(cudaMalloc(&sv.b, kB));
+  fill_a<<<148, 256, 0, s1>>>(sv.a, kA);
+  fill_b<<<148, 256, 0, s2>>>(sv.b, kB);
+  CK(cudaDeviceSynchronize());
+  auto set_state = hook<int (*)(const void*, uint64_t)>("crac_preload_set_app_state");
+  if (set_state && set_state(&sv, sizeof sv)) return 3;
+  std::printf("a=%p b=%p\nspinning\n", (void*)sv.a, (void*)sv.b);
+  std::fflush(stdout);
+  const auto t0 = std::chrono::steady_clock::now();
+  long iters = 0;
+  while (std::chrono::steady_clock::now() - t0 < std::chrono::milliseconds(ms)) {
+    fill_b<<<148, 256, 0, (iters & 1) ? s1 : s2>>>(sv.b, kB);
+    fill_a<<<148, 256, 0, (iters & 1) ? s2 : s1>>>(sv.a, kA);
+    if (++iters % 16 == 0) CK(cudaDeviceSynchronize());
+  }
+  CK(cudaDeviceSynchronize());
+  std::printf("spun %ld iterations\n", iters);
+  return 0;
+}
+
+int devresume() {
+  auto get_state = hook<int (*)(const void**, uint64_t*)>("crac_preload_app_state");
+  const void* p = nullptr;
+  uint64_t n = 0;
+  if (!get_state || get_state(&p, &n) || n != sizeof(Saved)) return 5;
+  Saved sv;
+  std::memcpy(&sv, p, sizeof sv);
+  if (sv.magic != 0x4445564f4e4cull || sv.step != 43) return 6;
+  unsigned long long* bad;
+  CK(cudaMalloc(&bad, sizeof *bad));
+  CK(cudaMemset(bad, 0, sizeof *bad));
+  count_bad<<<148, 256>>>(sv.a, kA, sv.b, kB, bad);
+  unsigned long long host_bad = 0;
+  CK(cudaMemcpy(&host_bad, bad, sizeof host_bad, cudaMemcpyDeviceToHost));
+  std::printf("resumed: device mismatches %llu\n", host_bad);
+  return host_bad ? 9 : 0;
+}
+
 int resume() {
   auto restarted = hook<int (*)()>("crac_preload_restarted");
   auto get_state = hook<int (*)(const void**, uint64_t*)>("crac_preload_app_state");
@@ -169,6 +215,8 @@ int main(int argc, char** argv) {
   if (argc >= 3 && !std::strcmp(argv[1], "run")) return run(argv[2]);
   if (argc >= 2 && !std::strcmp(argv[1], "resume")) return resume();
   if (argc >= 3 && !std::strcmp(argv[1], "spin")) return spin(std::atol(argv[2]));
+  if (argc >= 3 && !std::strcmp(argv[1], "devspin")) return devspin(std::atol(argv[2]));
+  if (argc >= 2 && !std::strcmp(argv[1], "devresume")) return devresume();
   std::fprintf(stderr, "usage: interpose_app run <image> | resume\n");
   return 1;
 }

@@ -145,3 +145,30 @@ def test_sigusr2_checkpoint_of_a_running_app(built, tmp_path):
     assert [x[1] for x in ours.payloads] == [a, b, h]  # quiesced: no torn kernel output
     r2 = _run(["resume"], LD_PRELOAD=PRELOAD, CRAC_RESTART_FROM=img)
     assert r2.returncode == 0, r2.stdout + r2.stderr
+
+
+def test_sigusr2_precopy_checkpoint_of_a_device_only_app(built, tmp_path):
+    """Device memory only: the preload's checkpoint is a pre-copy (the state
+    is copied while the application keeps rewriting it, then only what
+    changed is re-sent under the gate).  The image restarts into a process
+    that finds every byte, and the reference accepts it."""
+    import signal
+    import time
+    img = tmp_path / "dev.img"
+    e = dict(os.environ, LD_PRELOAD=str(PRELOAD), CRAC_ARENA_BYTES=str(ARENA),
+             CRAC_CKPT_PATH=str(img), CRAC_PRELOAD_VERBOSE="1")
+    p = subprocess.Popen([str(APP), "devspin", "4000"], env=e, stdout=subprocess.PIPE,
+                         stderr=subprocess.PIPE, text=True)
+    assert p.stdout.readline().startswith("a=")
+    assert p.stdout.readline().strip() == "spinning"
+    time.sleep(1.0)
+    p.send_signal(signal.SIGUSR2)
+    out, err = p.communicate(timeout=300)
+    assert p.returncode == 0, out + err
+    assert "checkpoints 1" in err, err
+    data = img.read_bytes()
+    ref.ref_decode_check(data)
+    a, b, _, _ = expected()
+    assert [x[1] for x in io.decode_image(data).payloads] == [a, b]
+    r2 = _run(["devresume"], LD_PRELOAD=PRELOAD, CRAC_RESTART_FROM=img)
+    assert r2.returncode == 0, r2.stdout + r2.stderr
