@@ -1395,13 +1395,14 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     binaries.emplace(b.handle, std::move(ks));
   }
 
-  std::set<uint64_t> live;
+  std::vector<uint64_t> live;
+  live.reserve(p.facts.active.size());
   {
     // map every live Device extent up front in coalesced runs, so the replay
     // itself makes no driver calls
     uint64_t run_lo = 0, run_hi = 0;
     for (const AllocationRecord& r : p.facts.active) {
-      live.insert(r.id);
+      live.push_back(r.id);
       if (r.kind != AllocationKind::Device) continue;
       const uint64_t lo = r.address, hi = r.address + round_up_align(r.size);
       if (run_hi && lo <= run_hi + (2ull << 20)) {
@@ -1524,7 +1525,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     plan(items);
     enqueue_data_path();
   }
-  ctx.begin_replay(std::move(live));
+  ctx.begin_replay(live);
   try {
     replay_log_into(ctx, p.log, &binaries, nullptr);
   } catch (...) {
