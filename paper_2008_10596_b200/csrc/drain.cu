@@ -4,24 +4,31 @@
 //         encode_image; the read_raw copies at ckpt_engine.cpp:49,54):
 //   host  : quiesce, small sections (META/LOG/STREAMS/APPSTATE/REGISTRY),
 //           record table of the bulk stream ALLOC_PAYLOADS||crc3||hdr4||UVM_PAGES
-//   GPU   : s_hash  K1 over every payload (64 KiB chunks) and managed page,
-//                   on all but kPackSMs SMs so the pack never waits for it
+//   GPU   : s_hash  K1 over every payload (64 KiB chunks) and every run of
+//                   device-resident managed pages, on all but kPackSMs SMs so
+//                   the pack never waits for it; K4 folds the section CRCs
 //           s_pack  pack kernel builds the exact stream bytes window by window
-//                   into a 4 x 64 MiB staging ring, copied out in 16 MiB pieces
-//           s_copy  D2H of each window into the pinned image (4 KiB aligned)
-//   host  : folds chunk CRCs with the frame CRCs into the section CRCs while
-//           the D2H drains, then patches crc3/crc4.
+//                   into a 4 x 64 MiB staging ring
+//           s_copy  D2H of each window into the pinned image (4 KiB aligned),
+//                   skipping host runs (plan_host_runs)
+//   host  : threads hash (PCLMUL CRC) and copy host-resident managed pages
+//           beside the window loop, then crc3/crc4 are patched.
 // Refill (replaces ref: src/image.cpp:280-345 decode + src/ckpt_engine.cpp:120-171):
 //   host  : strict parse of the framing, replay of the log (real backing only
-//           for allocations live at the end, pre-mapped in coalesced runs)
-//   GPU   : s_copy H2D windows (+16 B look-ahead) -> ring; s_pack scatter kernel
-//           writes every destination word (padding zero-filled), then K1
-//           re-hashes each region as soon as its last window has landed;
-//           managed residence via cudaMemPrefetchAsync
-//   host  : fold + compare against the stored CRCs -> ImageCorrupt on mismatch.
-// Incremental drain (new; the reference has none):
-//   K1 -> diff against the previous image's chunk CRCs -> ordered compaction
-//   -> the SMs write every dirty chunk straight into the pinned image.
+//           for allocations live at the end, pre-mapped in coalesced runs);
+//           Device-only images at the fixed VA start the data path first
+//   GPU   : s_copy H2D windows (+16 B look-ahead) -> ring, and direct H2D of
+//           big payload interiors straight into their allocations
+//           (plan_direct_runs); s_pack scatter kernel writes the rest (padding
+//           zero-filled), then K1 re-hashes regions in 2 GiB batches as their
+//           last window lands
+//   host  : threads write and hash host-resident managed pages (first touch
+//           restores residence), then fold + compare -> ImageCorrupt.
+// Incremental drain (new; the reference has none): K1 compares every chunk's
+//   CRC with the previous image's; writer CTAs copy the dirty chunks straight
+//   into the pinned image (crac_hash_drain_split).
+// Stall reduction (new): the HBM shadow (checkpoint_begin/finish) and the
+//   pre-copy drain (checkpoint_precopy_begin/finish).
 #include <cuda_runtime.h>
 
 #include <algorithm>
