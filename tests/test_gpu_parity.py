@@ -684,3 +684,55 @@ def test_async_then_incremental_and_implicit_finish(eng):
     assert img.tobytes() == s.checkpoint()[0]
     s.reserve_shadow(0)
     assert s.checkpoint_finish()["total_ms"] == 0  # nothing pending
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_random_mixed_paths_agree(eng, seed):
+    """Random Device layouts (sizes from 1 B to 40 MiB, so direct runs, edge
+    tiles and small payloads mix), random frees and mutations, then every
+    drain flavour on the same state: synchronous (== the reference's bytes),
+    incremental, shadow at a random size, pre-copy; each restart reproduces
+    the state."""
+    rnd = random.Random(seed)
+    s = eng.Session(seed=seed, arena_bytes=1 << 30)
+    r = ref.RefSession(seed=seed, arena_bytes=1 << 30)
+    ids = []
+    for k in range(40):
+        size = rnd.choice([1, 17, 4096, 65536 * 6 + rnd.randrange(1000), 3 * MIB + rnd.randrange(9999),
+                           rnd.randrange(1, 40 * MIB)])
+        pair = []
+        for api in (s, r):
+            i, _ = api.alloc(workloads.DEVICE, size)
+            api.fill_synthetic(i, seed * 100 + k)
+            pair.append(i)
+        ids.append(pair[0])
+        if k % 7 == 3:
+            victim = ids.pop(rnd.randrange(len(ids)))
+            s.free(victim)
+            r.free(victim)
+    want = r.checkpoint()[0]
+    img, _ = s.checkpoint()
+    assert img == want
+    rs, _ = eng.restart(img)
+    assert _state(rs) == _state(s)
+    # incremental after a mutation equals a fresh synchronous drain
+    image = eng.Image()
+    s.checkpoint_into(image)
+    s.mutate(seed=seed, epoch=1, threshold=(1 << 64) // 5)
+    st = s.checkpoint_into(image, incremental=True)
+    assert st["incremental"] == 1
+    sync = s.checkpoint()[0]
+    assert image.tobytes() == sync
+    # shadow drain of a random size, then a pre-copy racing a mutation
+    s.reserve_shadow(rnd.choice([0, 64, 128, 512]) * MIB)
+    s.checkpoint_begin(image)
+    s.checkpoint_finish()
+    assert image.tobytes() == sync
+    s.reserve_shadow(0)
+    s.checkpoint_precopy_begin(image)
+    s.mutate(seed=seed, epoch=2, threshold=(1 << 64) // 50)
+    s.checkpoint_precopy_finish()
+    final = s.checkpoint()[0]
+    assert image.tobytes() == final
+    rs2, _ = eng.restart(final)
+    assert rs2.checkpoint()[0] == final
