@@ -178,6 +178,10 @@ int crac_mutate_device(crac_session_t* s, uint64_t seed, uint64_t epoch, uint64_
  * session, chunk CRCs left on the device; stats.hash_ms / hash_bytes. */
 int crac_hash_session(crac_session_t* s, crac_stats_t* stats);
 
+/* Diagnostics: the CUDA runtime's pending (non-sticky) error of this library,
+ * without clearing it (cudaPeekAtLastError); 0 when none. */
+int crac_peek_cuda_error(void);
+
 /* Host CRC-32 the engine uses for host-resident pages and small sections
  * (zlib's crc32, bit-identical; PCLMUL folding).  No GPU needed. */
 uint32_t crac_crc32_host(const void* data, uint64_t n, uint32_t crc);

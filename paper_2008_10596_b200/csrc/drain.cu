@@ -785,9 +785,13 @@ void copy_direct(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, ui
     for (uint64_t c = d.lo; c < hi; c += kPiece) {
       const uint64_t n = std::min(kPiece, hi - c);
       uint8_t* dev = reinterpret_cast<uint8_t*>(d.dev + (c - d.lo));
-      check_cuda(d2h ? cudaMemcpyAsync(stream + c, dev, n, cudaMemcpyDeviceToHost, st)
-                     : cudaMemcpyAsync(dev, stream + c, n, cudaMemcpyHostToDevice, st),
-                 d2h ? "D2H direct" : "H2D direct");
+      const cudaError_t e = d2h ? cudaMemcpyAsync(stream + c, dev, n, cudaMemcpyDeviceToHost, st)
+                                : cudaMemcpyAsync(dev, stream + c, n, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess)
+        check_cuda(e, (std::string(d2h ? "D2H direct" : "H2D direct") + " [" + std::to_string(d.lo) +
+                       ", " + std::to_string(d.hi) + ") piece " + std::to_string(c) + "+" +
+                       std::to_string(n) + " dev " + std::to_string(uint64_t(dev)))
+                          .c_str());
     }
   }
 }
@@ -1406,12 +1410,17 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   live.reserve(p.facts.active.size());
   {
     // map every live Device extent up front in coalesced runs, so the replay
-    // itself makes no driver calls
-    uint64_t run_lo = 0, run_hi = 0;
+    // itself makes no driver calls (and the early data path below has its
+    // destinations).  Extents in address order: first fit hands out low
+    // addresses again after frees, so id order is not address order.
+    std::vector<std::pair<uint64_t, uint64_t>> ext;
     for (const AllocationRecord& r : p.facts.active) {
       live.push_back(r.id);
-      if (r.kind != AllocationKind::Device) continue;
-      const uint64_t lo = r.address, hi = r.address + round_up_align(r.size);
+      if (r.kind == AllocationKind::Device) ext.emplace_back(r.address, r.address + round_up_align(r.size));
+    }
+    std::sort(ext.begin(), ext.end());
+    uint64_t run_lo = 0, run_hi = 0;
+    for (const auto& [lo, hi] : ext) {
       if (run_hi && lo <= run_hi + (2ull << 20)) {
         run_hi = std::max(run_hi, hi);
       } else {

@@ -99,6 +99,7 @@ _SIGS = {
     "crac_checkpoint_precopy_finish": (C.c_int, [_P, C.POINTER(Stats)]),
     "crac_reserve_shadow_on": (C.c_int, [_P, _U64, C.c_int]),
     "crac_crc32_host": (C.c_uint32, [_P, _U64, _U32]),
+    "crac_peek_cuda_error": (C.c_int, []),
     "crac_stream_handle": (C.c_int, [_P, _U64, C.POINTER(_P)]),
     "crac_live_streams": (C.c_int, [_P, _U64, _PU64, _PU64]),
     "crac_gate_enter": (C.c_int, [_P]),

@@ -686,6 +686,30 @@ def test_async_then_incremental_and_implicit_finish(eng):
     assert s.checkpoint_finish()["total_ms"] == 0  # nothing pending
 
 
+def test_early_refill_with_address_gaps(eng):
+    """The refill's data path runs before the replay when the arena sits at
+    its logged VA: every live extent must be mapped up front even when id
+    order is not address order (first fit reuses low holes) and extents are
+    more than 2 MiB apart."""
+    s = eng.Session(seed=4, arena_bytes=1 << 30)
+    a = [s.alloc(workloads.DEVICE, 40 * MIB)[0] for _ in range(4)]
+    for i in a:
+        s.fill_synthetic(i, 1)
+    s.free(a[0])
+    s.free(a[2])
+    b, _ = s.alloc(workloads.DEVICE, 3 * MIB)  # lands in the low hole
+    s.fill_synthetic(b, 2)
+    c, _ = s.alloc(workloads.DEVICE, MIB + 7)
+    s.fill_synthetic(c, 3)
+    img, _ = s.checkpoint()
+    want = _state(s)
+    s.close()  # the restart takes the logged VA: Device-only, so the early path
+    rs, _ = eng.restart(img)
+    assert rs.fixed_va
+    assert _state(rs) == want
+    assert rs.checkpoint()[0] == img
+
+
 @pytest.mark.parametrize("seed", [1, 2, 3])
 def test_random_mixed_paths_agree(eng, seed):
     """Random Device layouts (sizes from 1 B to 40 MiB, so direct runs, edge
