@@ -763,3 +763,59 @@ def test_random_mixed_paths_agree(eng, seed):
     assert image.tobytes() == final
     rs2, _ = eng.restart(final)
     assert rs2.checkpoint()[0] == final
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_random_managed_and_pinned_paths_agree(eng, seed, tmp_path):
+    """Random managed allocations (residence set by random host / device
+    touches, long and short host runs, partial last pages), pinned and Device
+    payloads between them: synchronous drain == the reference's bytes; the
+    restart restores bytes and page flags; a shadow drain at a random size
+    with host and device page writes right after begin, and a file round
+    trip, agree with the synchronous image."""
+    rnd = random.Random(seed)
+    s = eng.Session(seed=seed, arena_bytes=512 * MIB)
+    r = ref.RefSession(seed=seed, arena_bytes=512 * MIB)
+    managed = []
+    for k in range(8):
+        kind = rnd.choice([workloads.MANAGED, workloads.MANAGED, workloads.PINNED, workloads.DEVICE])
+        size = rnd.choice([4096 * rnd.randrange(1, 64) + rnd.randrange(4096), rnd.randrange(1, 24 * MIB)])
+        ops = []
+        if kind == workloads.MANAGED:
+            for _ in range(rnd.randrange(1, 12)):
+                off = rnd.randrange(0, size)
+                n = min(size - off, rnd.choice([4096, 64 << 10, MIB, 3 * MIB]))
+                ops.append((off, n, rnd.choice([workloads.HOST_SIDE, workloads.DEVICE_SIDE])))
+        for api in (s, r):
+            i, _ = api.alloc(kind, size)
+            api.fill_synthetic(i, seed + k, rnd.choice([workloads.DEVICE_SIDE]) if kind == workloads.MANAGED
+                               else workloads.DEVICE_SIDE)
+            for off, n, side in ops:
+                if n > 0:
+                    api.page_read(i, off, n, side)
+        if kind == workloads.MANAGED:
+            managed.append(i)
+    want = r.checkpoint()[0]
+    img, _ = s.checkpoint()
+    assert img == want
+    rs, _ = eng.restart(img)
+    assert _state(rs) == _state(s)
+    assert rs.checkpoint()[0] == img
+    # shadow drain with writes racing the shadow D2H
+    image = eng.Image()
+    s.reserve_shadow(rnd.choice([64, 128, 512]) * MIB)
+    s.checkpoint_begin(image)
+    if managed:
+        m = managed[0]
+        s.page_write(m, 0, b"\x33" * 4096, workloads.HOST_SIDE)
+        s.page_write(m, 0, b"\x44" * 100, workloads.DEVICE_SIDE)
+    s.checkpoint_finish()
+    assert image.tobytes() == want
+    s.reserve_shadow(0)
+    # file round trip of the current state
+    now = s.checkpoint()[0]
+    p = tmp_path / "m.img"
+    s.checkpoint_to_file(p)
+    assert p.read_bytes() == now
+    back, _, _ = eng.restart_from_file(p)
+    assert back.checkpoint()[0] == now
