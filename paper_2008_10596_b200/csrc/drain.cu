@@ -1007,12 +1007,14 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   check_cuda(cudaEventRecord(E.ev_t0, E.s_pack), "event");
 
   const SnapshotMeta meta{ctx.seed(), ctx.arena_bytes(), kEngineVersion};
-  const std::vector<CallLogEntry> log = session.log().snapshot();
+  // the gate is held: the log cannot move, read it in place
+  const std::span<const CallLogEntry> log = session.log().quiesced_view();
   tr.mark("log-snapshot");
-  const std::vector<AllocationRecord> active = active_set(log);
+  active_set_into(log, E.scratch_active, E.scratch_alive);
+  const std::vector<AllocationRecord>& active = E.scratch_active;
   tr.mark("active-set");
   const std::vector<uint8_t> sec1 = meta_bytes(meta);
-  const std::vector<uint8_t> sec2 = log_bytes(log);
+  const uint64_t sec2_len = log.size() * kLogRecordBytes;
   const std::vector<uint8_t> sec5 = streams_bytes(ctx.live_stream_ids());
   const std::vector<uint8_t>& sec6 = session.app_state();
   const std::vector<uint8_t> sec7 = registry_bytes(ctx.registered_binaries());
@@ -1027,7 +1029,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   tr.mark("plan");
 
   // file layout: header | META | LOG | ALLOC hdr | stream | crc4 | STREAMS | APPSTATE | REGISTRY
-  const uint64_t s3 = 16 + (20 + sec1.size()) + (20 + sec2.size()) + 16;
+  const uint64_t s3 = 16 + (20 + sec1.size()) + (20 + sec2_len) + 16;
   const uint64_t total = s3 + P.stream_len + 4 + (20 + sec5.size()) + (20 + sec6.size()) +
                          (20 + sec7.size());
   out.prepare(total, s3);
@@ -1040,7 +1042,14 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   put_at<uint32_t>(img + 12, kSectionCount);
   uint64_t at = 16;
   at += write_section(img + at, 1, sec1);
-  at += write_section(img + at, 2, sec2);
+  {  // LOG, encoded in place
+    put_at<uint32_t>(img + at, 2);
+    put_at<uint32_t>(img + at + 4, 0);
+    put_at<uint64_t>(img + at + 8, sec2_len);
+    encode_log_into(img + at + 16, log);
+    put_at<uint32_t>(img + at + 16 + sec2_len, crc32_host(img + at + 16, sec2_len));
+    at += 20 + sec2_len;
+  }
   put_at<uint32_t>(img + at, 3);
   put_at<uint32_t>(img + at + 4, 0);
   put_at<uint64_t>(img + at + 8, P.len3);

@@ -187,6 +187,10 @@ struct DrainEngine {
   } pending;
 
   ImagePlan plan;
+  // host scratch of the drain prologue, reused (no page faults on fresh
+  // megabyte-sized vectors: C2's 40 k-entry log)
+  std::vector<AllocationRecord> scratch_active;
+  std::vector<uint8_t> scratch_alive;
   bool prev_valid = false;      // d_prev_crc holds the chunk CRCs of `plan`'s image
   uint64_t dst_for_image = 0;   // image the d_pay_dst table was built for
 

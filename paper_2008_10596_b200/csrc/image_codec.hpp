@@ -20,6 +20,8 @@ uint32_t crc32_fast(const uint8_t* p, size_t n, uint32_t crc = 0);
 
 std::vector<uint8_t> meta_bytes(const SnapshotMeta& m);
 std::vector<uint8_t> log_bytes(std::span<const CallLogEntry> log);
+// The LOG payload encoded straight into `dst` (kLogRecordBytes per entry).
+void encode_log_into(uint8_t* dst, std::span<const CallLogEntry> log);
 std::vector<uint8_t> streams_bytes(std::span<const uint64_t> streams);
 std::vector<uint8_t> registry_bytes(std::span<const BinaryInfo> binaries);
 
