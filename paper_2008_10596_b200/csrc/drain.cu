@@ -602,12 +602,25 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
   P.stream_len = pos;
   const uint64_t tiles = (pos + CRAC_TILE_BYTES - 1) / CRAC_TILE_BYTES;
   P.tile_rec.resize(tiles);
-  parallel_for(tiles, [&](uint64_t t) {  // last record starting at or before the tile
-    const uint64_t start = t * CRAC_TILE_BYTES;
-    const auto it = std::upper_bound(P.recs.begin(), P.recs.end(), start,
-                                     [](uint64_t v, const crac_record_t& r) { return v < r.out_off; });
-    P.tile_rec[t] = uint32_t((it - P.recs.begin()) - 1);
-  });
+  // last record starting at or before each tile: one sequential merge of the
+  // two sorted lists for small streams (C2), a parallel binary search per
+  // tile for big ones (C3's 4 M page records, C4's 2 M tiles)
+  if (tiles < 65536) {
+    size_t r = 0;
+    const size_t nr = P.recs.size();
+    for (uint64_t t = 0; t < tiles; ++t) {
+      const uint64_t start = t * CRAC_TILE_BYTES;
+      while (r + 1 < nr && P.recs[r + 1].out_off <= start) ++r;
+      P.tile_rec[t] = uint32_t(r);
+    }
+  } else {
+    parallel_for(tiles, [&](uint64_t t) {
+      const uint64_t start = t * CRAC_TILE_BYTES;
+      const auto it = std::upper_bound(P.recs.begin(), P.recs.end(), start,
+                                       [](uint64_t v, const crac_record_t& r) { return v < r.out_off; });
+      P.tile_rec[t] = uint32_t((it - P.recs.begin()) - 1);
+    });
+  }
 }
 
 template <typename D, typename H>
