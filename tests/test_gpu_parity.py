@@ -819,3 +819,30 @@ def test_random_managed_and_pinned_paths_agree(eng, seed, tmp_path):
     assert p.read_bytes() == now
     back, _, _ = eng.restart_from_file(p)
     assert back.checkpoint()[0] == now
+
+
+@pytest.mark.parametrize("seed", [21, 22])
+def test_random_churn_paths_agree(eng, seed):
+    """C2-shaped churn (random 256 B-64 KiB allocations and frees, fill8
+    launches on 4 streams): the image equals the reference's; a restart
+    (early data path when the VA is free) reproduces it; incremental and
+    pre-copy drains after more launches equal the synchronous drain."""
+    calls = 1500 + 500 * (seed % 3)
+    s = eng.Session(seed=seed, arena_bytes=64 * MIB)
+    r = ref.RefSession(seed=seed, arena_bytes=64 * MIB)
+    for api in (s, r):
+        workloads.build_churn(api, calls, seed)
+    img, _ = s.checkpoint()
+    assert img == r.checkpoint()[0]
+    rs, _ = eng.restart(img)
+    assert rs.checkpoint()[0] == img
+    image = eng.Image()
+    s.checkpoint_into(image)
+    s.mutate(seed=seed, epoch=3, threshold=(1 << 64) // 3)
+    st = s.checkpoint_into(image, incremental=True)
+    assert st["incremental"] == 1
+    assert image.tobytes() == s.checkpoint()[0]
+    s.checkpoint_precopy_begin(image)
+    s.mutate(seed=seed, epoch=4, threshold=(1 << 64) // 7)
+    s.checkpoint_precopy_finish()
+    assert image.tobytes() == s.checkpoint()[0]

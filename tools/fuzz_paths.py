@@ -14,7 +14,8 @@ bad = 0
 for seed in range(first, first + count):
     for name, fn in (("device", lambda sd: T.test_random_mixed_paths_agree(eng, sd)),
                      ("managed", lambda sd: T.test_random_managed_and_pinned_paths_agree(
-                         eng, sd, Path(tempfile.mkdtemp())))):
+                         eng, sd, Path(tempfile.mkdtemp()))),
+                     ("churn", lambda sd: T.test_random_churn_paths_agree(eng, sd))):
         try:
             fn(seed)
         except Exception as e:  # noqa: BLE001
