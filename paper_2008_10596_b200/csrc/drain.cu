@@ -821,6 +821,11 @@ uint64_t host_run_bytes(const ImagePlan& P) {
 void copy_window(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, uint8_t* buf,
                  uint8_t* stream, bool d2h, cudaStream_t st) {
   const auto& R = P.skip_runs;
+  // ring window pieces (CRAC_COPY_CHUNK_MIB, default DrainEngine::kCopyChunk)
+  static const uint64_t piece = [] {
+    const char* e = std::getenv("CRAC_COPY_CHUNK_MIB");
+    return e ? uint64_t(std::max(1, std::atoi(e))) << 20 : DrainEngine::kCopyChunk;
+  }();
   thread_local std::vector<void*> dsts, srcs;
   thread_local std::vector<size_t> sizes;
   dsts.clear();
@@ -839,8 +844,8 @@ void copy_window(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, ui
     // H2D: 16 bytes past a gap that a skip run ends, for the scatter's
     // straddling last word (ring bytes under a skip run are never read else)
     const uint64_t bc = d2h ? b : std::min(end, b + 16);
-    for (uint64_t c = a; c < bc; c += DrainEngine::kCopyChunk) {
-      const uint64_t n = std::min(DrainEngine::kCopyChunk, bc - c);
+    for (uint64_t c = a; c < bc; c += piece) {
+      const uint64_t n = std::min(piece, bc - c);
       dsts.push_back(d2h ? static_cast<void*>(stream + c) : static_cast<void*>(buf + (c - off)));
       srcs.push_back(d2h ? static_cast<void*>(buf + (c - off)) : static_cast<void*>(stream + c));
       sizes.push_back(n);
