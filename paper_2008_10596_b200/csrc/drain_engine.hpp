@@ -129,7 +129,7 @@ struct ImagePlan {
 struct DrainEngine {
   static constexpr int kSlots = 4;
   static constexpr uint64_t kWindow = 64ull << 20;     // pack/scatter launch (multiple of 64 KiB)
-  static constexpr uint64_t kCopyChunk = 64ull << 20;  // D2H/H2D piece: a whole window (tools/ab_piece.sh)
+  static constexpr uint64_t kCopyChunk = 16ull << 20;  // D2H/H2D piece (tools/ab_piece.sh: box-dependent, 16 MiB never the outlier)
   static constexpr uint32_t kChunk = 65536;         // payload hash chunk
   static constexpr uint32_t kPageChunk = 4096;      // managed hash chunk (= page)
   static constexpr int kPackSMs = 16;               // SMs K1 leaves to the pack during a drain
