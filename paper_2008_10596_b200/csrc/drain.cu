@@ -1112,6 +1112,32 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   plan_host_runs(P, P.stream_len);
   plan_direct_runs(P, head, true);  // only where the app stays stopped until they land
 
+  const uint64_t windows = (head + W - 1) / W;
+  Q.windows = windows;
+  if (stats) E.ensure_window_events(windows);
+  const bool land_events = !P.host_pages.empty();
+  if (land_events) E.ensure_land_events(windows);
+  // host-resident pages: hashed (all) and copied by host threads from now
+  // on, beside the plan upload, K1 and the window loop (long runs at once;
+  // short ring-part runs after their window has landed)
+  std::atomic<int64_t> recorded{-1};
+  std::exception_ptr host_err;
+  std::thread host_pass([&] {
+    try {
+      host_pages_drain(E, P, img + s3, head, recorded);
+    } catch (...) {
+      host_err = std::current_exception();
+    }
+  });
+  struct Joiner {
+    std::thread& t;
+    std::atomic<int64_t>& r;
+    ~Joiner() {
+      r.store(INT64_MAX);  // unblock waiters if the loop throws
+      if (t.joinable()) t.join();
+    }
+  } join_host{host_pass, recorded};
+
   // With the whole stream in the shadow, K1 copies every payload chunk to
   // its stream position right after hashing it: one HBM read of the state
   // instead of two; frames and the UVM_PAGES part are written beside it.
@@ -1155,31 +1181,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
                "pack shadow");
   }
 
-  const uint64_t windows = (head + W - 1) / W;
-  Q.windows = windows;
-  if (stats) E.ensure_window_events(windows);
-  const bool land_events = !P.host_pages.empty();
-  if (land_events) E.ensure_land_events(windows);
   check_cuda(cudaEventRecord(E.ev_c0, E.s_pack), "event");
-  // host-resident pages: hashed (all) and copied by host threads beside the
-  // window loop (long runs at once; short ring-part runs after their window)
-  std::atomic<int64_t> recorded{-1};
-  std::exception_ptr host_err;
-  std::thread host_pass([&] {
-    try {
-      host_pages_drain(E, P, img + s3, head, recorded);
-    } catch (...) {
-      host_err = std::current_exception();
-    }
-  });
-  struct Joiner {
-    std::thread& t;
-    std::atomic<int64_t>& r;
-    ~Joiner() {
-      r.store(INT64_MAX);  // unblock waiters if the loop throws
-      if (t.joinable()) t.join();
-    }
-  } join_host{host_pass, recorded};
   size_t run_i = 0, krun_i = 0, drun_i = 0;
   std::vector<std::pair<uint64_t, uint64_t>> kr;
   for (uint64_t w = 0; w < windows; ++w) {
