@@ -660,10 +660,9 @@ __device__ __forceinline__ void keep_prefix(uint4& v, uint32_t valid) {
   v.w &= mask(3);
 }
 
-constexpr int kPackThreads = 256;
+constexpr int kPackThreads = 512;
 constexpr uint32_t kSubTile = 512;
 constexpr uint32_t kTileWords = CRAC_TILE_BYTES / 16;             // 4096
-constexpr uint32_t kWordsPerThread = kTileWords / kPackThreads;   // 16
 
 __device__ __forceinline__ uint4 shfl_down4(uint4 v, int d) {
   v.x = __shfl_down_sync(0xFFFFFFFFu, v.x, d);
@@ -677,28 +676,30 @@ __device__ __forceinline__ uint4 shfl_down4(uint4 v, int d) {
 // 16-byte-aligned source `src` (shift 0..15 uniform).  Thread t owns words
 // t, t + 256, ... (coalesced); all loads are issued before any store, and
 // the upper half of a misaligned word comes from the neighbouring lane.
+template <uint32_t kThreads>
 __device__ __forceinline__ void tile_copy(uint4* __restrict__ dst, const uint4* __restrict__ src,
                                           uint32_t nwords, uint32_t shift) {
   const uint32_t lane = threadIdx.x & 31;
-  uint4 lo[kWordsPerThread];
+  constexpr uint32_t kWords = kTileWords / kThreads;  // per thread
+  uint4 lo[kWords];
 #pragma unroll
-  for (uint32_t k = 0; k < kWordsPerThread; ++k) {
-    const uint32_t w = threadIdx.x + k * kPackThreads;
+  for (uint32_t k = 0; k < kWords; ++k) {
+    const uint32_t w = threadIdx.x + k * kThreads;
     // one word past the end when misaligned: it is the upper half of the
     // last word, inside the source's 16-byte-rounded extent
     if (w < nwords || (shift && w == nwords)) lo[k] = ldg_stream(src + w);
   }
   if (shift == 0) {
 #pragma unroll
-    for (uint32_t k = 0; k < kWordsPerThread; ++k) {
-      const uint32_t w = threadIdx.x + k * kPackThreads;
+    for (uint32_t k = 0; k < kWords; ++k) {
+      const uint32_t w = threadIdx.x + k * kThreads;
       if (w < nwords) dst[w] = lo[k];
     }
     return;
   }
 #pragma unroll
-  for (uint32_t k = 0; k < kWordsPerThread; ++k) {
-    const uint32_t w = threadIdx.x + k * kPackThreads;
+  for (uint32_t k = 0; k < kWords; ++k) {
+    const uint32_t w = threadIdx.x + k * kThreads;
     uint4 hi = shfl_down4(lo[k], 1);
     if (lane == 31 && w < nwords) hi = ldg_stream(src + w + 1);
     if (w < nwords) dst[w] = shift16(lo[k], hi, shift);
@@ -743,7 +744,7 @@ __global__ void __launch_bounds__(kPackThreads)
         return;
       }
       const uint64_t rel = tile0 - P;
-      tile_copy(reinterpret_cast<uint4*>(dst + (tile0 - win_off)),
+      tile_copy<kPackThreads>(reinterpret_cast<uint4*>(dst + (tile0 - win_off)),
                 reinterpret_cast<const uint4*>(R.ptr) + (rel >> 4),
                 uint32_t((tile1 - tile0 + 15) >> 4), uint32_t(rel & 15));
       return;
@@ -818,7 +819,7 @@ __global__ void __launch_bounds__(kPackThreads)
       const uint64_t d0 = (tile0 - P + 15) >> 4;                 // first dest word
       const uint64_t d1 = (tile1 - P + 15) >> 4;                 // one past the last
       const uint64_t f0 = P + 16 * d0 - win_off;                 // its window offset
-      tile_copy(reinterpret_cast<uint4*>(R.ptr) + d0,
+      tile_copy<kPackThreads>(reinterpret_cast<uint4*>(R.ptr) + d0,
                 reinterpret_cast<const uint4*>(win) + (f0 >> 4), uint32_t(d1 - d0),
                 uint32_t(f0 & 15));
       return;
@@ -1032,7 +1033,8 @@ __global__ void __launch_bounds__(kGatherThreads)
     uint8_t* dst = host + dst_off[s] + off;
     if ((reinterpret_cast<uint64_t>(dst) & 15) == 0 && len == kTileWords * 16) {
       // aligned full chunk: every load in flight before the PCIe stores
-      tile_copy(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), kTileWords, 0);
+      tile_copy<kGatherThreads>(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src),
+                                kTileWords, 0);
       continue;
     }
     const uint32_t head = uint32_t((16 - (reinterpret_cast<uint64_t>(dst) & 15)) & 15);
