@@ -5,7 +5,7 @@ NCU=/usr/local/cuda/bin/ncu
 OUT=gpurun_out/r01e
 mkdir -p $OUT
 timeout 900 $NCU --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k regex:"k1_chunk_crc<16, 4>" -c 1 -o $OUT/prof_k1_split_drain \
+  -k regex:"k1_chunk_crc<\\(int\\)16, \\(int\\)4>" -c 1 -o $OUT/prof_k1_split_drain \
   python bench.py --workload c5 --c5-footprint-gib 8 --steps 1 --warmup 0 --no-stall \
   > $OUT/prof_k1_split_drain.log 2>&1
 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_pack_records -s 40 -c 1 \
