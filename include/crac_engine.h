@@ -85,7 +85,7 @@ int crac_checkpoint_incremental(crac_session_t* s, crac_image_t* img, crac_stats
  * into `img` continues after crac_checkpoint_begin returns and
  * crac_checkpoint_finish completes it.  Bytes equal crac_checkpoint's at the
  * instant of begin.  crac_reserve_shadow(s, 0) releases the reservation;
- * OutOfArena (1 + 8) if the HBM is not available. */
+ * OutOfArena (1 + 1) if the HBM is not available. */
 int crac_reserve_shadow(crac_session_t* s, uint64_t bytes);
 /* The shadow in another GPU's HBM (SURVEY §8f.3 buddy copy): reachable by
  * peer access (InvalidArgument otherwise); `device` = this session's GPU is
