@@ -104,3 +104,69 @@ def test_preload_exports_its_api_and_interposers(so):
     assert not [ln for ln in eng.splitlines() if " T cuda" in ln]
     needed = subprocess.run(["readelf", "-d", str(pre)], capture_output=True, text=True).stdout
     assert "libcrac_b200.so" in needed
+
+
+def test_host_codec_payload_frames_match_reference(so):
+    """ALLOC_PAYLOADS frames are validated at offsets computed from the log
+    (parse_payload_frames' fast path).  Frames tampered so that only the frame
+    check can catch them (the section CRC re-sealed) are rejected exactly when
+    the reference's sequential walk rejects them (ref: image.cpp:175-197)."""
+    import random
+    import struct
+    import sys
+    import zlib
+    sys.path.insert(0, str(ROOT))
+    from oracle import ref
+    s = ref.RefSession(seed=3, arena_bytes=1 << 26)
+    rng = random.Random(5)
+    ids = []
+    for k in range(60):
+        if ids and rng.random() < 0.3:
+            s.free(ids.pop(rng.randrange(len(ids))))
+        else:
+            i, _ = s.alloc(1, 256 * (1 + rng.randrange(16)))
+            ids.append(i)
+    img, _ = s.checkpoint()
+    so.decode_check(img)
+    ref.ref_decode_check(img)
+    # section 3 (ALLOC_PAYLOADS): walk to it, then list its frames
+    at = 16
+    for _ in range(2):
+        at += 20 + struct.unpack_from("<Q", img, at + 8)[0]
+    s3, l3 = at + 16, struct.unpack_from("<Q", img, at + 8)[0]
+    frames, p = [], s3
+    while p < s3 + l3:
+        frames.append(p)
+        p += 16 + struct.unpack_from("<Q", img, p + 8)[0]
+    assert len(frames) >= 20
+
+    def seal(b):
+        struct.pack_into("<I", b, s3 + l3, zlib.crc32(bytes(b[s3:s3 + l3])))
+        return bytes(b)
+
+    cases = []
+    for f in (frames[0], frames[len(frames) // 2], frames[-1]):
+        for field, delta in ((0, 1), (0, -1), (8, 256), (8, -256), (8, 1)):
+            b = bytearray(img)
+            v = struct.unpack_from("<Q", b, f + field)[0]
+            struct.pack_into("<Q", b, f + field, (v + delta) % (1 << 64))
+            cases.append(seal(b))
+    # two frames swapped (same total length)
+    b = bytearray(img)
+    a0, a1 = frames[1], frames[2]
+    b[a0:a0 + 16], b[a1:a1 + 16] = img[a1:a1 + 16], img[a0:a0 + 16]
+    cases.append(seal(b))
+    for c in cases:
+        try:
+            ref.ref_decode_check(c)
+            ref_ok = True
+        except ref.RefError:
+            ref_ok = False
+        try:
+            so.decode_check(c)
+            ours_ok = True
+        except so.CracError as e:
+            assert e.errc == "ImageCorrupt"
+            ours_ok = False
+        assert ours_ok == ref_ok
+        assert not ours_ok
