@@ -1435,6 +1435,52 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     binaries.emplace(b.handle, std::move(ks));
   }
 
+  // With the arena at its logged VA and only Device allocations live, every
+  // destination is the logged address itself: the H2D / scatter / verify
+  // pipeline starts before the replay and the replay (host bookkeeping only,
+  // the extents are pre-mapped) runs beside it, then vouches for the
+  // addresses.  Otherwise the data path waits for the replayed backings.
+  const bool early = ctx.fixed_va() && !p.facts.active.empty() &&
+                     std::all_of(p.facts.active.begin(), p.facts.active.end(),
+                                 [](const AllocationRecord& r) {
+                                   return r.kind == AllocationKind::Device;
+                                 });
+  ImagePlan& P = E.plan;
+  const uint64_t s3 = p.sec[2].payload_off;
+  auto plan = [&](const std::vector<BulkItem>& items) {
+    build_plan(items, P);
+    plan_host_runs(P, P.stream_len);
+    plan_direct_runs(P, P.stream_len, false);
+    P.log_len = p.log.size();
+    if (P.len3 != p.sec[2].length || P.len4 != p.sec[3].length ||
+        s3 + P.stream_len != p.sec[3].payload_off + p.sec[3].length)
+      raise(Errc::ImageCorrupt, "bulk sections do not match the log's active set");
+  };
+  // early: the plan (host work only) is built on a thread beside the premap
+  // (driver work only); the data path is enqueued once both are done
+  std::vector<BulkItem> early_items;
+  std::exception_ptr plan_err;
+  std::thread early_plan;
+  struct PlanJoiner {
+    std::thread& t;
+    ~PlanJoiner() {
+      if (t.joinable()) t.join();
+    }
+  } plan_joiner{early_plan};
+  if (early) {
+    early_items.reserve(p.facts.active.size());
+    for (const AllocationRecord& rec : p.facts.active)
+      early_items.push_back(BulkItem{rec.id, rec.kind, rec.size, rec.address, nullptr});
+    early_plan = std::thread([&, dev = E.device] {
+      try {
+        cudaSetDevice(dev);  // the record table may grow (pinned)
+        plan(early_items);
+      } catch (...) {
+        plan_err = std::current_exception();
+      }
+    });
+  }
+
   std::vector<uint64_t> live;
   live.reserve(p.facts.active.size());
   {
@@ -1462,28 +1508,6 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   }
   tr.mark("premap");
 
-  // With the arena at its logged VA and only Device allocations live, every
-  // destination is the logged address itself: the H2D / scatter / verify
-  // pipeline starts before the replay and the replay (host bookkeeping only,
-  // the extents are pre-mapped) runs beside it, then vouches for the
-  // addresses.  Otherwise the data path waits for the replayed backings.
-  const bool early = ctx.fixed_va() && !p.facts.active.empty() &&
-                     std::all_of(p.facts.active.begin(), p.facts.active.end(),
-                                 [](const AllocationRecord& r) {
-                                   return r.kind == AllocationKind::Device;
-                                 });
-  ImagePlan& P = E.plan;
-  const uint64_t s3 = p.sec[2].payload_off;
-  auto plan = [&](const std::vector<BulkItem>& items) {
-    build_plan(items, P);
-    plan_host_runs(P, P.stream_len);
-    plan_direct_runs(P, P.stream_len, false);
-    P.log_len = p.log.size();
-    if (P.len3 != p.sec[2].length || P.len4 != p.sec[3].length ||
-        s3 + P.stream_len != p.sec[3].payload_off + p.sec[3].length)
-      raise(Errc::ImageCorrupt, "bulk sections do not match the log's active set");
-    tr.mark("plan");
-  };
   uint64_t windows = 0, verifies = 0, scattered = 0;
   // enqueues H2D windows -> scatter -> K1 verify (payloads as their regions
   // complete, then the device-resident pages); nothing here waits
@@ -1564,10 +1588,9 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   };
 
   if (early) {
-    std::vector<BulkItem> items;
-    for (const AllocationRecord& rec : p.facts.active)
-      items.push_back(BulkItem{rec.id, rec.kind, rec.size, rec.address, nullptr});
-    plan(items);
+    early_plan.join();
+    if (plan_err) std::rethrow_exception(plan_err);
+    tr.mark("plan");
     enqueue_data_path();
   }
   ctx.begin_replay(live);
@@ -1604,7 +1627,10 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     items.push_back(it);
   }
   tr.mark("items");
-  if (!early) plan(items);
+  if (!early) {
+    plan(items);
+    tr.mark("plan");
+  }
 
   // managed pages land where they were: device-resident ones are first
   // touched by the scatter kernel (and verified by K1), host-resident ones
