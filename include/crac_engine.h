@@ -182,6 +182,11 @@ int crac_hash_session(crac_session_t* s, crac_stats_t* stats);
  * without clearing it (cudaPeekAtLastError); 0 when none. */
 int crac_peek_cuda_error(void);
 
+/* Frees the mapped arena a closed session left on `device` (-1: the current
+ * one) for the next session of the same size to adopt.  The next restart
+ * then maps its physical memory afresh, as in a new process (a cold restart). */
+int crac_drop_arena_cache(int device);
+
 /* Host CRC-32 the engine uses for host-resident pages and small sections
  * (zlib's crc32, bit-identical; PCLMUL folding).  No GPU needed. */
 uint32_t crac_crc32_host(const void* data, uint64_t n, uint32_t crc);

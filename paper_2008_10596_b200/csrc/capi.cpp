@@ -370,6 +370,14 @@ int crac_file_read(const char* path, void* dst, uint64_t capacity, uint32_t thre
 
 int crac_peek_cuda_error(void) { return int(cudaPeekAtLastError()); }
 
+int crac_drop_arena_cache(int device) {
+  return guard([&] {
+    int dev = device;
+    if (dev < 0) check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    drop_arena_cache(dev);
+  });
+}
+
 uint32_t crac_crc32_host(const void* data, uint64_t n, uint32_t crc) {
   return codec::crc32_fast(static_cast<const uint8_t*>(data), n, crc);
 }

@@ -100,6 +100,7 @@ _SIGS = {
     "crac_reserve_shadow_on": (C.c_int, [_P, _U64, C.c_int]),
     "crac_crc32_host": (C.c_uint32, [_P, _U64, _U32]),
     "crac_peek_cuda_error": (C.c_int, []),
+    "crac_drop_arena_cache": (C.c_int, [C.c_int]),
     "crac_stream_handle": (C.c_int, [_P, _U64, C.POINTER(_P)]),
     "crac_live_streams": (C.c_int, [_P, _U64, _PU64, _PU64]),
     "crac_gate_enter": (C.c_int, [_P]),
@@ -501,6 +502,12 @@ def read_file(path, threads: int = 0, chunk_bytes: int = 0, direct: bool = True,
     _check(lib().crac_file_read(str(path).encode(), C.c_void_p(base), cap - offset, threads,
                                 chunk_bytes, int(direct), C.byref(got), C.byref(io)))
     return C.string_at(base, got.value), io.as_dict()
+
+
+def drop_arena_cache(device: int = -1) -> None:
+    """Frees the arena a closed session left cached on `device`: the next
+    restart maps its memory afresh, as a restart in a new process does."""
+    _check(lib().crac_drop_arena_cache(device))
 
 
 def decode_check(image) -> None:
