@@ -846,3 +846,30 @@ def test_random_churn_paths_agree(eng, seed):
     s.mutate(seed=seed, epoch=4, threshold=(1 << 64) // 7)
     s.checkpoint_precopy_finish()
     assert image.tobytes() == s.checkpoint()[0]
+
+
+def test_cold_restart_after_dropping_the_arena_cache(eng):
+    """A restart after crac_drop_arena_cache maps its physical memory afresh
+    (as in a new process) and reproduces the state and the image; so does a
+    warm restart that adopts the cached arena."""
+    import gc
+    gc.collect()
+    s = eng.Session(seed=8, arena_bytes=1 << 30)
+    ids = [s.alloc(workloads.DEVICE, sz)[0] for sz in (5 * MIB + 3, 64 * 1024, 17, 9 * MIB)]
+    for k, i in enumerate(ids):
+        s.fill_synthetic(i, 40 + k)
+    s.free(ids[1])
+    img, _ = s.checkpoint()
+    want = _state(s)
+    s.close()
+    eng.drop_arena_cache()
+    cold, _ = eng.restart(img)
+    assert _state(cold) == want
+    assert cold.checkpoint()[0] == img
+    cold.close()  # its arena is cached again: the next restart adopts it
+    warm, _ = eng.restart(img)
+    assert _state(warm) == want
+    assert warm.checkpoint()[0] == img
+    warm.close()
+    eng.drop_arena_cache()
+    eng.drop_arena_cache()  # nothing cached: a no-op
