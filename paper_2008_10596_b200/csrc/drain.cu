@@ -460,29 +460,34 @@ struct BulkItem {
 
 void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
   PhaseTrace tr("  plan");
-  P.recs.clear();
-  P.pay_spans.clear();
   P.page_spans.clear();
-  P.pay_first.assign(1, 0);
   P.page_first.assign(1, 0);
-  P.pay_rec_off.clear();
-  P.pay_kind.clear();
-  P.log_sizes.clear();
-  {  // one allocation for the whole record table
-    uint64_t n = 1;
-    for (const BulkItem& it : items)
-      n += it.kind == AllocationKind::Managed ? 1 + page_count_for(it.size) : 1;
-    P.recs.reserve(n);
-  }
-  uint64_t pos = 0, len4 = 0;
+  // every payload array sized once and filled by index (C2: 16 k payloads)
+  uint64_t n_pay = 0, n_recs = 1;
   for (const BulkItem& it : items) {
-    P.log_sizes.push_back(it.id);
-    P.log_sizes.push_back(it.size);
+    const bool managed = it.kind == AllocationKind::Managed;
+    n_pay += !managed;
+    n_recs += managed ? 1 + page_count_for(it.size) : 1;
+  }
+  P.recs.reserve(n_recs);  // one allocation for the whole record table
+  P.recs.resize(n_pay);
+  P.pay_spans.resize(n_pay);
+  P.pay_first.resize(n_pay + 1);
+  P.pay_first[0] = 0;
+  P.pay_rec_off.resize(n_pay);
+  P.pay_kind.resize(n_pay);
+  P.log_sizes.resize(2 * items.size());
+  uint64_t pos = 0, len4 = 0, k = 0, first = 0;
+  for (size_t j = 0; j < items.size(); ++j) {
+    const BulkItem& it = items[j];
+    P.log_sizes[2 * j] = it.id;
+    P.log_sizes[2 * j + 1] = it.size;
     if (it.kind == AllocationKind::Managed) {
       len4 += 16 + 16 * page_count_for(it.size) + it.size;
       continue;
     }
-    crac_record_t r{};
+    crac_record_t& r = P.recs[k];
+    r = crac_record_t{};
     r.out_off = pos;
     r.ptr = it.ptr;
     r.len = it.size;
@@ -490,13 +495,13 @@ void build_plan(const std::vector<BulkItem>& items, ImagePlan& P) {
     r.frame_len = 16;
     std::memcpy(r.frame, &it.id, 8);
     std::memcpy(r.frame + 8, &it.size, 8);
-    P.recs.push_back(r);
-    P.pay_spans.push_back(crac_span_t{it.ptr, it.size});
-    P.pay_first.push_back(P.pay_first.back() +
-                          (it.size + DrainEngine::kChunk - 1) / DrainEngine::kChunk);
-    P.pay_rec_off.push_back(pos + 16);
-    P.pay_kind.push_back(uint8_t(it.kind));
+    P.pay_spans[k] = crac_span_t{it.ptr, it.size};
+    first += (it.size + DrainEngine::kChunk - 1) / DrainEngine::kChunk;
+    P.pay_first[k + 1] = first;
+    P.pay_rec_off[k] = pos + 16;
+    P.pay_kind[k] = uint8_t(it.kind);
     pos += 16 + it.size;
+    ++k;
   }
   P.len3 = pos;
   P.len4 = len4;
