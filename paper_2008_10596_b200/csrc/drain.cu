@@ -1127,13 +1127,15 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   // short ring-part runs after their window has landed)
   std::atomic<int64_t> recorded{-1};
   std::exception_ptr host_err;
-  std::thread host_pass([&] {
-    try {
-      host_pages_drain(E, P, img + s3, head, recorded);
-    } catch (...) {
-      host_err = std::current_exception();
-    }
-  });
+  std::thread host_pass;
+  if (!P.host_pages.empty())
+    host_pass = std::thread([&] {
+      try {
+        host_pages_drain(E, P, img + s3, head, recorded);
+      } catch (...) {
+        host_err = std::current_exception();
+      }
+    });
   struct Joiner {
     std::thread& t;
     std::atomic<int64_t>& r;
@@ -1216,7 +1218,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
     recorded.store(int64_t(w), std::memory_order_release);
   }
   tr.mark("enqueue");
-  host_pass.join();
+  if (host_pass.joinable()) host_pass.join();
   if (host_err) std::rethrow_exception(host_err);
   // then K4 folds every CRC
   if (!P.host_pages.empty())

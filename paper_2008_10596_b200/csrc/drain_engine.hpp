@@ -99,9 +99,11 @@ struct ImagePlan {
   uint64_t len3 = 0, len4 = 0;
   uint64_t stream_len = 0;  // len3 + 20 + len4
   std::vector<crac_record_t, PinnedAlloc<crac_record_t>> recs;
-  std::vector<uint32_t> tile_rec;
-  std::vector<crac_span_t> pay_spans, page_spans;  // page_spans: device-resident runs
-  std::vector<uint64_t> pay_first, page_first;
+  // the arrays upload_plan copies to the device are page-locked, so those
+  // copies are plain DMA (no staging through the driver's pageable path)
+  std::vector<uint32_t, PinnedAlloc<uint32_t>> tile_rec;
+  std::vector<crac_span_t, PinnedAlloc<crac_span_t>> pay_spans, page_spans;  // page_spans: device-resident runs
+  std::vector<uint64_t, PinnedAlloc<uint64_t>> pay_first, page_first;
   // page-CRC index space (record.reserved): device-resident pages [0, n_dev),
   // in page_spans order; host-resident pages n_dev + k for host_pages[k]
   uint64_t n_dev_pages = 0;
