@@ -1493,25 +1493,31 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   {
     // map every live Device extent up front in coalesced runs, so the replay
     // itself makes no driver calls (and the early data path below has its
-    // destinations).  Extents in address order: first fit hands out low
-    // addresses again after frees, so id order is not address order.
-    std::vector<std::pair<uint64_t, uint64_t>> ext;
+    // destinations).  The runs come from a bitmap of the 2 MiB blocks the
+    // extents touch, in address order (first fit hands out low addresses
+    // again after frees, so id order is not address order), without
+    // sorting the extents (C2: 16 k); one-block gaps are bridged.
+    constexpr uint64_t kBlock = 2ull << 20;
+    std::vector<uint8_t> need((cfg.arena_bytes + kBlock - 1) / kBlock, 0);
     for (const AllocationRecord& r : p.facts.active) {
       live.push_back(r.id);
-      if (r.kind == AllocationKind::Device) ext.emplace_back(r.address, r.address + round_up_align(r.size));
+      if (r.kind != AllocationKind::Device) continue;
+      const uint64_t off = r.address - kArenaBase;  // parse_log checked it lies in the arena
+      const uint64_t b1 = (off + round_up_align(r.size) - 1) / kBlock;
+      for (uint64_t b = off / kBlock; b <= b1; ++b) need[b] = 1;
     }
-    std::sort(ext.begin(), ext.end());
-    uint64_t run_lo = 0, run_hi = 0;
-    for (const auto& [lo, hi] : ext) {
-      if (run_hi && lo <= run_hi + (2ull << 20)) {
-        run_hi = std::max(run_hi, hi);
-      } else {
-        if (run_hi) ctx.premap(run_lo, run_hi - run_lo);
-        run_lo = lo;
-        run_hi = hi;
+    const uint64_t nb = need.size();
+    for (uint64_t b = 0; b < nb;) {
+      if (!need[b]) {
+        ++b;
+        continue;
       }
+      uint64_t e = b + 1;
+      while (e < nb && (need[e] || (e + 1 < nb && need[e + 1]))) ++e;
+      const uint64_t hi = std::min(e * kBlock, cfg.arena_bytes);
+      ctx.premap(kArenaBase + b * kBlock, hi - b * kBlock);
+      b = e;
     }
-    if (run_hi) ctx.premap(run_lo, run_hi - run_lo);
   }
   tr.mark("premap");
 
