@@ -8,8 +8,12 @@
  * onto the logged dispatch table of one process-wide cracsim::Session (the
  * call path of ref: src/shim.cpp:204-253, which the reference drives from its
  * harness because it has no real cudart underneath), and admits
- *   cudaLaunchKernel / cudaMemcpy{,Async} / cudaMemset{,Async}
- * through the session's dispatch gate so a checkpoint quiesces them.
+ *   cudaLaunchKernel{,ExC} / cudaLaunchCooperativeKernel / cudaGraphLaunch /
+ *   cudaMemcpy{,2D,3D,Peer,ToSymbol,FromSymbol}{,Async} /
+ *   cudaMemset{,2D,3D}{,Async}
+ * through the session's dispatch gate so a checkpoint quiesces them (driver
+ * API calls a library makes through cuGetProcAddress pointers bypass the
+ * gate: INTEGRATION.md §4, "Un-gated calls").
  * cudaMalloc memory lives in the session's fixed-VA arena, so a device
  * pointer the application holds is the same pointer after a restart.
  *

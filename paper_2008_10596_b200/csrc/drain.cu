@@ -1353,7 +1353,13 @@ void reserve_shadow(Session& session, uint64_t bytes, int device) {
   if (!bytes) return;
   // +64: the pack of the last window writes whole 16-byte words
   check_cuda(cudaSetDevice(device), "set device");
-  const cudaError_t e = cudaMalloc(&E.d_shadow, bytes + 64);
+  cudaError_t e = cudaMalloc(&E.d_shadow, bytes + 64);
+  if (e == cudaErrorMemoryAllocation) {
+    // a closed session's cached arena may hold the memory (device_core.cu)
+    cudaGetLastError();
+    drop_arena_cache(device);
+    e = cudaMalloc(&E.d_shadow, bytes + 64);
+  }
   if (e == cudaSuccess && device != own && !E.s_peer) {
     check_cuda(cudaStreamCreateWithFlags(&E.s_peer, cudaStreamNonBlocking), "peer stream");
     check_cuda(cudaEventCreateWithFlags(&E.ev_peer, cudaEventDisableTiming), "peer event");
@@ -1503,6 +1509,13 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       live.push_back(r.id);
       if (r.kind != AllocationKind::Device) continue;
       const uint64_t off = r.address - kArenaBase;  // parse_log checked it lies in the arena
+      // parse_log's arena check is the reference's (image.cpp:133-135), whose
+      // round_up_align wraps to 0 for sizes near 2^64; such an extent cannot
+      // lie in the arena, and its payload frame cannot exist (the reference
+      // rejects the image in decode_payloads/decode_uvm): ImageCorrupt here,
+      // before anything is indexed by it
+      if (r.size > cfg.arena_bytes - off)
+        raise(Errc::ImageCorrupt, "Alloc extent outside arena");
       const uint64_t b1 = (off + round_up_align(r.size) - 1) / kBlock;
       for (uint64_t b = off / kBlock; b <= b1; ++b) need[b] = 1;
     }
@@ -1652,7 +1665,15 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   mi = 0;
   for (const AllocationRecord& rec : p.facts.active)
     if (rec.kind == AllocationKind::Managed) ctx.set_managed_flags(rec.id, p.managed[mi++].flags);
-  std::thread host_fill([&] { host_pages_refill(E, P, raw.data() + s3); });
+  std::exception_ptr fill_err;
+  std::thread host_fill([&, dev = E.device] {
+    try {
+      cudaSetDevice(dev);  // the host-CRC buffer is pinned: no context on device 0
+      host_pages_refill(E, P, raw.data() + s3);
+    } catch (...) {
+      fill_err = std::current_exception();
+    }
+  });
   struct Joiner {
     std::thread& t;
     ~Joiner() {
@@ -1664,6 +1685,11 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   if (!early) enqueue_data_path();
   if (P.stream_len > 20) {
     host_fill.join();  // the host-resident pages' CRCs
+    if (fill_err) {
+      cudaStreamSynchronize(E.s_copy);  // the enqueued data path reads the image
+      cudaStreamSynchronize(E.s_pack);
+      std::rethrow_exception(fill_err);
+    }
     tr.mark("host-fill-join");
     if (!P.host_pages.empty())
       check_cuda(cudaMemcpyAsync(E.d_page_crc.ptr + P.n_dev_pages, E.h_host_crc.ptr,

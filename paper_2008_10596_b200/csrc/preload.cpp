@@ -395,6 +395,54 @@ cudaError_t cudaMemsetAsync(void* devPtr, int value, size_t count, cudaStream_t 
   return f(devPtr, value, count, stream);
 }
 
+// The rest of the runtime's device-state-changing calls: same gate.  (Driver
+// API launches a library obtains through cuGetProcAddress -- cuBLAS under
+// the runtime, for example -- never reach an LD_PRELOAD symbol; they are
+// quiesced by the drain's device-wide synchronize.)
+#define CRAC_GATED(ret, name, params, args)                              \
+  ret name params {                                                      \
+    static auto f = real<ret(*) params>(#name);                          \
+    Admitted a;                                                          \
+    return f args;                                                       \
+  }
+
+CRAC_GATED(cudaError_t, cudaMemcpy2D,
+           (void* d, size_t dp, const void* s, size_t sp, size_t w, size_t h, cudaMemcpyKind k),
+           (d, dp, s, sp, w, h, k))
+CRAC_GATED(cudaError_t, cudaMemcpy2DAsync,
+           (void* d, size_t dp, const void* s, size_t sp, size_t w, size_t h, cudaMemcpyKind k,
+            cudaStream_t st),
+           (d, dp, s, sp, w, h, k, st))
+CRAC_GATED(cudaError_t, cudaMemcpy3D, (const cudaMemcpy3DParms* p), (p))
+CRAC_GATED(cudaError_t, cudaMemcpy3DAsync, (const cudaMemcpy3DParms* p, cudaStream_t st), (p, st))
+CRAC_GATED(cudaError_t, cudaMemcpyPeer, (void* d, int dd, const void* s, int sd, size_t n),
+           (d, dd, s, sd, n))
+CRAC_GATED(cudaError_t, cudaMemcpyPeerAsync,
+           (void* d, int dd, const void* s, int sd, size_t n, cudaStream_t st), (d, dd, s, sd, n, st))
+CRAC_GATED(cudaError_t, cudaMemcpyToSymbol,
+           (const void* sym, const void* s, size_t n, size_t off, cudaMemcpyKind k), (sym, s, n, off, k))
+CRAC_GATED(cudaError_t, cudaMemcpyToSymbolAsync,
+           (const void* sym, const void* s, size_t n, size_t off, cudaMemcpyKind k, cudaStream_t st),
+           (sym, s, n, off, k, st))
+CRAC_GATED(cudaError_t, cudaMemcpyFromSymbol,
+           (void* d, const void* sym, size_t n, size_t off, cudaMemcpyKind k), (d, sym, n, off, k))
+CRAC_GATED(cudaError_t, cudaMemcpyFromSymbolAsync,
+           (void* d, const void* sym, size_t n, size_t off, cudaMemcpyKind k, cudaStream_t st),
+           (d, sym, n, off, k, st))
+CRAC_GATED(cudaError_t, cudaMemset2D, (void* d, size_t p, int v, size_t w, size_t h), (d, p, v, w, h))
+CRAC_GATED(cudaError_t, cudaMemset2DAsync,
+           (void* d, size_t p, int v, size_t w, size_t h, cudaStream_t st), (d, p, v, w, h, st))
+CRAC_GATED(cudaError_t, cudaMemset3D, (cudaPitchedPtr p, int v, cudaExtent e), (p, v, e))
+CRAC_GATED(cudaError_t, cudaMemset3DAsync, (cudaPitchedPtr p, int v, cudaExtent e, cudaStream_t st),
+           (p, v, e, st))
+CRAC_GATED(cudaError_t, cudaLaunchKernelExC,
+           (const cudaLaunchConfig_t* c, const void* fn, void** args), (c, fn, args))
+CRAC_GATED(cudaError_t, cudaLaunchCooperativeKernel,
+           (const void* fn, dim3 g, dim3 b, void** args, size_t sh, cudaStream_t st),
+           (fn, g, b, args, sh, st))
+CRAC_GATED(cudaError_t, cudaGraphLaunch, (cudaGraphExec_t e, cudaStream_t st), (e, st))
+#undef CRAC_GATED
+
 // ---- application API (crac_preload.h) -------------------------------------------
 int crac_preload_checkpoint(const char* path) {
   State* g = session();

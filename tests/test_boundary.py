@@ -95,7 +95,12 @@ def test_preload_exports_its_api_and_interposers(so):
     interposed = {"cudaMalloc", "cudaMallocManaged", "cudaMallocHost", "cudaHostAlloc",
                   "cudaFree", "cudaFreeHost", "cudaStreamCreate", "cudaStreamCreateWithFlags",
                   "cudaStreamCreateWithPriority", "cudaStreamDestroy", "cudaLaunchKernel",
-                  "cudaMemcpy", "cudaMemcpyAsync", "cudaMemset", "cudaMemsetAsync"}
+                  "cudaMemcpy", "cudaMemcpyAsync", "cudaMemset", "cudaMemsetAsync",
+                  "cudaLaunchKernelExC", "cudaLaunchCooperativeKernel", "cudaGraphLaunch",
+                  "cudaMemcpy2D", "cudaMemcpy2DAsync", "cudaMemcpy3D", "cudaMemcpy3DAsync",
+                  "cudaMemcpyPeer", "cudaMemcpyPeerAsync", "cudaMemcpyToSymbol",
+                  "cudaMemcpyToSymbolAsync", "cudaMemcpyFromSymbol", "cudaMemcpyFromSymbolAsync",
+                  "cudaMemset2D", "cudaMemset2DAsync", "cudaMemset3D", "cudaMemset3DAsync"}
     assert api | interposed <= syms, sorted((api | interposed) - syms)
     # the engine library itself must not export cuda* (its static runtime
     # would otherwise be interposed by the preload)
@@ -170,3 +175,40 @@ def test_host_codec_payload_frames_match_reference(so):
             ours_ok = False
         assert ours_ok == ref_ok
         assert not ours_ok
+
+
+@pytest.mark.parametrize("kind,size,pay,uvm", [
+    # one Device alloc of 2^64-1 at the arena base, a 15-byte ALLOC_PAYLOADS
+    # (16 + size wraps to 15): the advisor's reproduction
+    (1, (1 << 64) - 1, b"\0" * 15, b""),
+    (1, (1 << 64) - 17, b"\0" * 32, b""),
+    # the same through the managed prefix sums
+    (3, (1 << 64) - 1, b"", b"\0" * 40),
+    (3, (1 << 64) - 4096, b"", b"\0" * 64),
+])
+def test_host_codec_rejects_wrapping_logged_sizes(so, kind, size, pay, uvm):
+    """A logged size near 2^64 passes the reference's own arena check
+    (round_up_align wraps to 0, ref: image.cpp:133-135) but can never have a
+    payload frame: the reference rejects such an image in its bounds-checked
+    walk; ours must raise ImageCorrupt too (all CRCs valid), never read past
+    the section (image.cpp:185, drain.cu:1506)."""
+    import struct
+    import sys
+    import zlib
+    sys.path.insert(0, str(ROOT))
+    from oracle import ref
+    from oracle.image_oracle import K_ARENA_BASE, MAGIC
+    secs = [struct.pack("<QQII", 0, 1 << 24, 1, 0),
+            struct.pack("<QBBHQQQ", 1, 1, kind, 0, size, 1, K_ARENA_BASE),
+            pay, uvm, b"", b"", struct.pack("<Q", 0)]
+    img = bytearray(MAGIC + struct.pack("<II", 1, 7))
+    for tag, p in enumerate(secs, start=1):
+        img += struct.pack("<IIQ", tag, 0, len(p)) + p + struct.pack("<I", zlib.crc32(p))
+    img = bytes(img)
+    with pytest.raises(ref.RefError) as r:
+        ref.ref_decode_check(img)
+    assert r.value.errc == "ImageCorrupt"
+    for call in (so.decode_check, so.summarize_image):
+        with pytest.raises(so.CracError) as e:
+            call(img)
+        assert e.value.errc == "ImageCorrupt"
