@@ -73,14 +73,28 @@ int crac_chunk_crc32_range(const crac_span_t* d_spans, const uint64_t* d_chunk_f
                            uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
                            uint32_t* d_crc, uint32_t max_ctas, void* stream);
 
+/* K1 plus the chunk key: the same pass also writes d_key[c], a second,
+ * independent 32-bit lane (integer multiply-add over the chunk's 32-bit
+ * words with position-dependent offsets, not GF(2)-linear; definition in
+ * kernels.cu "Key2").  (d_crc[c], d_key[c]) is the 64-bit dirty key of the
+ * incremental and pre-copy drains: a change that preserves the CRC-32 (four
+ * compensating bytes suffice) still changes the key.  d_key may be null
+ * (= crac_chunk_crc32_range). */
+int crac_chunk_key_range(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
+                         uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
+                         uint32_t* d_crc, uint32_t* d_key, uint32_t max_ctas, void* stream);
+
 /* Fused incremental drain (K1 + K2b in one pass): hashes chunks [c_lo, c_hi)
- * into d_crc; every chunk whose CRC differs from d_crc_prev is written by the
- * hashing warp straight into host_image + d_dst_off[span] + chunk offset
- * (pinned, UVA-mapped) and its d_crc_prev entry updated.  d_counters[0] +=
- * dirty chunks, d_counters[1] += dirty bytes (caller zeroes them). */
+ * into d_crc (and d_key); every chunk whose dirty key (d_crc, d_key) differs
+ * from (d_crc_prev, d_key_prev) is written by the hashing warp straight into
+ * host_image + d_dst_off[span] + chunk offset (pinned, UVA-mapped) and its
+ * previous-key entries updated.  d_key / d_key_prev: both null (CRC-only
+ * comparison) or both set.  d_counters[0] += dirty chunks, d_counters[1] +=
+ * dirty bytes (caller zeroes them). */
 int crac_hash_drain_range(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
                           uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
-                          uint32_t* d_crc, uint32_t* d_crc_prev, const uint64_t* d_dst_off,
+                          uint32_t* d_crc, uint32_t* d_crc_prev, uint32_t* d_key,
+                          uint32_t* d_key_prev, const uint64_t* d_dst_off,
                           uint8_t* host_image, unsigned long long* d_counters, void* stream);
 /* Split form of crac_hash_drain_range: the first n_writers CTAs only write
  * dirty chunks to the image, the others hash and hand each dirty chunk over
@@ -90,7 +104,8 @@ int crac_hash_drain_range(const crac_span_t* d_spans, const uint64_t* d_chunk_fi
  * <= SMs / 4. */
 int crac_hash_drain_split(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
                           uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
-                          uint32_t* d_crc, uint32_t* d_crc_prev, const uint64_t* d_dst_off,
+                          uint32_t* d_crc, uint32_t* d_crc_prev, uint32_t* d_key,
+                          uint32_t* d_key_prev, const uint64_t* d_dst_off,
                           uint8_t* host_image, unsigned long long* d_counters,
                           unsigned long long* d_queue, uint32_t n_writers, void* stream);
 
@@ -122,14 +137,14 @@ int crac_fold_sections(const crac_record_t* d_recs, uint32_t n_recs, const uint6
                        uint64_t len3, uint64_t total_pay_chunks, uint32_t* d_out, void* stream);
 
 /* Hash + copy (stall-reduced snapshot): hashes chunks [c_lo, c_hi) into
- * d_crc and writes every chunk to d_dst + d_dst_off[span] + chunk offset
+ * d_crc (and the chunk key into d_key, unless null) and writes every chunk to d_dst + d_dst_off[span] + chunk offset
  * from the registers it was hashed from (one HBM read; d_dst is device or
  * UVA memory).  dst_aligned = 1 promises every d_dst + d_dst_off[span] is
  * 16-byte aligned (faster kernel); 0 accepts any alignment. */
 int crac_hash_copy_range(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
                          uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
-                         uint32_t* d_crc, const uint64_t* d_dst_off, uint8_t* d_dst,
-                         int dst_aligned, void* stream);
+                         uint32_t* d_crc, uint32_t* d_key, const uint64_t* d_dst_off,
+                         uint8_t* d_dst, int dst_aligned, void* stream);
 
 /* The frame bytes (frame_len <= 24) of records [0, n_recs) at
  * d_stream + out_off, with byte stores only, so a concurrent

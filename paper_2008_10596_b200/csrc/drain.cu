@@ -164,6 +164,8 @@ DrainEngine::~DrainEngine() {
   d_pay_crc.release();
   d_page_crc.release();
   d_prev_crc.release();
+  d_pay_key.release();
+  d_prev_key.release();
   d_block_counts.release();
   d_dirty_idx.release();
   d_dirty_count.release();
@@ -646,15 +648,31 @@ void upload_plan(DrainEngine& E, const ImagePlan& P, cudaStream_t st) {
   upload(E.d_page_first, P.page_first, st);
   const uint64_t n_pay = P.pay_first.back(), n_page = P.n_dev_pages + P.host_pages.size();
   E.d_pay_crc.ensure(std::max<uint64_t>(n_pay, 1));
+  E.d_pay_key.ensure(std::max<uint64_t>(n_pay, 1));
   E.d_page_crc.ensure(std::max<uint64_t>(n_page, 1));
 }
 
+// with_key: also the chunks' second dirty-key lane (drains and hash-only,
+// whose chunk keys seed the next incremental drain; not the refill verify)
 void hash_payloads(DrainEngine& E, const ImagePlan& P, uint64_t c_lo, uint64_t c_hi,
-                   uint32_t max_ctas, cudaStream_t st) {
-  check_cuda(cudaError_t(crac_chunk_crc32_range(E.d_pay_spans.ptr, E.d_pay_first.ptr,
-                                                uint32_t(P.pay_spans.size()), DrainEngine::kChunk,
-                                                c_lo, c_hi, E.d_pay_crc.ptr, max_ctas, st)),
+                   uint32_t max_ctas, cudaStream_t st, bool with_key = true) {
+  check_cuda(cudaError_t(crac_chunk_key_range(E.d_pay_spans.ptr, E.d_pay_first.ptr,
+                                              uint32_t(P.pay_spans.size()), DrainEngine::kChunk,
+                                              c_lo, c_hi, E.d_pay_crc.ptr,
+                                              with_key ? E.d_pay_key.ptr : nullptr, max_ctas, st)),
              "K1 payloads");
+}
+
+// The previous image's dirty keys := this pass's (CRC and key lanes).
+void seed_prev_keys(DrainEngine& E, uint64_t n_pay, cudaStream_t st) {
+  E.d_prev_crc.ensure(n_pay);
+  E.d_prev_key.ensure(n_pay);
+  check_cuda(cudaMemcpyAsync(E.d_prev_crc.ptr, E.d_pay_crc.ptr, n_pay * 4,
+                             cudaMemcpyDeviceToDevice, st),
+             "seed prev crc");
+  check_cuda(cudaMemcpyAsync(E.d_prev_key.ptr, E.d_pay_key.ptr, n_pay * 4,
+                             cudaMemcpyDeviceToDevice, st),
+             "seed prev key");
 }
 
 void hash_pages(DrainEngine& E, const ImagePlan& P, uint32_t max_ctas, cudaStream_t st) {
@@ -1162,7 +1180,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
                                      [](uint64_t o) { return o % 16 == 0; });
     check_cuda(cudaError_t(crac_hash_copy_range(
                    E.d_pay_spans.ptr, E.d_pay_first.ptr, uint32_t(P.pay_spans.size()),
-                   DrainEngine::kChunk, 0, P.pay_first.back(), E.d_pay_crc.ptr,
+                   DrainEngine::kChunk, 0, P.pay_first.back(), E.d_pay_crc.ptr, E.d_pay_key.ptr,
                    E.d_pay_soff.ptr, E.d_shadow, aligned ? 1 : 0, E.s_hash)),
                "K1 hash+copy");
     check_cuda(cudaError_t(crac_write_frames(E.d_recs.ptr, uint32_t(P.pay_spans.size()),
@@ -1239,12 +1257,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   finish_fold(E, P, Q.crc3, Q.crc4);
   // seed the incremental table with this image's payload chunk CRCs
   const uint64_t n_pay = P.pay_first.back();
-  if (n_pay) {
-    E.d_prev_crc.ensure(n_pay);
-    check_cuda(cudaMemcpyAsync(E.d_prev_crc.ptr, E.d_pay_crc.ptr, n_pay * 4,
-                               cudaMemcpyDeviceToDevice, E.s_hash),
-               "seed prev crc");
-  }
+  if (n_pay) seed_prev_keys(E, n_pay, E.s_hash);
   check_cuda(cudaEventSynchronize(E.ev_s1), "snapshot sync");
   tr.mark("d2h-wait");
 
@@ -1588,7 +1601,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
           E.ensure_verify_events(verifies + 1);
           cudaEventRecord(E.ev_v0[verifies], E.s_pack);
         }
-        hash_payloads(E, P, P.pay_first[spans_done], P.pay_first[done], 0, E.s_pack);
+        hash_payloads(E, P, P.pay_first[spans_done], P.pay_first[done], 0, E.s_pack, false);
         if (stats) cudaEventRecord(E.ev_v1[verifies], E.s_pack);
         ++verifies;
         spans_done = done;
@@ -1777,15 +1790,15 @@ void incremental_locked(Session& session, PinnedImage& image, DrainStats* stats)
   if (split)
     check_cuda(cudaError_t(crac_hash_drain_split(
                    E.d_pay_spans.ptr, E.d_pay_first.ptr, uint32_t(P.pay_spans.size()),
-                   DrainEngine::kChunk, 0, n, E.d_pay_crc.ptr, E.d_prev_crc.ptr, E.d_pay_dst.ptr,
-                   img, E.d_counters.ptr,
+                   DrainEngine::kChunk, 0, n, E.d_pay_crc.ptr, E.d_prev_crc.ptr, E.d_pay_key.ptr,
+                   E.d_prev_key.ptr, E.d_pay_dst.ptr, img, E.d_counters.ptr,
                    reinterpret_cast<unsigned long long*>(E.d_dirty_idx.ptr), writers, E.s_pack)),
                "hash+drain split");
   else
     check_cuda(cudaError_t(crac_hash_drain_range(
                    E.d_pay_spans.ptr, E.d_pay_first.ptr, uint32_t(P.pay_spans.size()),
-                   DrainEngine::kChunk, 0, n, E.d_pay_crc.ptr, E.d_prev_crc.ptr, E.d_pay_dst.ptr,
-                   img, E.d_counters.ptr, E.s_pack)),
+                   DrainEngine::kChunk, 0, n, E.d_pay_crc.ptr, E.d_prev_crc.ptr, E.d_pay_key.ptr,
+                   E.d_prev_key.ptr, E.d_pay_dst.ptr, img, E.d_counters.ptr, E.s_pack)),
                "hash+drain");
   check_cuda(cudaEventRecord(E.ev_h1, E.s_pack), "event");
   check_cuda(cudaMemcpyAsync(E.h_count.ptr, E.d_counters.ptr, 16, cudaMemcpyDeviceToHost, E.s_pack),
@@ -1889,10 +1902,7 @@ void precopy_wait(Session& session, double* phase1_ms) {
   // the image now holds, chunk by chunk, the bytes whose CRCs K1 left in
   // d_pay_crc: they seed the incremental pass
   const uint64_t n_pay = P.pay_first.back();
-  E.d_prev_crc.ensure(n_pay);
-  check_cuda(cudaMemcpyAsync(E.d_prev_crc.ptr, E.d_pay_crc.ptr, n_pay * 4, cudaMemcpyDeviceToDevice,
-                             E.s_hash),
-             "seed prev crc");
+  seed_prev_keys(E, n_pay, E.s_hash);
   check_cuda(cudaStreamSynchronize(E.s_hash), "pre-copy seed");
   P.valid = true;
   P.image_ptr = reinterpret_cast<uint64_t>(Q.out->data());
@@ -1971,7 +1981,8 @@ void checkpoint_precopy_begin(Session& session, PinnedImage& out, DrainStats* st
   uint8_t* stream = img + P.s3;  // page-locked host memory, written by the SMs over PCIe
   check_cuda(cudaError_t(crac_hash_copy_range(E.d_pay_spans.ptr, E.d_pay_first.ptr,
                                               uint32_t(P.pay_spans.size()), DrainEngine::kChunk, 0,
-                                              P.pay_first.back(), E.d_pay_crc.ptr, E.d_pay_soff.ptr,
+                                              P.pay_first.back(), E.d_pay_crc.ptr, E.d_pay_key.ptr,
+                                              E.d_pay_soff.ptr,
                                               stream, aligned ? 1 : 0, E.s_hash)),
              "pre-copy hash+copy");
   check_cuda(cudaError_t(crac_write_frames(E.d_recs.ptr, uint32_t(P.pay_spans.size()), stream,

@@ -151,6 +151,9 @@ struct DrainEngine {
   DevArray<crac_span_t> d_pay_spans, d_page_spans;
   DevArray<uint64_t> d_pay_first, d_page_first, d_pay_dst, d_pay_soff;
   DevArray<uint32_t> d_pay_crc, d_page_crc, d_prev_crc, d_block_counts;
+  // second dirty-key lane of every payload chunk (crac_chunk_key_range): the
+  // incremental / pre-copy drains compare (crc, key), a 64-bit dirty key
+  DevArray<uint32_t> d_pay_key, d_prev_key;
   DevArray<uint64_t> d_dirty_idx, d_dirty_count;
   DevArray<unsigned long long> d_counters;
   DevArray<uint32_t> d_fold;   // linear parts of crc3 / crc4 (K4)

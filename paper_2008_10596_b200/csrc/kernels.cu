@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "crac_gpu.h"
@@ -198,6 +199,42 @@ struct NoSink {
   __device__ __forceinline__ void operator()(uint32_t, uint4, uint4, bool) const {}
 };
 
+// Second dirty-key lane (crac_gpu.h "chunk key"): an integer-arithmetic hash
+// computed from the same registers as the CRC, so a change that preserves a
+// chunk's CRC-32 (GF(2)-linear: four compensating bytes suffice) still
+// changes the 64-bit dirty key (CRC, key) with probability ~1 - 2^-32.
+// 16-byte word j of a chunk, (x, y, z, w), row r = j / 32, lane l = j % 32:
+//   k = (l + 1) * 0x27D4EB2F + r * 0x9E3779B9
+//   t = (x + k) * (y + 0x85EBCA6B) + (z + (k ^ 0xC2B2AE35)) * (w + 0x165667B1)
+// (32 x 32 -> 64-bit products, sums mod 2^64); a trailing partial word is
+// zero-padded; key = fold(mix64(sum ^ len * 0x9E3779B97F4A7C15)).  ~0.4
+// integer op per byte beside the CRC's one table lookup per byte.
+struct NoKey {
+  __device__ __forceinline__ void add(uint32_t, uint4) {}
+};
+struct Key2 {
+  uint64_t sum = 0;
+  uint32_t kl = 0;  // (lane + 1) * 0x27D4EB2F
+  __device__ __forceinline__ void add(uint32_t r, uint4 w) {
+    const uint32_t k = kl + r * 0x9E3779B9u;
+    sum += uint64_t(w.x + k) * (w.y + 0x85EBCA6Bu) + uint64_t(w.z + (k ^ 0xC2B2AE35u)) * (w.w + 0x165667B1u);
+  }
+};
+
+__device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ uint32_t key_final(uint64_t sum, uint32_t len) {
+  uint64_t x = sum ^ (uint64_t(len) * 0x9E3779B97F4A7C15ull);
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return uint32_t(x) ^ uint32_t(x >> 32);
+}
+
 __device__ __forceinline__ uint4 shfl4(uint4 v, uint32_t src) {
   v.x = __shfl_sync(0xFFFFFFFFu, v.x, src);
   v.y = __shfl_sync(0xFFFFFFFFu, v.y, src);
@@ -234,9 +271,9 @@ struct CopySink {
 // Runs one lane's column over `rows` rows of 512 B starting at p (the lane's
 // first word).  Loads of the next kRows rows are in flight while the current
 // kRows rows are hashed.  The last row uses group A (no trailing gap).
-template <int kRows, typename Sink>
+template <int kRows, typename Sink, typename Key>
 __device__ __forceinline__ uint32_t k1_rows(const LaneLut& lut, const uint8_t* p, uint32_t rows,
-                                            const Sink& sink) {
+                                            const Sink& sink, Key& key) {
   uint32_t acc = 0, r = 0;
   if (rows >= uint32_t(kRows)) {
     uint4 cur[kRows];
@@ -249,6 +286,7 @@ __device__ __forceinline__ uint32_t k1_rows(const LaneLut& lut, const uint8_t* p
 #pragma unroll
       for (int k = 0; k < kRows; ++k) {
         acc = word16<true>(lut, acc, cur[k]);
+        key.add(r + k, cur[k]);
         sink(r + k, cur[k], k + 1 < kRows ? cur[(k + 1) % kRows] : nxt[0], true);
       }
 #pragma unroll
@@ -257,16 +295,19 @@ __device__ __forceinline__ uint32_t k1_rows(const LaneLut& lut, const uint8_t* p
 #pragma unroll
     for (int k = 0; k < kRows - 1; ++k) {
       acc = word16<true>(lut, acc, cur[k]);
+      key.add(r + k, cur[k]);
       sink(r + k, cur[k], cur[k + 1], true);
     }
     acc = (r + kRows == rows) ? word16<false>(lut, acc, cur[kRows - 1])
                               : word16<true>(lut, acc, cur[kRows - 1]);
+    key.add(r + kRows - 1, cur[kRows - 1]);
     sink(r + kRows - 1, cur[kRows - 1], cur[kRows - 1], false);
     r += kRows;
   }
   for (; r < rows; ++r) {
     const uint4 w = ldg_stream(p + r * 512);
     acc = (r + 1 == rows) ? word16<false>(lut, acc, w) : word16<true>(lut, acc, w);
+    key.add(r, w);
     sink(r, w, w, false);
   }
   return acc;
@@ -283,6 +324,7 @@ __device__ __forceinline__ uint32_t k1_rows(const LaneLut& lut, const uint8_t* p
 // re-read of dirty chunks only).
 struct HashDrain {
   uint32_t* prev;                // previous chunk CRCs; updated for dirty chunks
+  uint32_t* prev_key;            // previous chunk keys (second lane); may be null
   const uint64_t* dst_off;       // per span: image offset of its first payload byte
   uint8_t* host;                 // pinned image (UVA)
   unsigned long long* counters;  // [0] dirty chunks, [1] dirty bytes
@@ -369,11 +411,14 @@ __device__ void drain_writer(const crac_span_t* __restrict__ spans,
 // 2 hash + copy every chunk from registers (stall-reduced snapshot), every
 // destination 16-byte aligned; 3 the same for any destination alignment;
 // 4 split incremental drain (hashers push dirty chunks, writer CTAs copy).
-template <int kRows, int kMode>
+// kKey: also the second dirty-key lane (Key2) into out_key[c] (and, in the
+// drain modes, compared with / stored to hd.prev_key).
+template <int kRows, int kMode, bool kKey>
 __global__ void __launch_bounds__(kK1Threads, 1)
     k1_chunk_crc(const crac_span_t* __restrict__ spans, const uint64_t* __restrict__ chunk_first,
                  uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
-                 uint32_t* __restrict__ out, uint32_t k_full, HashDrain hd) {
+                 uint32_t* __restrict__ out, uint32_t* __restrict__ out_key, uint32_t k_full,
+                 HashDrain hd) {
   extern __shared__ __align__(16) uint32_t s_tab[];
   {
     const uint4* src = reinterpret_cast<const uint4*>(g_tab);
@@ -418,13 +463,15 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     // ---- main body: rows of 512 B, kRows-deep double-buffered loads ----
     uint32_t acc;
     uint8_t* dst = nullptr;
+    std::conditional_t<kKey, Key2, NoKey> key;
+    if constexpr (kKey) key.kl = (lane + 1) * 0x27D4EB2Fu;
     if ((kMode == 2 || kMode == 3)) {
       dst = hd.host + hd.dst_off[s] + off;
       const uint32_t m = uint32_t(reinterpret_cast<uint64_t>(dst) & 15);
       acc = k1_rows<kRows>(lut, base + lane * 16, rows,
-                           CopySink<kMode == 2>{dst - m, base + lane * 16, m, rows, lane});
+                           CopySink<kMode == 2>{dst - m, base + lane * 16, m, rows, lane}, key);
     } else {
-      acc = k1_rows<kRows>(lut, base + lane * 16, rows, NoSink{});
+      acc = k1_rows<kRows>(lut, base + lane * 16, rows, NoSink{}, key);
     }
     uint32_t L = rows ? warp_xor(crac::gf_mul(g_xp16[31 - lane], acc)) : 0u;
 
@@ -436,21 +483,42 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       if (lane < nt) {
         const uint4 w = *reinterpret_cast<const uint4*>(base + rows * 512 + lane * 16);
         part = crac::gf_mul(g_xp16[nt - 1 - lane], word16<false>(lut, 0u, w));
+        key.add(rows, w);
       }
       uint32_t lt = warp_xor(part);
       if (lane == 0) {
         const uint8_t* tb = base + rows * 512 + nt * 16;
-        for (uint32_t i = 0; i < (t & 15); ++i) lt = (lt >> 8) ^ g_t0[(lt ^ tb[i]) & 0xFFu];
+        uint4 pw = make_uint4(0, 0, 0, 0);  // the trailing partial word, zero-padded
+        for (uint32_t i = 0; i < (t & 15); ++i) {
+          lt = (lt >> 8) ^ g_t0[(lt ^ tb[i]) & 0xFFu];
+          if constexpr (kKey) (&pw.x)[i >> 2] |= uint32_t(tb[i]) << (8 * (i & 3));
+        }
         L = crac::gf_mul(g_xpt[t], L) ^ lt;
+        if constexpr (kKey) {
+          if (t & 15) {  // word j = 32 rows + nt: the key of lane slot nt
+            Key2 tail;
+            tail.kl = (nt + 1) * 0x27D4EB2Fu;
+            tail.add(rows, pw);
+            key.sum += tail.sum;
+          }
+        }
       }
     }
     if (lane == 0) L ^= (len == chunk_bytes ? k_full : crac::crc_affine(len, g_pow2));
+    uint32_t K = 0;
+    if constexpr (kKey) K = key_final(warp_sum64(key.sum), len);
     if (kMode == 0) {
-      if (lane == 0) out[c] = L;
+      if (lane == 0) {
+        out[c] = L;
+        if constexpr (kKey) out_key[c] = K;
+      }
       continue;
     }
     if ((kMode == 2 || kMode == 3)) {
-      if (lane == 0) out[c] = L;
+      if (lane == 0) {
+        out[c] = L;
+        if constexpr (kKey) out_key[c] = K;
+      }
       // byte-exact edges the register copy left: the head word (misaligned
       // destination), the m bytes of the last main row's straddling word,
       // and the tail (< 512 B, source aligned again)
@@ -466,9 +534,18 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     }
     const uint32_t crc = __shfl_sync(0xFFFFFFFFu, L, 0);
     if (lane == 0) out[c] = crc;
-    if (crc != hd.prev[c]) {  // warp-uniform
+    bool changed = crc != hd.prev[c];
+    if constexpr (kKey) {  // the 64-bit dirty key (CRC, key), when the caller keeps keys
+      if (hd.prev_key) {
+        if (lane == 0) out_key[c] = K;
+        changed |= K != hd.prev_key[c];
+      }
+    }
+    if (changed) {  // warp-uniform
       if (lane == 0) {
         hd.prev[c] = crc;
+        if constexpr (kKey)
+          if (hd.prev_key) hd.prev_key[c] = K;
         atomicAdd(&hd.counters[0], 1ull);
         atomicAdd(&hd.counters[1], (unsigned long long)len);
         if (kMode == 4) {  // hand the chunk to the writers and keep hashing
@@ -1143,8 +1220,10 @@ int crac_gpu_init(void) {
     if (!e) e = cudaMemcpyToSymbol(g_xp16, h.xp16.data(), 33 * 4);
     if (!e) e = cudaMemcpyToSymbol(g_xpt, h.xpt.data(), 512 * 4);
     if (!e) e = cudaMemcpyToSymbol(g_pow2, h.pow2.data(), 64 * 4);
-    for (auto k : {k1_chunk_crc<4, 0>, k1_chunk_crc<8, 0>, k1_chunk_crc<16, 0>,
-                   k1_chunk_crc<16, 1>, k1_chunk_crc<16, 2>, k1_chunk_crc<8, 3>, k1_chunk_crc<16, 4>})
+    for (auto k : {k1_chunk_crc<4, 0, false>, k1_chunk_crc<8, 0, false>, k1_chunk_crc<16, 0, false>,
+                   k1_chunk_crc<4, 0, true>, k1_chunk_crc<8, 0, true>, k1_chunk_crc<16, 0, true>,
+                   k1_chunk_crc<16, 1, true>, k1_chunk_crc<16, 2, false>, k1_chunk_crc<8, 3, false>,
+                   k1_chunk_crc<16, 2, true>, k1_chunk_crc<8, 3, true>, k1_chunk_crc<16, 4, true>})
       if (!e) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTabBytes));
     if (!e) e = cudaFuncSetAttribute(k1_chunk_crc_tma<16, 3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(k1_tma_smem<16, 3, 4>()));
@@ -1166,6 +1245,13 @@ int crac_chunk_crc32(const crac_span_t* d_spans, const uint64_t* d_chunk_first, 
 int crac_chunk_crc32_range(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
                            uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
                            uint32_t* d_crc, uint32_t max_ctas, void* stream) {
+  return crac_chunk_key_range(d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc,
+                              nullptr, max_ctas, stream);
+}
+
+int crac_chunk_key_range(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
+                         uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
+                         uint32_t* d_crc, uint32_t* d_key, uint32_t max_ctas, void* stream) {
   if (c_hi <= c_lo) return 0;
   if (chunk_bytes == 0 || chunk_bytes % 512) return int(cudaErrorInvalidValue);
   if (int rc = crac_gpu_init()) return rc;
@@ -1184,7 +1270,7 @@ int crac_chunk_crc32_range(const crac_span_t* d_spans, const uint64_t* d_chunk_f
     const char* e = std::getenv("CRAC_K1_TMA");
     return e ? e[0] : '\0';
   }();
-  if (tma) {  // measured alternative (see k1_chunk_crc_tma)
+  if (tma && !d_key) {  // measured alternative (see k1_chunk_crc_tma)
     const uint64_t w = tma == 'A' ? 16 : 8;
     const uint64_t b = std::min<uint64_t>((warps_needed + w - 1) / w, cap);
     const cudaStream_t st = cudaStream_t(stream);
@@ -1201,38 +1287,44 @@ int crac_chunk_crc32_range(const crac_span_t* d_spans, const uint64_t* d_chunk_f
     return int(cudaGetLastError());
   }
   const int rows = forced ? forced : (chunk_bytes >= 32 * 512 ? 16 : chunk_bytes >= 8 * 512 ? 8 : 4);
-  auto kern = rows == 4 ? k1_chunk_crc<4, 0>
-              : rows == 16 ? k1_chunk_crc<16, 0> : k1_chunk_crc<8, 0>;
+  auto kern = d_key ? (rows == 4 ? k1_chunk_crc<4, 0, true>
+                       : rows == 16 ? k1_chunk_crc<16, 0, true> : k1_chunk_crc<8, 0, true>)
+                    : (rows == 4 ? k1_chunk_crc<4, 0, false>
+                       : rows == 16 ? k1_chunk_crc<16, 0, false> : k1_chunk_crc<8, 0, false>);
   kern<<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
-      d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, k_full_for(chunk_bytes),
-      HashDrain{});
+      d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, d_key,
+      k_full_for(chunk_bytes), HashDrain{});
   return int(cudaGetLastError());
 }
 
 int crac_hash_drain_range(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
                           uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
-                          uint32_t* d_crc, uint32_t* d_crc_prev, const uint64_t* d_dst_off,
+                          uint32_t* d_crc, uint32_t* d_crc_prev, uint32_t* d_key,
+                          uint32_t* d_key_prev, const uint64_t* d_dst_off,
                           uint8_t* host_image, unsigned long long* d_counters, void* stream) {
   if (c_hi <= c_lo) return 0;
   if (chunk_bytes == 0 || chunk_bytes % 512) return int(cudaErrorInvalidValue);
   if (int rc = crac_gpu_init()) return rc;
   uint64_t blocks = (c_hi - c_lo + kK1Warps - 1) / kK1Warps;
   if (blocks > uint64_t(sm_count())) blocks = sm_count();
-  if (!d_crc_prev || !d_counters) return int(cudaErrorInvalidValue);
-  k1_chunk_crc<16, 1><<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
-      d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, k_full_for(chunk_bytes),
-      HashDrain{d_crc_prev, d_dst_off, host_image, d_counters, nullptr, nullptr, 0});
+  if (!d_crc_prev || !d_counters || (!d_key) != (!d_key_prev)) return int(cudaErrorInvalidValue);
+  k1_chunk_crc<16, 1, true><<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
+      d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, d_key,
+      k_full_for(chunk_bytes),
+      HashDrain{d_crc_prev, d_key_prev, d_dst_off, host_image, d_counters, nullptr, nullptr, 0});
   return int(cudaGetLastError());
 }
 
 int crac_hash_drain_split(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
                           uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
-                          uint32_t* d_crc, uint32_t* d_crc_prev, const uint64_t* d_dst_off,
+                          uint32_t* d_crc, uint32_t* d_crc_prev, uint32_t* d_key,
+                          uint32_t* d_key_prev, const uint64_t* d_dst_off,
                           uint8_t* host_image, unsigned long long* d_counters,
                           unsigned long long* d_queue, uint32_t n_writers, void* stream) {
   if (c_hi <= c_lo) return 0;
   if (chunk_bytes == 0 || chunk_bytes % 512) return int(cudaErrorInvalidValue);
-  if (!d_crc_prev || !d_counters || !d_queue || n_writers == 0) return int(cudaErrorInvalidValue);
+  if (!d_crc_prev || !d_counters || !d_queue || n_writers == 0 || (!d_key) != (!d_key_prev))
+    return int(cudaErrorInvalidValue);
   if (int rc = crac_gpu_init()) return rc;
   // one CTA per SM (128 KiB of tables each): every CTA of the grid is resident
   // at once, writers included, and hashers get all the other SMs
@@ -1243,25 +1335,28 @@ int crac_hash_drain_split(const crac_span_t* d_spans, const uint64_t* d_chunk_fi
   cudaStream_t st = cudaStream_t(stream);
   const uint64_t q = c_hi - c_lo + uint64_t(n_writers) * kK1Warps + 1;
   if (cudaError_t e = cudaMemsetAsync(d_queue, 0, q * 8, st); e != cudaSuccess) return int(e);
-  k1_chunk_crc<16, 4><<<unsigned(hashers + n_writers), kK1Threads, kTabBytes, st>>>(
-      d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, k_full_for(chunk_bytes),
-      HashDrain{d_crc_prev, d_dst_off, host_image, d_counters, d_queue, d_counters + 2, n_writers});
+  k1_chunk_crc<16, 4, true><<<unsigned(hashers + n_writers), kK1Threads, kTabBytes, st>>>(
+      d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, d_key,
+      k_full_for(chunk_bytes),
+      HashDrain{d_crc_prev, d_key_prev, d_dst_off, host_image, d_counters, d_queue, d_counters + 2,
+                n_writers});
   return int(cudaGetLastError());
 }
 
 int crac_hash_copy_range(const crac_span_t* d_spans, const uint64_t* d_chunk_first,
                          uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
-                         uint32_t* d_crc, const uint64_t* d_dst_off, uint8_t* d_dst,
-                         int dst_aligned, void* stream) {
+                         uint32_t* d_crc, uint32_t* d_key, const uint64_t* d_dst_off,
+                         uint8_t* d_dst, int dst_aligned, void* stream) {
   if (c_hi <= c_lo) return 0;
   if (chunk_bytes == 0 || chunk_bytes % 512) return int(cudaErrorInvalidValue);
   if (int rc = crac_gpu_init()) return rc;
   uint64_t blocks = (c_hi - c_lo + kK1Warps - 1) / kK1Warps;
   if (blocks > uint64_t(sm_count())) blocks = sm_count();
-  auto kern = dst_aligned ? k1_chunk_crc<16, 2> : k1_chunk_crc<8, 3>;
+  auto kern = d_key ? (dst_aligned ? k1_chunk_crc<16, 2, true> : k1_chunk_crc<8, 3, true>)
+                    : (dst_aligned ? k1_chunk_crc<16, 2, false> : k1_chunk_crc<8, 3, false>);
   kern<<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
-      d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, k_full_for(chunk_bytes),
-      HashDrain{nullptr, d_dst_off, d_dst, nullptr});
+      d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, d_key,
+      k_full_for(chunk_bytes), HashDrain{nullptr, nullptr, d_dst_off, d_dst, nullptr});
   return int(cudaGetLastError());
 }
 

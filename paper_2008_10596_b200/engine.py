@@ -131,15 +131,18 @@ _SIGS = {
     "crac_gpu_init": (C.c_int, []),
     "crac_chunk_crc32": (C.c_int, [_P, _P, _U32, _U32, _U64, _P, _P]),
     "crac_chunk_crc32_range": (C.c_int, [_P, _P, _U32, _U32, _U64, _U64, _P, _U32, _P]),
+    "crac_chunk_key_range": (C.c_int, [_P, _P, _U32, _U32, _U64, _U64, _P, _P, _U32, _P]),
     "crac_gather_chunks_to_host": (C.c_int, [_P, _P, _U32, _U32, _P, _U64, _U64, _P, _P, _P]),
     "crac_write_frames": (C.c_int, [_P, _U32, _P, _P]),
-    "crac_hash_copy_range": (C.c_int, [_P, _P, _U32, _U32, _U64, _U64, _P, _P, _P, C.c_int, _P]),
+    "crac_hash_copy_range": (C.c_int, [_P, _P, _U32, _U32, _U64, _U64, _P, _P, _P, _P, C.c_int,
+                                       _P]),
     "crac_gather_chunks_to_host_dev": (C.c_int, [_P, _P, _U32, _U32, _P, _P, _U64, _U32, _P, _P, _P]),
     "crac_diff_compact_range": (C.c_int, [_P, _P, _U64, _U64, _P, _P, _P, _P]),
     "crac_fold_sections": (C.c_int, [_P, _U32, _P, _P, _U32, _P, _U64, _U64, _P, _P]),
-    "crac_hash_drain_range": (C.c_int, [_P, _P, _U32, _U32, _U64, _U64, _P, _P, _P, _P, _P, _P]),
+    "crac_hash_drain_range": (C.c_int, [_P, _P, _U32, _U32, _U64, _U64, _P, _P, _P, _P, _P, _P,
+                                        _P, _P]),
     "crac_hash_drain_split": (C.c_int, [_P, _P, _U32, _U32, _U64, _U64, _P, _P, _P, _P, _P, _P,
-                                        _U32, _P]),
+                                        _P, _P, _U32, _P]),
     "crac_pack_records": (C.c_int, [_P, _U32, _P, _U64, _U64, _P, _P]),
     "crac_scatter_records": (C.c_int, [_P, _U32, _P, _P, _U64, _U64, _P]),
     "crac_diff_compact": (C.c_int, [_P, _P, _U64, _P, _P, _P, _P]),

@@ -136,8 +136,8 @@ def test_fused_hash_drain_writes_only_changed_chunks(eng):
     image = torch.zeros(buf.numel() + 32, dtype=torch.uint8).pin_memory()
     d_off = torch.tensor([16], dtype=torch.int64).cuda()
     counters = torch.zeros(2, dtype=torch.int64).cuda()
-    args = lambda: (_p(spans), _p(first_d), 1, chunk, 0, n, _p(crc), _p(prev), _p(d_off),
-                    _p(image), _p(counters), None)
+    args = lambda: (_p(spans), _p(first_d), 1, chunk, 0, n, _p(crc), _p(prev), None, None,
+                    _p(d_off), _p(image), _p(counters), None)
     assert L.crac_hash_drain_range(*args()) == 0  # prev all zero: everything is dirty
     torch.cuda.synchronize()
     data = bytes(buf.cpu().numpy())
@@ -178,8 +178,8 @@ def test_split_hash_drain_writes_only_changed_chunks(eng, writers):
     d_off = torch.tensor(offs, dtype=torch.int64).cuda()
     counters = torch.zeros(5, dtype=torch.int64).cuda()
     queue = torch.zeros(n + 16 * writers + 1, dtype=torch.int64).cuda()
-    args = lambda: (_p(spans), _p(first_d), 2, chunk, 0, n, _p(crc), _p(prev), _p(d_off),
-                    _p(image), _p(counters), _p(queue), writers, None)
+    args = lambda: (_p(spans), _p(first_d), 2, chunk, 0, n, _p(crc), _p(prev), None, None,
+                    _p(d_off), _p(image), _p(counters), _p(queue), writers, None)
     assert L.crac_hash_drain_split(*args()) == 0  # everything dirty
     torch.cuda.synchronize()
     img = bytes(image.numpy())
@@ -205,7 +205,8 @@ def test_split_hash_drain_writes_only_changed_chunks(eng, writers):
     assert img[offs[1]:offs[1] + 41 * chunk] == bytes(41 * chunk)
     assert img[16 + chunk:16 + 2 * chunk] == bytes(chunk)  # clean chunks untouched
     assert L.crac_hash_drain_split(_p(spans), _p(first_d), 2, chunk, 0, n, _p(crc), _p(prev),
-                                   _p(d_off), _p(image), _p(counters), _p(queue), 0, None) != 0
+                                   None, None, _p(d_off), _p(image), _p(counters), _p(queue), 0,
+                                   None) != 0
 
 
 def test_pack_scatter_round_trip_random_records(eng):
@@ -292,7 +293,7 @@ def test_hash_copy_writes_every_chunk_and_hashes(eng, aligned):
     dst = torch.full((pos + 64,), 0xAB, dtype=torch.uint8).cuda()
     crc = torch.zeros(first[-1], dtype=torch.int32).cuda()
     assert L.crac_hash_copy_range(_p(spans), _p(first_d), len(bufs), chunk, 0, first[-1], _p(crc),
-                                  _p(d_off), _p(dst), aligned, None) == 0
+                                  None, _p(d_off), _p(dst), aligned, None) == 0
     torch.cuda.synchronize()
     out = bytes(dst.cpu().numpy())
     want_crc = []
@@ -304,3 +305,80 @@ def test_hash_copy_writes_every_chunk_and_hashes(eng, aligned):
         prev_end = o + len(h)
         want_crc += [zlib.crc32(h[i:i + chunk]) for i in range(0, len(h), chunk)]
     assert [x & 0xFFFFFFFF for x in crc.cpu().tolist()] == want_crc
+
+
+@pytest.mark.parametrize("chunk", [512, 4096, 65536])
+def test_chunk_key_matches_restatement(eng, chunk):
+    """crac_chunk_key_range: CRC lane == zlib, key lane == tests/dirtykey.py
+    (whatever row batching the chunk size selects), ragged tails included."""
+    from dirtykey import chunk_keys
+    L = eng.lib()
+    sizes = [chunk * 3 + 5, 511, 512, 17, chunk * 2 + 512 * 3 + 33, 1]
+    bufs = [_rand(n, 70 + k).cuda() for k, n in enumerate(sizes)]
+    spans = _spans(bufs)
+    first_d, first = _first(bufs, chunk)
+    crc = torch.zeros(first[-1], dtype=torch.int32).cuda()
+    key = torch.zeros(first[-1], dtype=torch.int32).cuda()
+    assert L.crac_chunk_key_range(_p(spans), _p(first_d), len(bufs), chunk, 0, first[-1], _p(crc),
+                                  _p(key), 0, None) == 0
+    torch.cuda.synchronize()
+    want_crc, want_key = [], []
+    for b in bufs:
+        h = bytes(b.cpu().numpy())
+        want_crc += [zlib.crc32(h[i:i + chunk]) for i in range(0, len(h), chunk)]
+        want_key += chunk_keys(h, chunk)
+    assert [x & 0xFFFFFFFF for x in crc.cpu().tolist()] == want_crc
+    assert [x & 0xFFFFFFFF for x in key.cpu().tolist()] == want_key
+
+
+@pytest.mark.parametrize("split", [False, True])
+def test_forged_crc_collision_is_resent_with_keys(eng, split):
+    """A change that keeps a chunk's CRC-32 (4 compensating bytes) is missed
+    by a CRC-only dirty check and caught by the 64-bit dirty key."""
+    from dirtykey import chunk_key, forge_crc
+    L = eng.lib()
+    chunk = 65536
+    buf = _rand(chunk * 40 + 77, 11).cuda()
+    spans = _spans([buf])
+    first_d, first = _first([buf], chunk)
+    n = first[-1]
+    d_off = torch.tensor([16], dtype=torch.int64).cuda()
+    image = torch.zeros(buf.numel() + 64, dtype=torch.uint8).pin_memory()
+    crc, key = torch.zeros(n, dtype=torch.int32).cuda(), torch.zeros(n, dtype=torch.int32).cuda()
+    counters = torch.zeros(5, dtype=torch.int64).cuda()
+    queue = torch.zeros(n + 16 * 4 + 1, dtype=torch.int64).cuda()
+
+    def run(prev, prev_key, with_key):
+        counters.zero_()
+        k = (_p(key), _p(prev_key)) if with_key else (None, None)
+        if split:
+            rc = L.crac_hash_drain_split(_p(spans), _p(first_d), 1, chunk, 0, n, _p(crc), _p(prev),
+                                         *k, _p(d_off), _p(image), _p(counters), _p(queue), 4, None)
+        else:
+            rc = L.crac_hash_drain_range(_p(spans), _p(first_d), 1, chunk, 0, n, _p(crc), _p(prev),
+                                         *k, _p(d_off), _p(image), _p(counters), None)
+        assert rc == 0
+        torch.cuda.synchronize()
+        return counters.cpu().tolist()[0]
+
+    prev, prev_key = torch.zeros(n, dtype=torch.int32).cuda(), torch.zeros(n, dtype=torch.int32).cuda()
+    assert run(prev, prev_key, True) == n  # seeds both lanes
+    data = bytearray(buf.cpu().numpy().tobytes())
+    assert [x & 0xFFFFFFFF for x in prev_key.cpu().tolist()] == \
+        [chunk_key(bytes(data[i:i + chunk])) for i in range(0, len(data), chunk)]
+    # forge chunk 17: one byte flipped, 4 bytes compensate the CRC
+    c = 17
+    piece = bytearray(data[c * chunk:(c + 1) * chunk])
+    target = zlib.crc32(piece)
+    piece[1000] ^= 0x80
+    forge_crc(piece, 5000, target)
+    buf[c * chunk:(c + 1) * chunk] = torch.frombuffer(bytearray(piece), dtype=torch.uint8).cuda()
+    # CRC lane only: the change is invisible
+    prev_crc_only = prev.clone()
+    image.zero_()
+    assert run(prev_crc_only, None, False) == 0
+    # the 64-bit key sees it and re-sends exactly that chunk
+    assert run(prev, prev_key, True) == 1
+    img = bytes(image.numpy())
+    assert img[16 + c * chunk:16 + (c + 1) * chunk] == bytes(piece)
+    assert img[16:16 + c * chunk] == bytes(c * chunk)

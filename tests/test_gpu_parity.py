@@ -873,3 +873,28 @@ def test_cold_restart_after_dropping_the_arena_cache(eng):
     warm.close()
     eng.drop_arena_cache()
     eng.drop_arena_cache()  # nothing cached: a no-op
+
+
+def test_incremental_resends_a_crc_preserving_change(eng):
+    """SURVEY §7 hard part 5: the dirty key is (CRC-32, chunk key).  A chunk
+    rewritten so its CRC-32 is unchanged is still re-sent; the incremental
+    image equals the reference's full image (and the GPU's own full drain)."""
+    from dirtykey import forge_crc
+    sizes = [(3 << 20) + 4096 * k + 13 * k for k in range(6)]
+    s = eng.Session(seed=1, arena_bytes=64 << 20)
+    r = ref.RefSession(seed=1, arena_bytes=64 << 20)
+    ids = workloads.build_regions(s, 6, lambda k: sizes[k], seed=5)
+    assert workloads.build_regions(r, 6, lambda k: sizes[k], seed=5) == ids
+    image = eng.Image()
+    s.checkpoint_into(image)
+    for k, off in ((2, 65536 * 7), (4, 65536 * 48)):  # chunk 48 of region 4 is its ragged last one
+        cur = bytearray(s.copy_d2h(ids[k], off, min(65536, sizes[k] - off)))
+        target = zlib.crc32(cur)
+        cur[10] ^= 0x01
+        forge_crc(cur, len(cur) - 9, target)
+        for api in (s, r):
+            api.copy_h2d(ids[k], off, bytes(cur))
+    st = s.checkpoint_into(image, incremental=True)
+    assert st["incremental"]
+    assert st["dirty_chunks"] == 2
+    assert image.tobytes() == r.checkpoint()[0] == s.checkpoint()[0]
