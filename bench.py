@@ -6,15 +6,22 @@ Workload (BASELINE.json configs[3], "C4"): every rank owns one B200 holding
 synthetic content.  One step = full checkpoint drain of that state into a
 page-locked host image (crac_checkpoint) + session teardown + restart refill
 from the image (crac_restart: replay, H2D, scatter, CRC verify).  Ranks drain
-independently; the only cross-rank step is a host barrier (gloo), exactly the
-"global barrier" of the config.  Inputs (120 GiB/GPU) exceed L2 by ~1000x.
+independently; the only cross-rank step is the host barrier of the global
+checkpoint (the config's "global barrier").  Inputs (120 GiB/GPU) exceed L2 by ~1000x.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-value  = 2 x live bytes x ranks / (max over ranks of the summed device-event
-         time of the drain and refill operations)
-e2e    = same bytes / (max over ranks of the CUDA-event interval around the K
-         steps through the public C-ABI, host image buffers, teardown included)
+value  = 2 x live bytes x ranks / sum over steps of (max over ranks of the
+         device-event time of that step's drain + refill); the ranks start
+         every step together, so this is max end - min start per step
+e2e    = same bytes / sum over steps of (max over ranks of the CUDA-event
+         interval around the step through the public C-ABI: host image
+         buffers, session teardown and arena release included)
+The restart is cold: the closed session's arena is freed before each refill,
+as in a new process.  With N > 1 ranks every drain meets the other ranks at
+the product's global-checkpoint barrier (crac_barrier, crac_engine.h).
+`--gpus N` outside torchrun spawns the N ranks itself; `--dry-run` runs the
+rank plumbing only (no GPU).
 --impl reference times the reference's own CPU path (oracle/_ref, the
 unmodified library) on the host cores, one sample session per core.
 """
@@ -59,7 +66,28 @@ def parse_args():
     ap.add_argument("--no-cold", action="store_true", help="skip the cold-restart measurement")
     ap.add_argument("--c3-footprint-gib", type=float, default=16.0)
     ap.add_argument("--c5-footprint-gib", type=float, default=64.0)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="rank plumbing only (no GPU): every rank prints its device assignment")
+    ap.add_argument("--no-verify", action="store_true",
+                    help="skip the host-side check of the final image and the restarted state")
     return ap.parse_args()
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: launch N ranks of this script
+    (RANK / LOCAL_RANK / WORLD_SIZE set as torchrun does, one GPU each) and
+    return the worst exit code.  Rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, str(Path(__file__).resolve()), *sys.argv[1:]],
+                                      env=env))
+    return max(p.wait() for p in procs)
 
 
 def dist_env():
@@ -179,6 +207,16 @@ class HostGroup:
         t = torch.tensor([x], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+    def max_list(self, xs: list) -> list:
+        """Elementwise max over ranks (per-step times)."""
+        if self.world == 1:
+            return list(xs)
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor(list(xs), dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
 
     def close(self) -> None:
         if self.world > 1:
@@ -608,7 +646,7 @@ def drop_cache(path: Path) -> None:
         pass
 
 
-def run_file(args, engine, sess, live, group, rank, world, cfg_extra) -> None:
+def run_file(args, engine, sess, live, group, rank, world, cfg_extra, gbar=None) -> None:
     """Persistence: checkpoint_to_file then restart_from_file of
     the C4-shaped state; wall time per phase, storage ceiling beside it."""
     io_dir = Path(args.io_dir or os.environ.get("CRAC_IO_DIR", "/tmp"))
@@ -626,6 +664,8 @@ def run_file(args, engine, sess, live, group, rank, world, cfg_extra) -> None:
         t2 = time.perf_counter()
         sess, refill, rio = engine.restart_from_file(path, staging)
         t3 = time.perf_counter()
+        if gbar:
+            sess.set_barrier(gbar)
         rows.append({"ckpt_s": t1 - t0, "restart_s": t3 - t2, "drain_ms": drain["total_ms"],
                      "write_ms": wio["ms"], "read_ms": rio["ms"], "refill_ms": refill["total_ms"],
                      "direct": wio["direct"] and rio["direct"], "bytes": wio["bytes"]})
@@ -692,11 +732,37 @@ def cpu_baseline_file(sample_gib: float, region: int, io_dir: Path) -> dict:
                          "restart_from_file_s": round(t["total_s"], 3)}}
 
 
+def dry_run(args, world, rank, local) -> None:
+    """The N-rank plumbing without a GPU: the device each rank would own, the
+    gloo group, and the product's shared-memory checkpoint barrier."""
+    pin_device(local, world)
+    group = HostGroup(world, rank)
+    from paper_2008_10596_b200 import engine
+    b = engine.Barrier(barrier_name(world), world, rank, timeout_ms=60000)
+    b.wait()
+    group.barrier()
+    print(json.dumps({"dry_run": True, "rank": rank, "world": world, "local_rank": local,
+                      "cuda_visible_devices": os.environ.get("CUDA_VISIBLE_DEVICES"),
+                      "barrier_generation": b.generation()}), flush=True)
+    group.barrier()
+    b.close(unlink=rank == 0)
+    group.close()
+
+
+def barrier_name(world: int) -> str:
+    return f"/crac_bench_{os.environ.get('MASTER_PORT', '0')}_{world}"
+
+
 def main() -> None:
     args = parse_args()
+    if args.gpus > 1 and "RANK" not in os.environ and args.impl == "b200":
+        sys.exit(spawn_ranks(args.gpus))
     world, rank, local, local_world = dist_env()
     if args.impl == "reference":
         run_reference(args, world, rank)
+        return
+    if args.dry_run:
+        dry_run(args, world, rank, local)
         return
     pin_device(local, world)
 
@@ -705,6 +771,9 @@ def main() -> None:
 
     group = HostGroup(world, rank)
     barrier, max_over_ranks = group.barrier, group.max
+    # the product's global-checkpoint barrier (crac_engine.h): every drain of
+    # every rank meets the others at quiesce-complete and image-complete
+    gbar = engine.Barrier(barrier_name(world), world, rank, timeout_ms=600000) if world > 1 else None
 
     torch.cuda.set_device(0)
     # host RAM bounds the per-rank image; HBM bounds the per-rank state
@@ -717,11 +786,20 @@ def main() -> None:
 
     t_setup = time.perf_counter()
     sess, live, cfg_extra = build_workload(args, engine, rank, min(host_cap, dev_cap))
+    want = cfg_extra.get("requested_footprint_gib")
+    if want and live < int(want * GIB) // (args.region_mib * MIB) * args.region_mib * MIB:
+        cfg_extra["footprint_reduced"] = {
+            "requested_gib": want, "actual_gib": round(live / GIB, 3),
+            "reason": f"host RAM for {local_world} pinned images ({mem_available() // GIB} GiB "
+                      f"available) or HBM bounds the per-rank state"}
+        print(f"WARNING: footprint reduced to {live / GIB:.1f} GiB per rank", file=sys.stderr)
     image = engine.Image()
     setup_s = time.perf_counter() - t_setup
+    if gbar:
+        sess.set_barrier(gbar)
     if args.workload == "file":
         image.close()
-        run_file(args, engine, sess, live, group, rank, world, cfg_extra)
+        run_file(args, engine, sess, live, group, rank, world, cfg_extra, gbar)
         group.close()
         return
     if args.workload == "c5":
@@ -731,10 +809,16 @@ def main() -> None:
         return
 
     def step(s):
+        """One checkpoint + restart, as a restart in a new process sees it:
+        the drain, the old session's teardown, its arena freed (no cached
+        mapping survives), then the refill from the host image."""
         dr = s.checkpoint_into(image)
         addr, n = image.address()
         s.close()
+        engine.drop_arena_cache()
         s2, rf = engine.restart_from_address(addr, n)
+        if gbar:
+            s2.set_barrier(gbar)
         return s2, dr, rf
 
     t_warm = time.perf_counter()
@@ -745,30 +829,59 @@ def main() -> None:
     clocks = ClockSampler() if rank == 0 else None
     if clocks:
         clocks.start()
-    barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
+    drains, refills, e2e_steps = [], [], []
     wall0 = time.perf_counter()
-    drains, refills = [], []
     for _ in range(args.steps):
+        barrier()  # every rank starts the step together
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
         sess, dr, rf = step(sess)
+        ev1.record()
+        torch.cuda.synchronize()
         drains.append(dr)
         refills.append(rf)
-    ev1.record()
-    torch.cuda.synchronize()
+        e2e_steps.append(ev0.elapsed_time(ev1))
     wall = time.perf_counter() - wall0
     barrier()
-    e2e_ms = ev0.elapsed_time(ev1)
     clk = clocks.stop() if clocks else None
 
-    dev_ms = sum(d["total_ms"] for d in drains) + sum(r["total_ms"] for r in refills)
-    dev_ms_max = max_over_ranks(dev_ms)
-    e2e_ms_max = max_over_ranks(e2e_ms)
+    # whole box: each step lasts until its slowest rank is done (the ranks
+    # start it together), i.e. max end - min start per step, summed
+    dev_steps = group.max_list(
+        [d["total_ms"] + r["total_ms"] for d, r in zip(drains, refills)])
+    e2e_steps_max = group.max_list(e2e_steps)
+    dev_ms_max = sum(dev_steps)
+    e2e_ms_max = sum(e2e_steps_max)
     drain_ms = max_over_ranks(sum(d["total_ms"] for d in drains) / args.steps)
     refill_ms = max_over_ranks(sum(r["total_ms"] for r in refills) / args.steps)
 
-    # kernel roofline: the kernel with the largest device time in the step
+    # independent checks of the last step (outside the timed region): the
+    # image on the host cores against recomputed CRCs and regenerated
+    # content, the restarted (cold) device state against regenerated content
+    verified = None
+    if not args.no_verify:
+        seed = rank + 1
+        synth = args.workload == "c4"
+        rep = engine.verify_image(address=image.address(), synth_seed=seed if synth else None)
+        dev = sess.verify_synthetic(seed) if synth else None
+        ok = rep["ok"] and (dev is None or dev["bad_allocations"] == 0)
+        ok = bool(max_over_ranks(0.0 if ok else 1.0) == 0.0)
+        verified = {
+            "ok": ok,
+            "image": {k: rep[k] for k in ("sections_checked", "crc_bytes", "payloads_compared",
+                                          "payload_bytes_compared", "mismatched_payloads",
+                                          "bad_sections", "threads")} | {"s": round(rep["ms"] / 1e3, 2)},
+            "restarted_state": dev,
+            "method": "host: every section CRC recomputed on all host cores (PCLMUL, no GPU code) "
+                      "and every Device payload compared with f(seed, id, offset) regenerated "
+                      "(crac_image_verify); device: the state the last (cold) restart refilled "
+                      "compared word by word with the regenerated content "
+                      "(crac_session_verify_synthetic); all ranks"}
+        if not ok:
+            print(f"VERIFY FAILED on rank {rank}: {rep} {dev}", file=sys.stderr)
+
+    # kernels in the timed region, each against HBM
     def mean(key, xs):
         return statistics.mean(x[key] for x in xs)
     kernels = {}
@@ -786,32 +899,31 @@ def main() -> None:
         n = refills[-1]["hash_launches"]
         kernels["k1_chunk_crc (refill verify)"] = (mean("hash_ms", refills) / n,
                                                    refills[-1]["hash_bytes"] / n, n)
-    # The roofline kernel is the hash (the north star: "achieved HBM GB/s of
-    # the hash/compaction kernels against ~8 TB/s"); it also reads every byte
-    # of the state.  With direct runs the pack/scatter only produce the edges
-    # around the copy engine's direct copies (a few hundred KiB per window,
-    # launch-latency bound), so every kernel is listed beside it.
     by_time = max(kernels, key=lambda k: kernels[k][0] * kernels[k][2]) if kernels else None
-    dom = "k1_chunk_crc" if "k1_chunk_crc" in kernels else by_time
-    dom_ms, dom_bytes, _ = kernels[dom] if dom else (0.0, 0, 0)
-    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
-    traffic, traffic_src = ncu_traffic(dom)
-    if traffic is not None and traffic < 16:  # a ratio: scale to this launch
-        traffic = int(traffic * dom_bytes)
+    kern_rows = {}
+    for k, (ms, nbytes, launches) in kernels.items():
+        gbps = nbytes / (ms * 1e6) if ms else 0.0
+        traffic, src = ncu_traffic(k)
+        if traffic is not None and traffic < 16:  # a ratio: scale to this launch
+            traffic = int(traffic * nbytes)
+        kern_rows[k] = {"bound": "hbm", "achieved": round(gbps, 1), "peak": hbm, "unit": "GB/s",
+                        "frac": round(gbps / hbm, 4), "traffic": traffic, "traffic_source": src,
+                        "avg_launch_ms": round(ms, 4), "bytes_per_launch": int(nbytes),
+                        "launches": launches, "device_ms_per_step": round(ms * launches, 3)}
 
-    # cold restart (outside the timed loop): the arena a closed session leaves
-    # for the next one is freed first, so this restart maps its physical
-    # memory afresh, as a restart in a new process does
-    cold = None
+    # cold restart is now the timed step itself; the warm-arena variant is
+    # reported beside it for comparison (arena adopted from the closed session)
+    warm = None
     if not args.no_cold:
         sess.checkpoint_into(image)
         addr, n = image.address()
         sess.close()
-        engine.drop_arena_cache()
         sess, rf = engine.restart_from_address(addr, n)
-        cold = {"restart_ms": round(rf["total_ms"], 3),
+        if gbar:
+            sess.set_barrier(gbar)
+        warm = {"restart_ms": round(rf["total_ms"], 3),
                 "restart_GBps": round(live / (rf["total_ms"] * 1e-3) / 1e9, 3),
-                "note": "arena cache dropped first: physical memory mapped inside the restart"}
+                "note": "arena of the closed session adopted (mapped memory reused), not the headline"}
 
     # incremental (C5 shape on the resident state): hash-only and a 1 % dirty drain
     incremental = None
@@ -852,6 +964,7 @@ def main() -> None:
         link = 2 / (1 / pd + 1 / ph)  # one drain + one refill of the same bytes
         d2h = drains[-1]["d2h_bytes"] / (mean("copy_ms", drains) * 1e-3) / 1e9 if mean("copy_ms", drains) else 0
         h2d = refills[-1]["h2d_bytes"] / (mean("copy_ms", refills) * 1e-3) / 1e9 if mean("copy_ms", refills) else 0
+        per_gpu = value / world
         line = {
             "metric": "checkpoint & restart GB/s per GPU and whole box at 1/2/4/8 B200; % of roofline",
             "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -860,47 +973,49 @@ def main() -> None:
             "data": "synthetic",
             "config": {"workload": WORKLOAD_NAMES[args.workload], "live_bytes_per_gpu": live,
                        **cfg_extra, "parallelism": f"independent drains x{world}",
+                       "global_barrier": "crac_barrier (shared memory) at quiesce-complete and "
+                                         "image-complete of every drain" if world > 1 else None,
+                       "restart": "cold: the closed session's arena is freed before each refill",
                        "l2": "inputs larger than L2" if live > 256 * MIB else "inputs may fit L2"},
             "per_gpu": {"checkpoint_GBps": round(live / (drain_ms * 1e-3) / 1e9, 3),
                         "restart_GBps": round(live / (refill_ms * 1e-3) / 1e9, 3),
                         "checkpoint_ms": round(drain_ms, 3), "restart_ms": round(refill_ms, 3),
-                        "image_bytes": drains[-1]["image_bytes"], "cold_restart": cold},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
-                         "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                         "traffic": traffic, "traffic_source": traffic_src,
-                         "peak_source": peaks["source"],
-                         "algorithmic_bytes_per_launch": int(dom_bytes),
-                         "avg_launch_ms": round(dom_ms, 4),
-                         "largest_device_time": by_time,
-                         "in_situ": {k: {"avg_launch_ms": round(v[0], 4),
-                                         "bytes_per_launch": int(v[1]), "launches": v[2],
-                                         "GBps": round(v[1] / (v[0] * 1e6), 1) if v[0] else 0.0,
-                                         "frac": round(v[1] / (v[0] * 1e6) / hbm, 4) if v[0] else 0.0}
-                                     for k, v in kernels.items()},
+                        "restart_host_pre_ms": round(mean("host_pre_ms", refills), 3),
+                        "image_bytes": drains[-1]["image_bytes"], "warm_restart": warm},
+            "roofline": {"bound": "pcie", "achieved": round(per_gpu, 3), "peak": round(link, 2),
+                         "unit": "GB/s", "frac": round(per_gpu / link, 4),
+                         "traffic": drains[-1]["d2h_bytes"] + refills[-1]["h2d_bytes"],
+                         "how": "state bytes per GPU per second of drain + refill against the "
+                                "harmonic mean of this GPU's measured D2H and H2D copy-engine "
+                                "peaks (every state byte crosses the link once each way); "
+                                "traffic = link bytes per step",
+                         "peak_source": "measured in this run (best of 5 passes of 2 GiB in 16 and "
+                                        "64 MiB pinned copies)",
+                         "d2h_GBps": round(d2h, 2), "h2d_GBps": round(h2d, 2),
+                         "d2h_peak_GBps": pd, "h2d_peak_GBps": ph,
+                         "d2h_GBps_per_step": [round(d["d2h_bytes"] / (d["copy_ms"] * 1e6), 2)
+                                               for d in drains if d["copy_ms"]],
+                         "h2d_GBps_per_step": [round(r["h2d_bytes"] / (r["copy_ms"] * 1e6), 2)
+                                               for r in refills if r["copy_ms"]],
+                         "dominant_kernel": by_time,
+                         "kernels": kern_rows,
+                         "hbm_peak_source": peaks["source"],
                          "isolated": {k: {**v, "frac": round(v["GBps"] / hbm, 4)}
                                       for k, v in isolated.items()},
-                         "note": "kernel = the hash over the whole state (K1, one launch "
-                                 "per drain on all but 16 SMs, beside the D2H); in_situ = every "
-                                 "kernel in the timed region (pack/scatter per window: only "
-                                 "the edges around the direct copies of big payloads); HBM "
-                                 "copies beside PCIe traffic run ~2x slower, cudaMemcpy D2D "
-                                 "included (isolated.d2d_copy_beside_d2h, "
-                                 "profiles/r01/copy_interference.txt); 'isolated' = the "
-                                 "kernel back to back on one stream; traffic = ncu DRAM bytes "
-                                 "per launch"},
-            "pcie_roofline": {"d2h_GBps": round(d2h, 2), "h2d_GBps": round(h2d, 2),
-                              "d2h_peak_GBps": pd, "h2d_peak_GBps": ph,
-                              "peak_source": "measured in this run (best of 5 passes of 2 GiB in 16 and 64 MiB pinned copies)",
-                              "binding_GBps": round(link, 2),
-                              "d2h_GBps_per_step": [round(d["d2h_bytes"] / (d["copy_ms"] * 1e6), 2)
-                                                    for d in drains if d["copy_ms"]],
-                              "h2d_GBps_per_step": [round(r["h2d_bytes"] / (r["copy_ms"] * 1e6), 2)
-                                                    for r in refills if r["copy_ms"]],
-                              "value_frac": round(value / world / link, 4)},
+                         "note": "kernels = every kernel of the timed region against HBM, CUDA "
+                                 "events on the engine streams; k1_chunk_crc = the hash over the "
+                                 "whole state (one launch per drain beside the D2H); pack/scatter "
+                                 "per window produce only the edges around the direct copies; "
+                                 "'isolated' = back to back on one stream; traffic = ncu DRAM "
+                                 "bytes per launch (profiles/)"},
             "e2e": {"value": round(e2e, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": refills[-1]["h2d_bytes"],
                     "d2h_bytes_per_step": drains[-1]["d2h_bytes"],
-                    "wall_s": round(wall, 3)},
+                    "wall_s": round(wall, 3),
+                    "how": "CUDA events around each step through the public API (drain into the "
+                           "pinned host image, session teardown + arena release, refill from "
+                           "the host image), max over ranks per step"},
+            "verified": verified,
             "gpu_launches": launches,
             "image_pages": image.pages(),
             "clocks": clk,
@@ -911,6 +1026,9 @@ def main() -> None:
         }
         print(json.dumps(line), flush=True)
     sess.close()
+    if gbar:
+        barrier()
+        gbar.close(unlink=rank == 0)
     group.close()
 
 

@@ -33,10 +33,13 @@ typedef struct crac_stats {
   int32_t reserved;
   double stall_ms;       /* quiesce -> the app may resume */
   uint64_t shadow_bytes; /* stream bytes staged in the HBM shadow */
+  double barrier_ms;     /* host wait in the global-checkpoint hook (ABI 2) */
+  double host_pre_ms;    /* refill: parse + set-up before the first device event,
+                            included in total_ms (ABI 2) */
 } crac_stats_t;
 
 const char* crac_last_error(void);
-int crac_abi_version(void); /* 1 */
+int crac_abi_version(void); /* 2: crac_stats_t grew barrier_ms/host_pre_ms; barrier API */
 
 /* Session — ref: include/cracsim/ckpt_engine.hpp:18-55 (SessionConfig, Session) */
 int crac_session_create(uint64_t seed, uint64_t arena_bytes, int mode, uint32_t quiesce_timeout_ms,
@@ -86,6 +89,52 @@ int crac_checkpoint_incremental(crac_session_t* s, crac_image_t* img, crac_stats
  * crac_checkpoint_finish completes it.  Bytes equal crac_checkpoint's at the
  * instant of begin.  crac_reserve_shadow(s, 0) releases the reservation;
  * OutOfArena (1 + 1) if the HBM is not available. */
+/* Global checkpoint across the per-GPU processes of a job (the
+ * reference is single-process, ckpt_engine.cpp:29-61 quiesces one table).
+ * With a hook set, every checkpoint entry point calls fn(ctx, phase) at
+ *   CRAC_PHASE_QUIESCED        inside the quiesce, before any state is read;
+ *   CRAC_PHASE_IMAGE_COMPLETE  once this rank's image is complete (for
+ *                              crac_checkpoint_begin: in crac_checkpoint_finish);
+ *   CRAC_PHASE_PERSISTED       crac_checkpoint_to_file, after the fdatasync.
+ * fn returns 0 when every rank arrived; nonzero fails the checkpoint with
+ * QuiesceTimeout (the application is resumed).  fn = NULL removes the hook. */
+#define CRAC_PHASE_QUIESCED 0
+#define CRAC_PHASE_IMAGE_COMPLETE 1
+#define CRAC_PHASE_PERSISTED 2
+typedef int (*crac_barrier_fn)(void* ctx, int phase);
+int crac_session_set_barrier(crac_session_t* s, crac_barrier_fn fn, void* ctx);
+/* Built-in hook for the ranks of one node: a barrier in POSIX shared memory
+ * (name "/x", created by the first opener; every rank passes the same world).
+ * crac_barrier_wait returns QuiesceTimeout (12) after timeout_ms, with its
+ * arrival withdrawn.  Install with crac_session_set_barrier(s, crac_barrier_hook, b). */
+typedef struct crac_barrier crac_barrier_t;
+int crac_barrier_open(const char* name, uint32_t world, uint32_t rank, uint32_t timeout_ms,
+                      crac_barrier_t** out);
+int crac_barrier_wait(crac_barrier_t* b);
+int crac_barrier_hook(void* b, int phase); /* a crac_barrier_fn; b = crac_barrier_t* */
+uint64_t crac_barrier_generation(crac_barrier_t* b);
+void crac_barrier_close(crac_barrier_t* b, int unlink);
+
+/* Independent host check of an image (no GPU, no code shared with the drain):
+ * strict parse, every section CRC recomputed on `threads` host cores (0 = all),
+ * and with check_synth every Device payload compared byte for byte with the
+ * synthetic content f(synth_seed, id, offset) of crac_fill_synthetic.  Returns
+ * 0 with the findings in *out (a failed check is a finding, not an error);
+ * ImageCorrupt when the framing itself is invalid. */
+typedef struct crac_verify {
+  uint64_t sections_checked, crc_bytes;
+  uint64_t payloads_compared, payload_bytes_compared, mismatched_payloads, first_bad_id;
+  uint32_t bad_sections; /* bit s: recomputed CRC of section s+1 differs */
+  uint32_t threads;
+  double ms;
+} crac_verify_t;
+int crac_image_verify(const void* image, uint64_t size, uint32_t threads, uint64_t synth_seed,
+                      int check_synth, crac_verify_t* out);
+/* Compares every live Device allocation of `s` on the GPU with
+ * f(seed, id, offset); *bad_allocations = allocations with any differing word. */
+int crac_session_verify_synthetic(crac_session_t* s, uint64_t seed, uint64_t* bad_allocations,
+                                  uint64_t* bytes_checked);
+
 int crac_reserve_shadow(crac_session_t* s, uint64_t bytes);
 /* The shadow in another GPU's HBM (SURVEY §8f.3 buddy copy): reachable by
  * peer access (InvalidArgument otherwise); `device` = this session's GPU is

@@ -192,6 +192,10 @@ int crac_gather_chunks(const crac_span_t* d_spans, const uint64_t* d_chunk_first
  * Word k of allocation `id`: mix64(k + 0x1000003*id + (seed << 56)), LE. */
 int crac_fill_synth(uint8_t* d_dst, uint64_t len, uint64_t seed, uint64_t id,
                     uint64_t word_offset, void* stream);
+/* Sets *d_flag = 1 if any byte of [d_src, +len) differs from the synthetic
+ * content of crac_fill_synth(seed, id, word offset 0); leaves it otherwise. */
+int crac_verify_synth(const uint8_t* d_src, uint64_t len, uint64_t seed, uint64_t id,
+                      uint32_t* d_flag, void* stream);
 
 /* Rewrites chunk c of span s iff mix64(seed ^ (epoch << 40) ^ (chunk_first[s]+c)) <
  * threshold, with synth content of seed' = seed + epoch (ids from d_ids). */

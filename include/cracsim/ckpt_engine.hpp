@@ -23,6 +23,7 @@
 #include <chrono>
 #include <memory>
 
+#include "cracsim/global_barrier.hpp"
 #include "cracsim/image.hpp"
 #include "cracsim/image_io.hpp"
 
@@ -54,6 +55,15 @@ class Session {
   std::vector<uint8_t>& app_state() { return app_state_; }
   const SessionConfig& config() const { return cfg_; }
   DrainEngine& drain_engine();
+  // Global-checkpoint hook (global_barrier.hpp); called by every checkpoint
+  // entry point at kPhaseQuiesced and kPhaseImageComplete.
+  void set_barrier(GlobalBarrier b) { barrier_ = b; }
+  const GlobalBarrier& barrier() const { return barrier_; }
+  // Runs the hook (no-op without one); a nonzero return raises QuiesceTimeout.
+  // The wait is added to barrier_ms.
+  void global_barrier(int phase);
+  double barrier_ms = 0;     // host time in the hook during the last checkpoint
+  bool commit_armed = false; // a checkpoint_begin awaits its kPhaseImageComplete
 
  private:
   SessionConfig cfg_;
@@ -63,6 +73,7 @@ class Session {
   std::unique_ptr<DispatchTable> table_;
   std::vector<uint8_t> app_state_;
   std::unique_ptr<DrainEngine> drain_;
+  GlobalBarrier barrier_;
 };
 
 // Page-locked host buffer holding one image; reused across checkpoints.  The
@@ -115,6 +126,9 @@ struct DrainStats {
   bool incremental = false;
   double stall_ms = 0;       // quiesce -> app may resume (device events)
   uint64_t shadow_bytes = 0; // stream bytes staged in the HBM shadow
+  double barrier_ms = 0;     // host wait in the global-checkpoint hook
+  double host_pre_ms = 0;    // refill: parse + session set-up before the first
+                             // device event (included in total_ms)
 };
 
 // ---- reference surface ----

@@ -33,7 +33,8 @@ EXTRA = {
     "kernels.cu": ["-Xptxas", "-v"] if os.environ.get("CRAC_PTXAS_V") else [],
 }
 SOURCES = ["kernels.cu", "device_core.cu", "drain.cu", "std_kernels.cu",
-           "shim.cpp", "image.cpp", "image_io.cpp", "crc_host.cpp", "ckpt_engine.cpp", "capi.cpp"]
+           "shim.cpp", "image.cpp", "image_io.cpp", "crc_host.cpp", "ckpt_engine.cpp", "capi.cpp",
+           "global_barrier.cpp", "verify.cpp"]
 
 
 def _headers_mtime() -> float:
@@ -62,7 +63,8 @@ def build(force: bool = False) -> Path:
         objs = list(ex.map(lambda s: _compile(s, force, hdr), SOURCES))
     newest = max(o.stat().st_mtime for o in objs)
     if force or not LIB.exists() or LIB.stat().st_mtime < newest:
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lz", "-lpthread"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lz", "-lpthread",
+               "-Xlinker", "--no-undefined"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -3,6 +3,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 
 #include "crac_engine.h"
 #include "crac_gpu.h"
@@ -10,6 +11,11 @@
 #include "image_codec.hpp"
 
 using namespace cracsim;
+
+namespace cracsim {
+void verify_image(const void* image, uint64_t size, uint32_t threads, uint64_t synth_seed,
+                  int check_synth, crac_verify_t* out);  // verify.cpp
+}
 
 struct crac_session {
   Session s;
@@ -61,6 +67,8 @@ void to_c(const DrainStats& d, crac_stats_t* o) {
   o->incremental = d.incremental ? 1 : 0;
   o->stall_ms = d.stall_ms;
   o->shadow_bytes = d.shadow_bytes;
+  o->barrier_ms = d.barrier_ms;
+  o->host_pre_ms = d.host_pre_ms;
 }
 
 void to_c(const FileIoStats& f, crac_io_stats_t* o) {
@@ -80,7 +88,7 @@ T* heap_copy(const T* p, size_t n) {
 extern "C" {
 
 const char* crac_last_error(void) { return g_err.c_str(); }
-int crac_abi_version(void) { return 1; }
+int crac_abi_version(void) { return 2; }
 
 int crac_session_create(uint64_t seed, uint64_t arena_bytes, int mode, uint32_t timeout_ms,
                         crac_session_t** out) {
@@ -249,6 +257,72 @@ int crac_checkpoint(crac_session_t* s, crac_image_t* img, crac_stats_t* stats) {
     checkpoint_image(s->s, img->img, stats ? &d : nullptr);
     to_c(d, stats);
   });
+}
+
+int crac_image_verify(const void* image, uint64_t size, uint32_t threads, uint64_t synth_seed,
+                      int check_synth, crac_verify_t* out) {
+  return guard([&] { verify_image(image, size, threads, synth_seed, check_synth, out); });
+}
+
+int crac_session_verify_synthetic(crac_session_t* s, uint64_t seed, uint64_t* bad_allocations,
+                                  uint64_t* bytes_checked) {
+  return guard([&] {
+    DeviceContext& ctx = s->s.device();
+    std::vector<AllocationRecord> dev;
+    for (const auto& r : ctx.live_records())
+      if (r.kind == AllocationKind::Device) dev.push_back(r);
+    uint32_t* d_flags = nullptr;
+    check_cuda(cudaMalloc(&d_flags, 4 * (dev.size() + 1)), "verify flags");
+    std::unique_ptr<uint32_t, decltype(&cudaFree)> keep(d_flags, &cudaFree);
+    check_cuda(cudaMemset(d_flags, 0, 4 * (dev.size() + 1)), "verify memset");
+    uint64_t bytes = 0;
+    for (size_t k = 0; k < dev.size(); ++k) {
+      const uint64_t p = ctx.backing_ptr(dev[k].id);
+      check_cuda(cudaError_t(crac_verify_synth(reinterpret_cast<const uint8_t*>(p), dev[k].size,
+                                               seed, dev[k].id, d_flags + k, nullptr)),
+                 "verify synth");
+      bytes += dev[k].size;
+    }
+    std::vector<uint32_t> h(dev.size() + 1);
+    check_cuda(cudaMemcpy(h.data(), d_flags, 4 * h.size(), cudaMemcpyDeviceToHost), "verify readback");
+    uint64_t bad = 0;
+    for (size_t k = 0; k < dev.size(); ++k) bad += h[k] != 0;
+    *bad_allocations = bad;
+    *bytes_checked = bytes;
+  });
+}
+
+int crac_session_set_barrier(crac_session_t* s, crac_barrier_fn fn, void* ctx) {
+  return guard([&] { s->s.set_barrier(GlobalBarrier{fn, ctx}); });
+}
+
+int crac_barrier_open(const char* name, uint32_t world, uint32_t rank, uint32_t timeout_ms,
+                      crac_barrier_t** out) {
+  return guard([&] {
+    if (!name || !out) raise(Errc::InvalidArgument, "crac_barrier_open: null argument");
+    *out = reinterpret_cast<crac_barrier_t*>(
+        new ShmBarrier(name, world, rank, std::chrono::milliseconds(timeout_ms)));
+  });
+}
+
+int crac_barrier_wait(crac_barrier_t* b) {
+  return guard([&] {
+    if (!reinterpret_cast<ShmBarrier*>(b)->wait())
+      raise(Errc::QuiesceTimeout, "barrier wait timed out");
+  });
+}
+
+int crac_barrier_hook(void* b, int phase) { return ShmBarrier::hook(b, phase); }
+
+uint64_t crac_barrier_generation(crac_barrier_t* b) {
+  return reinterpret_cast<ShmBarrier*>(b)->generation();
+}
+
+void crac_barrier_close(crac_barrier_t* b, int unlink) {
+  auto* p = reinterpret_cast<ShmBarrier*>(b);
+  if (!p) return;
+  if (unlink) p->unlink_on_close();
+  delete p;
 }
 
 int crac_reserve_shadow(crac_session_t* s, uint64_t bytes) {

@@ -28,6 +28,16 @@ Session::~Session() {
 Session::Session(Session&&) noexcept = default;
 Session& Session::operator=(Session&&) noexcept = default;
 
+void Session::global_barrier(int phase) {
+  if (!barrier_) return;
+  const auto t0 = std::chrono::steady_clock::now();
+  const int rc = barrier_.fn(barrier_.ctx, phase);
+  barrier_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (rc != 0)
+    raise(Errc::QuiesceTimeout, "global checkpoint barrier failed at phase " + std::to_string(phase) +
+                                    " (hook returned " + std::to_string(rc) + ")");
+}
+
 DrainEngine& Session::drain_engine() {
   if (!drain_) drain_ = acquire_engine(ctx_->device());
   return *drain_;
@@ -58,6 +68,9 @@ void checkpoint_to_file(Session& session, PinnedImage& image, const std::filesys
   } else {
     write_file_parallel(path, image.bytes(), io);
   }
+  // every rank's file is durable (write_file_parallel ends with fdatasync)
+  session.global_barrier(kPhasePersisted);
+  if (drain) drain->barrier_ms = session.barrier_ms;
 }
 
 void read_image_into(const std::filesystem::path& path, PinnedImage& staging, FileIoStats* io) {

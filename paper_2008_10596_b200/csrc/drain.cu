@@ -849,11 +849,8 @@ void copy_window(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, ui
     const char* e = std::getenv("CRAC_COPY_CHUNK_MIB");
     return e ? uint64_t(std::max(1, std::atoi(e))) << 20 : DrainEngine::kCopyChunk;
   }();
-  thread_local std::vector<void*> dsts, srcs;
-  thread_local std::vector<size_t> sizes;
-  dsts.clear();
-  srcs.clear();
-  sizes.clear();
+  // one cudaMemcpyAsync per piece (host runs cut C3 windows into ~32 pieces)
+  const cudaMemcpyKind kind = d2h ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice;
   for (uint64_t a = off; a < end;) {
     while (run < R.size() && R[run].second <= a) ++run;
     uint64_t b = end;
@@ -869,30 +866,13 @@ void copy_window(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, ui
     const uint64_t bc = d2h ? b : std::min(end, b + 16);
     for (uint64_t c = a; c < bc; c += piece) {
       const uint64_t n = std::min(piece, bc - c);
-      dsts.push_back(d2h ? static_cast<void*>(stream + c) : static_cast<void*>(buf + (c - off)));
-      srcs.push_back(d2h ? static_cast<void*>(buf + (c - off)) : static_cast<void*>(stream + c));
-      sizes.push_back(n);
+      void* dst = d2h ? static_cast<void*>(stream + c) : static_cast<void*>(buf + (c - off));
+      const void* src = d2h ? static_cast<const void*>(buf + (c - off))
+                            : static_cast<const void*>(stream + c);
+      check_cuda(cudaMemcpyAsync(dst, src, n, kind, st), d2h ? "D2H" : "H2D");
     }
     a = b;
   }
-  static const int batch_env = [] {
-    const char* e = std::getenv("CRAC_COPY_BATCH");
-    return e ? std::atoi(e) : -1;
-  }();
-  if (sizes.size() > 1 && (batch_env == 1 || (batch_env < 0 && !R.empty()))) {
-    // one call for the window's pieces (host runs cut C3 windows into ~32)
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t attr_idx = 0, fail = 0;
-    if (cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &attr,
-                             &attr_idx, 1, &fail, st) == cudaSuccess)
-      return;
-    cudaGetLastError();  // batch API unavailable: issue the pieces one by one
-  }
-  for (size_t i = 0; i < sizes.size(); ++i)
-    check_cuda(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i],
-                               d2h ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st),
-               d2h ? "D2H" : "H2D");
 }
 
 // Host-resident managed pages of a drain.  Each host thread takes a block of
@@ -1323,23 +1303,46 @@ void drain_finish(Session& session, DrainStats* stats) {
 
 void precopy_wait(Session& session, double* phase1_ms);
 
+// The global-checkpoint hook (global_barrier.hpp) of a split drain whose
+// image completes in a later call: checkpoint_begin arms it, whichever call
+// completes the image (checkpoint_finish or any drain that finishes the
+// pending one first) runs the kPhaseImageComplete arrival, so every rank's
+// barrier sequence stays quiesced -> image-complete.
+void commit_pending(Session& session) {
+  if (!session.commit_armed) return;
+  session.commit_armed = false;
+  session.global_barrier(kPhaseImageComplete);
+}
+
 void finish_pending(Session& session) {
   if (session.drain_engine().pending.precopy) {
     precopy_wait(session, nullptr);
     return;
   }
   if (session.drain_engine().pending.active) drain_finish(session, nullptr);
+  commit_pending(session);
+}
+
+// A full drain; `global` runs the global-checkpoint hook around it (the
+// internal fallbacks of the incremental / pre-copy drains pass false when
+// their caller already owns the barrier sequence).
+void full_drain(Session& session, PinnedImage& out, DrainStats* stats, bool global) {
+  finish_pending(session);
+  if (global) session.barrier_ms = 0;
+  {
+    QuiesceScope q(session.table(), session.config().quiesce_timeout);
+    if (global) session.global_barrier(kPhaseQuiesced);
+    drain_locked(session, out, false, stats);
+  }
+  drain_finish(session, stats);
+  if (global) session.global_barrier(kPhaseImageComplete);
+  if (stats) stats->barrier_ms = session.barrier_ms;
 }
 
 }  // namespace
 
 void checkpoint_image(Session& session, PinnedImage& out, DrainStats* stats) {
-  finish_pending(session);
-  {
-    QuiesceScope q(session.table(), session.config().quiesce_timeout);
-    drain_locked(session, out, false, stats);
-  }
-  drain_finish(session, stats);
+  full_drain(session, out, stats, true);
 }
 
 void reserve_shadow(Session& session, uint64_t bytes, int device) {
@@ -1389,17 +1392,25 @@ void reserve_shadow(Session& session, uint64_t bytes, int device) {
 
 void checkpoint_begin(Session& session, PinnedImage& out, DrainStats* stats) {
   finish_pending(session);
+  session.barrier_ms = 0;
   QuiesceScope q(session.table(), session.config().quiesce_timeout);
+  session.global_barrier(kPhaseQuiesced);
   drain_locked(session, out, true, nullptr);
+  DrainEngine& E = session.drain_engine();
+  session.commit_armed = true;
   if (stats) {
     *stats = DrainStats{};
-    DrainEngine& E = session.drain_engine();
     stats->stall_ms = elapsed(E.ev_t0, E.ev_s1);
     stats->shadow_bytes = E.plan.stream_len - E.pending.head;
+    stats->barrier_ms = session.barrier_ms;
   }
 }
 
-void checkpoint_finish(Session& session, DrainStats* stats) { drain_finish(session, stats); }
+void checkpoint_finish(Session& session, DrainStats* stats) {
+  drain_finish(session, stats);
+  commit_pending(session);
+  if (stats) stats->barrier_ms = session.barrier_ms;
+}
 
 void hash_only(Session& session, DrainStats* stats) {
   finish_pending(session);
@@ -1432,6 +1443,9 @@ void hash_only(Session& session, DrainStats* stats) {
 Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catalog, TableMode mode,
                       std::chrono::milliseconds quiesce_timeout, DrainStats* stats) {
   if (stats) *stats = DrainStats{};
+  // the refill's time starts here: the host parse and the session set-up
+  // before the first device event count (host clock, added to total_ms)
+  const auto t_entry = std::chrono::steady_clock::now();
   PhaseTrace tr("refill");
   std::vector<uint8_t> storage;
   const std::span<const uint8_t> raw = unwrap(image, storage, nullptr);
@@ -1447,6 +1461,8 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   DeviceContext& ctx = session.device();
   DrainEngine& E = session.drain_engine();
   check_cuda(cudaEventRecord(E.ev_t0, E.s_pack), "event");
+  const double host_pre_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_entry).count();
   tr.mark("session");
 
   std::map<uint64_t, std::vector<KernelDescriptor>> binaries;
@@ -1509,13 +1525,26 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
 
   std::vector<uint64_t> live;
   live.reserve(p.facts.active.size());
+  // Every live Device extent is mapped before the replay, in coalesced runs,
+  // so the replay itself makes no driver calls.  The runs come from a bitmap
+  // of the 2 MiB blocks the extents touch, in address order (first fit hands
+  // out low addresses again after frees, so id order is not address order),
+  // without sorting the extents (C2: 16 k); one-block gaps are bridged.  The
+  // runs are mapped in pieces of at most kMapPiece in address order: the early
+  // data path maps, before it enqueues a window, the prefix of pieces that
+  // covers every destination the window writes, so a cold restart's physical
+  // allocation (cuMemCreate + map + access: ~1 ms per GiB) overlaps the H2D of
+  // the windows before it instead of preceding the first one.
+  constexpr uint64_t kMapPiece = 1ull << 30;
+  std::vector<std::pair<uint64_t, uint64_t>> map_pieces;  // arena offsets [lo, hi)
+  size_t mapped_pieces = 0;
+  auto map_upto = [&](uint64_t off_hi) {  // maps the pieces starting below off_hi
+    while (mapped_pieces < map_pieces.size() && map_pieces[mapped_pieces].first < off_hi) {
+      const auto& [lo, hi] = map_pieces[mapped_pieces++];
+      ctx.premap(kArenaBase + lo, hi - lo);
+    }
+  };
   {
-    // map every live Device extent up front in coalesced runs, so the replay
-    // itself makes no driver calls (and the early data path below has its
-    // destinations).  The runs come from a bitmap of the 2 MiB blocks the
-    // extents touch, in address order (first fit hands out low addresses
-    // again after frees, so id order is not address order), without
-    // sorting the extents (C2: 16 k); one-block gaps are bridged.
     constexpr uint64_t kBlock = 2ull << 20;
     std::vector<uint8_t> need((cfg.arena_bytes + kBlock - 1) / kBlock, 0);
     for (const AllocationRecord& r : p.facts.active) {
@@ -1541,10 +1570,13 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       uint64_t e = b + 1;
       while (e < nb && (need[e] || (e + 1 < nb && need[e + 1]))) ++e;
       const uint64_t hi = std::min(e * kBlock, cfg.arena_bytes);
-      ctx.premap(kArenaBase + b * kBlock, hi - b * kBlock);
+      for (uint64_t lo = b * kBlock; lo < hi; lo += kMapPiece)
+        map_pieces.emplace_back(lo, std::min(hi, lo + kMapPiece));
       b = e;
     }
   }
+  if (!early) map_upto(~0ull);
+  else map_upto(1);  // the first piece now, beside the plan thread
   tr.mark("premap");
 
   uint64_t windows = 0, verifies = 0, scattered = 0;
@@ -1558,7 +1590,8 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     windows = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
     if (stats) E.ensure_window_events(windows);
     check_cuda(cudaEventRecord(E.ev_c0, E.s_copy), "event");
-    size_t spans_done = 0, run_i = 0, krun_i = 0, drun_i = 0;
+    size_t spans_done = 0, run_i = 0, krun_i = 0, drun_i = 0, rec_i = 0;
+    uint64_t dst_hi = 0;  // highest arena offset written by the windows enqueued so far
     std::vector<std::pair<uint64_t, uint64_t>> kr;
     constexpr uint64_t kVerifyBatch = 32768;  // 2 GiB of 64 KiB chunks: big enough to keep
                                               // K1 efficient beside the H2D; the tail
@@ -1569,6 +1602,14 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       const uint64_t off = w * DrainEngine::kWindow;
       const uint64_t len = std::min(DrainEngine::kWindow, P.stream_len - off);
       const uint64_t with_ahead = std::min(len + 16, P.stream_len - off);
+      if (early) {  // destinations of this window mapped before anything targets them
+        while (rec_i < P.recs.size() && P.recs[rec_i].out_off < off + len) {
+          const crac_record_t& r = P.recs[rec_i++];
+          if (r.len && r.ptr >= kArenaBase)
+            dst_hi = std::max(dst_hi, r.ptr - kArenaBase + std::max(r.len, r.ext));
+        }
+        map_upto(dst_hi);
+      }
       if (w >= uint64_t(DrainEngine::kSlots))
         check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_free[slot], 0), "wait");
       copy_window(P, run_i, off, off + with_ahead, buf, const_cast<uint8_t*>(raw.data() + s3),
@@ -1631,6 +1672,8 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     if (plan_err) std::rethrow_exception(plan_err);
     tr.mark("plan");
     enqueue_data_path();
+    map_upto(~0ull);  // extents no window wrote (empty payloads)
+    tr.mark("premap-rest");
   }
   ctx.begin_replay(live);
   try {
@@ -1727,7 +1770,8 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   session.log().reset(std::move(p.log));
   session.app_state() = std::move(p.app_state);
   if (stats) {
-    stats->total_ms = elapsed(E.ev_t0, E.ev_t1);
+    stats->host_pre_ms = host_pre_ms;
+    stats->total_ms = host_pre_ms + elapsed(E.ev_t0, E.ev_t1);
     if (windows) {
       stats->copy_ms = elapsed(E.ev_c0, E.ev_c1);
       stats->pack_launches = windows;
@@ -1862,16 +1906,25 @@ void checkpoint_incremental(Session& session, PinnedImage& image, DrainStats* st
     return sig == P.log_sizes;
   };
   if (!layout_unchanged()) {
-    checkpoint_image(session, image, stats);
+    full_drain(session, image, stats, true);
     return;
   }
   bool raced = false;
+  session.barrier_ms = 0;
   {
     QuiesceScope q(session.table(), session.config().quiesce_timeout);
     raced = !layout_unchanged();  // re-check under the gate: the log cannot move now
-    if (!raced) incremental_locked(session, image, stats);
+    if (!raced) {
+      session.global_barrier(kPhaseQuiesced);
+      incremental_locked(session, image, stats);
+    }
   }
-  if (raced) checkpoint_image(session, image, stats);
+  if (raced) {
+    full_drain(session, image, stats, true);
+    return;
+  }
+  session.global_barrier(kPhaseImageComplete);
+  if (stats) stats->barrier_ms = session.barrier_ms;
 }
 
 }  // namespace cracsim
@@ -1973,7 +2026,7 @@ void checkpoint_precopy_begin(Session& session, PinnedImage& out, DrainStats* st
     }
   }  // the application runs from here on
   if (!eligible) {
-    checkpoint_image(session, out, stats);
+    full_drain(session, out, stats, true);
     return;
   }
   const bool aligned = std::all_of(P.pay_rec_off.begin(), P.pay_rec_off.end(),

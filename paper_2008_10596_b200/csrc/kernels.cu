@@ -40,6 +40,9 @@ constexpr uint32_t kTabWords = 2 * 256 * 64;  // 2 groups x 256 rows x 64 words 
 constexpr uint32_t kTabBytes = kTabWords * 4;
 constexpr uint32_t kGroupB = 256 * 64 * 4;    // byte offset of group B
 constexpr uint32_t kRowGap = 496;             // bytes between a lane's words
+// in-flight rows of the K1 variants that also compute the dirty-key lane: 16
+// (the CRC-only depth) spills the key's registers (ptxas -v), 8 does not
+constexpr int kKeyRows = 8;
 
 __device__ uint32_t g_tab[kTabWords];  // smem image of the lookup tables
 __device__ uint32_t g_t0[256];         // plain byte table
@@ -313,6 +316,53 @@ __device__ __forceinline__ uint32_t k1_rows(const LaneLut& lut, const uint8_t* p
   return acc;
 }
 
+// Two chunks of `rows` rows (rows % kRows == 0) hashed together by the same
+// lanes: two independent CRC chains (and key lanes) per lane, interleaved so
+// the lookups of one chain fill the latency of the other's.
+template <int kRows, typename Key>
+__device__ __forceinline__ void k1_rows2(const LaneLut& lut, const uint8_t* p0, const uint8_t* p1,
+                                         uint32_t rows, Key& k0, Key& k1, uint32_t& a0,
+                                         uint32_t& a1) {
+  uint32_t acc0 = 0, acc1 = 0, r = 0;
+  uint4 c0[kRows], c1[kRows];
+#pragma unroll
+  for (int k = 0; k < kRows; ++k) {
+    c0[k] = ldg_stream(p0 + k * 512);
+    c1[k] = ldg_stream(p1 + k * 512);
+  }
+  for (; r + 2 * kRows <= rows; r += kRows) {
+    uint4 n0[kRows], n1[kRows];
+#pragma unroll
+    for (int k = 0; k < kRows; ++k) {
+      n0[k] = ldg_stream(p0 + (r + kRows + k) * 512);
+      n1[k] = ldg_stream(p1 + (r + kRows + k) * 512);
+    }
+#pragma unroll
+    for (int k = 0; k < kRows; ++k) {
+      acc0 = word16<true>(lut, acc0, c0[k]);
+      acc1 = word16<true>(lut, acc1, c1[k]);
+      k0.add(r + k, c0[k]);
+      k1.add(r + k, c1[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kRows; ++k) {
+      c0[k] = n0[k];
+      c1[k] = n1[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kRows - 1; ++k) {
+    acc0 = word16<true>(lut, acc0, c0[k]);
+    acc1 = word16<true>(lut, acc1, c1[k]);
+    k0.add(r + k, c0[k]);
+    k1.add(r + k, c1[k]);
+  }
+  a0 = word16<false>(lut, acc0, c0[kRows - 1]);
+  a1 = word16<false>(lut, acc1, c1[kRows - 1]);
+  k0.add(r + kRows - 1, c0[kRows - 1]);
+  k1.add(r + kRows - 1, c1[kRows - 1]);
+}
+
 // ---------------------------------------------------------------------------
 // K1
 // ---------------------------------------------------------------------------
@@ -413,7 +463,7 @@ __device__ void drain_writer(const crac_span_t* __restrict__ spans,
 // 4 split incremental drain (hashers push dirty chunks, writer CTAs copy).
 // kKey: also the second dirty-key lane (Key2) into out_key[c] (and, in the
 // drain modes, compared with / stored to hd.prev_key).
-template <int kRows, int kMode, bool kKey>
+template <int kRows, int kMode, bool kKey, bool kPair = false>
 __global__ void __launch_bounds__(kK1Threads, 1)
     k1_chunk_crc(const crac_span_t* __restrict__ spans, const uint64_t* __restrict__ chunk_first,
                  uint32_t n_spans, uint32_t chunk_bytes, uint64_t c_lo, uint64_t c_hi,
@@ -446,6 +496,43 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     return;
   }
 
+  // Post-hash work of one chunk: lane columns -> the chunk's zlib CRC (and
+  // key), then the mode's output (CRC store / dirty compare + drain).
+  auto finish = [&](uint64_t c, uint32_t s, uint32_t L, uint32_t K, uint32_t len,
+                    const uint8_t* base, uint64_t off) {
+    if (kMode == 0) {
+      if (lane == 0) {
+        out[c] = L;
+        if constexpr (kKey) out_key[c] = K;
+      }
+      return;
+    }
+    const uint32_t crc = __shfl_sync(0xFFFFFFFFu, L, 0);
+    if (lane == 0) out[c] = crc;
+    bool changed = crc != hd.prev[c];
+    if constexpr (kKey) {  // the 64-bit dirty key (CRC, key), when the caller keeps keys
+      if (hd.prev_key) {
+        if (lane == 0) out_key[c] = K;
+        changed |= K != hd.prev_key[c];
+      }
+    }
+    if (changed) {  // warp-uniform
+      if (lane == 0) {
+        hd.prev[c] = crc;
+        if constexpr (kKey)
+          if (hd.prev_key) hd.prev_key[c] = K;
+        atomicAdd(&hd.counters[0], 1ull);
+        atomicAdd(&hd.counters[1], (unsigned long long)len);
+        if (kMode == 4) {  // hand the chunk to the writers and keep hashing
+          const unsigned long long slot = atomicAdd(&hd.qctl[0], 1ull);
+          *reinterpret_cast<volatile unsigned long long*>(&hd.queue[slot]) = c + 1;
+          __threadfence();
+        }
+      }
+      if (kMode != 4) chunk_to_host(hd.host + hd.dst_off[s] + off, base, len, lane);
+    }
+  };
+
   uint32_t s = find_span(chunk_first, n_spans, c_begin);
   uint64_t s_next = __ldg(chunk_first + s + 1);
   for (uint64_t c = c_begin; c < c_end; ++c) {
@@ -459,6 +546,46 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     const uint32_t len = rem_len < chunk_bytes ? uint32_t(rem_len) : chunk_bytes;
     const uint8_t* base = reinterpret_cast<const uint8_t*>(sp.ptr + off);
     const uint32_t rows = len >> 9;
+
+    if constexpr (kPair) {
+      // two whole chunks at once: two independent CRC chains per lane (the
+      // chain is a serial PRMT -> LDS -> XOR dependency; ncu shows the warps
+      // stalled on the lookups' latency, not on a pipe)
+      if (len == chunk_bytes && rows % kRows == 0 && c + 1 < c_end) {
+        uint32_t s1 = s;
+        uint64_t s1_next = s_next;
+        while (c + 1 >= s1_next) {
+          ++s1;
+          s1_next = __ldg(chunk_first + s1 + 1);
+        }
+        const crac_span_t sp1 = spans[s1];
+        const uint64_t off1 = (c + 1 - __ldg(chunk_first + s1)) * chunk_bytes;
+        if (sp1.len - off1 >= chunk_bytes) {
+          const uint8_t* base1 = reinterpret_cast<const uint8_t*>(sp1.ptr + off1);
+          std::conditional_t<kKey, Key2, NoKey> key0, key1;
+          if constexpr (kKey) key0.kl = key1.kl = (lane + 1) * 0x27D4EB2Fu;
+          uint32_t a0, a1;
+          k1_rows2<kRows>(lut, base + lane * 16, base1 + lane * 16, rows, key0, key1, a0, a1);
+          uint32_t L0 = warp_xor(crac::gf_mul(g_xp16[31 - lane], a0));
+          uint32_t L1 = warp_xor(crac::gf_mul(g_xp16[31 - lane], a1));
+          if (lane == 0) {
+            L0 ^= k_full;
+            L1 ^= k_full;
+          }
+          uint32_t K0 = 0, K1 = 0;
+          if constexpr (kKey) {
+            K0 = key_final(warp_sum64(key0.sum), len);
+            K1 = key_final(warp_sum64(key1.sum), len);
+          }
+          finish(c, s, L0, K0, len, base, off);
+          finish(c + 1, s1, L1, K1, len, base1, off1);
+          ++c;
+          s = s1;
+          s_next = s1_next;
+          continue;
+        }
+      }
+    }
 
     // ---- main body: rows of 512 B, kRows-deep double-buffered loads ----
     uint32_t acc;
@@ -507,13 +634,6 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     if (lane == 0) L ^= (len == chunk_bytes ? k_full : crac::crc_affine(len, g_pow2));
     uint32_t K = 0;
     if constexpr (kKey) K = key_final(warp_sum64(key.sum), len);
-    if (kMode == 0) {
-      if (lane == 0) {
-        out[c] = L;
-        if constexpr (kKey) out_key[c] = K;
-      }
-      continue;
-    }
     if ((kMode == 2 || kMode == 3)) {
       if (lane == 0) {
         out[c] = L;
@@ -532,30 +652,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       chunk_to_host(dst + rows * 512, base + rows * 512, len - rows * 512, lane);
       continue;
     }
-    const uint32_t crc = __shfl_sync(0xFFFFFFFFu, L, 0);
-    if (lane == 0) out[c] = crc;
-    bool changed = crc != hd.prev[c];
-    if constexpr (kKey) {  // the 64-bit dirty key (CRC, key), when the caller keeps keys
-      if (hd.prev_key) {
-        if (lane == 0) out_key[c] = K;
-        changed |= K != hd.prev_key[c];
-      }
-    }
-    if (changed) {  // warp-uniform
-      if (lane == 0) {
-        hd.prev[c] = crc;
-        if constexpr (kKey)
-          if (hd.prev_key) hd.prev_key[c] = K;
-        atomicAdd(&hd.counters[0], 1ull);
-        atomicAdd(&hd.counters[1], (unsigned long long)len);
-        if (kMode == 4) {  // hand the chunk to the writers and keep hashing
-          const unsigned long long slot = atomicAdd(&hd.qctl[0], 1ull);
-          *reinterpret_cast<volatile unsigned long long*>(&hd.queue[slot]) = c + 1;
-          __threadfence();
-        }
-      }
-      if (kMode != 4) chunk_to_host(hd.host + hd.dst_off[s] + off, base, len, lane);
-    }
+    finish(c, s, L, K, len, base, off);
   }
   if (kMode == 4 && lane == 0) {
     __threadfence();
@@ -1158,6 +1255,26 @@ __global__ void k_fill_synth(uint8_t* __restrict__ dst, uint64_t len, uint64_t s
   }
 }
 
+// Restart check against regenerated content (bench "verified", tests): sets
+// *flag = 1 if any byte of the allocation differs from synth_word.
+__global__ void k_verify_synth(const uint8_t* __restrict__ src, uint64_t len, uint64_t seed,
+                               uint64_t id, uint32_t* __restrict__ flag) {
+  const uint64_t pairs = len / 16;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint32_t diff = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < pairs;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint4 v = ldg_stream(s4 + i);
+    const uint64_t w0 = synth_word(seed, id, 2 * i), w1 = synth_word(seed, id, 2 * i + 1);
+    diff |= (v.x ^ uint32_t(w0)) | (v.y ^ uint32_t(w0 >> 32)) | (v.z ^ uint32_t(w1)) |
+            (v.w ^ uint32_t(w1 >> 32));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (uint64_t b = pairs * 16; b < len; ++b)
+      diff |= src[b] ^ uint8_t(synth_word(seed, id, b / 8) >> (8 * (b % 8)));
+  if (__syncthreads_or(diff != 0) && threadIdx.x == 0) *flag = 1u;
+}
+
 __global__ void k_mutate(const crac_span_t* __restrict__ spans, const uint64_t* __restrict__ ids,
                          const uint64_t* __restrict__ chunk_first, uint32_t n_spans,
                          uint32_t chunk_bytes, uint64_t total_chunks, uint64_t seed,
@@ -1222,8 +1339,12 @@ int crac_gpu_init(void) {
     if (!e) e = cudaMemcpyToSymbol(g_pow2, h.pow2.data(), 64 * 4);
     for (auto k : {k1_chunk_crc<4, 0, false>, k1_chunk_crc<8, 0, false>, k1_chunk_crc<16, 0, false>,
                    k1_chunk_crc<4, 0, true>, k1_chunk_crc<8, 0, true>, k1_chunk_crc<16, 0, true>,
-                   k1_chunk_crc<16, 1, true>, k1_chunk_crc<16, 2, false>, k1_chunk_crc<8, 3, false>,
-                   k1_chunk_crc<16, 2, true>, k1_chunk_crc<8, 3, true>, k1_chunk_crc<16, 4, true>})
+                   k1_chunk_crc<12, 0, true>, k1_chunk_crc<kKeyRows, 1, true>,
+                   k1_chunk_crc<16, 2, false>, k1_chunk_crc<8, 3, false>,
+                   k1_chunk_crc<kKeyRows, 2, true>, k1_chunk_crc<8, 3, true>,
+                   k1_chunk_crc<kKeyRows, 4, true>, k1_chunk_crc<4, 0, true, true>,
+                   k1_chunk_crc<8, 0, true, true>, k1_chunk_crc<4, 0, false, true>,
+                   k1_chunk_crc<8, 0, false, true>})
       if (!e) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTabBytes));
     if (!e) e = cudaFuncSetAttribute(k1_chunk_crc_tma<16, 3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(k1_tma_smem<16, 3, 4>()));
@@ -1286,11 +1407,27 @@ int crac_chunk_key_range(const crac_span_t* d_spans, const uint64_t* d_chunk_fir
           d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, kf);
     return int(cudaGetLastError());
   }
-  const int rows = forced ? forced : (chunk_bytes >= 32 * 512 ? 16 : chunk_bytes >= 8 * 512 ? 8 : 4);
+  // with the key lane, the key's registers beside 2 x 16 in-flight rows
+  // spill (ptxas: 136 B at 16 rows); CRAC_K1_KEY_ROWS picks the depth then
+  static const int forced_key = [] {
+    const char* e = std::getenv("CRAC_K1_KEY_ROWS");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int rows_nokey = forced ? forced : (chunk_bytes >= 32 * 512 ? 16 : chunk_bytes >= 8 * 512 ? 8 : 4);
+  const int rows = d_key ? (forced_key ? forced_key : kKeyRows) : rows_nokey;
+  // paired chunks (two CRC chains per lane): CRAC_K1_PAIR=<rows per chain>
+  static const int pair = [] {
+    const char* e = std::getenv("CRAC_K1_PAIR");
+    return e ? std::atoi(e) : 0;
+  }();
   auto kern = d_key ? (rows == 4 ? k1_chunk_crc<4, 0, true>
-                       : rows == 16 ? k1_chunk_crc<16, 0, true> : k1_chunk_crc<8, 0, true>)
+                       : rows == 16 ? k1_chunk_crc<16, 0, true>
+                       : rows == 12 ? k1_chunk_crc<12, 0, true> : k1_chunk_crc<8, 0, true>)
                     : (rows == 4 ? k1_chunk_crc<4, 0, false>
                        : rows == 16 ? k1_chunk_crc<16, 0, false> : k1_chunk_crc<8, 0, false>);
+  if (pair && chunk_bytes >= 8 * 512)
+    kern = d_key ? (pair == 4 ? k1_chunk_crc<4, 0, true, true> : k1_chunk_crc<8, 0, true, true>)
+                 : (pair == 4 ? k1_chunk_crc<4, 0, false, true> : k1_chunk_crc<8, 0, false, true>);
   kern<<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
       d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, d_key,
       k_full_for(chunk_bytes), HashDrain{});
@@ -1308,7 +1445,7 @@ int crac_hash_drain_range(const crac_span_t* d_spans, const uint64_t* d_chunk_fi
   uint64_t blocks = (c_hi - c_lo + kK1Warps - 1) / kK1Warps;
   if (blocks > uint64_t(sm_count())) blocks = sm_count();
   if (!d_crc_prev || !d_counters || (!d_key) != (!d_key_prev)) return int(cudaErrorInvalidValue);
-  k1_chunk_crc<16, 1, true><<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
+  k1_chunk_crc<kKeyRows, 1, true><<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
       d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, d_key,
       k_full_for(chunk_bytes),
       HashDrain{d_crc_prev, d_key_prev, d_dst_off, host_image, d_counters, nullptr, nullptr, 0});
@@ -1335,7 +1472,7 @@ int crac_hash_drain_split(const crac_span_t* d_spans, const uint64_t* d_chunk_fi
   cudaStream_t st = cudaStream_t(stream);
   const uint64_t q = c_hi - c_lo + uint64_t(n_writers) * kK1Warps + 1;
   if (cudaError_t e = cudaMemsetAsync(d_queue, 0, q * 8, st); e != cudaSuccess) return int(e);
-  k1_chunk_crc<16, 4, true><<<unsigned(hashers + n_writers), kK1Threads, kTabBytes, st>>>(
+  k1_chunk_crc<kKeyRows, 4, true><<<unsigned(hashers + n_writers), kK1Threads, kTabBytes, st>>>(
       d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, d_key,
       k_full_for(chunk_bytes),
       HashDrain{d_crc_prev, d_key_prev, d_dst_off, host_image, d_counters, d_queue, d_counters + 2,
@@ -1352,7 +1489,7 @@ int crac_hash_copy_range(const crac_span_t* d_spans, const uint64_t* d_chunk_fir
   if (int rc = crac_gpu_init()) return rc;
   uint64_t blocks = (c_hi - c_lo + kK1Warps - 1) / kK1Warps;
   if (blocks > uint64_t(sm_count())) blocks = sm_count();
-  auto kern = d_key ? (dst_aligned ? k1_chunk_crc<16, 2, true> : k1_chunk_crc<8, 3, true>)
+  auto kern = d_key ? (dst_aligned ? k1_chunk_crc<kKeyRows, 2, true> : k1_chunk_crc<8, 3, true>)
                     : (dst_aligned ? k1_chunk_crc<16, 2, false> : k1_chunk_crc<8, 3, false>);
   kern<<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
       d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, d_key,
@@ -1471,6 +1608,15 @@ int crac_gather_chunks_to_host_dev(const crac_span_t* d_spans, const uint64_t* d
   k_gather_to_host<<<unsigned(blocks), kGatherThreads, 0, cudaStream_t(stream)>>>(
       d_spans, d_chunk_first, n_spans, chunk_bytes, d_dirty_idx, 0, max_count, d_count, d_dst_off,
       host_image);
+  return int(cudaGetLastError());
+}
+
+int crac_verify_synth(const uint8_t* d_src, uint64_t len, uint64_t seed, uint64_t id,
+                      uint32_t* d_flag, void* stream) {
+  if (len == 0) return 0;
+  const uint64_t pairs = std::max<uint64_t>(1, len / 16);
+  const uint64_t blocks = std::min<uint64_t>((pairs + 255) / 256, uint64_t(sm_count()) * 8);
+  k_verify_synth<<<unsigned(blocks), 256, 0, cudaStream_t(stream)>>>(d_src, len, seed, id, d_flag);
   return int(cudaGetLastError());
 }
 

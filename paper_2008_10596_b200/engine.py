@@ -41,7 +41,8 @@ class Stats(C.Structure):
                 ("image_bytes", C.c_uint64), ("dirty_chunks", C.c_uint64),
                 ("total_chunks", C.c_uint64), ("incremental", C.c_int32),
                 ("reserved", C.c_int32), ("stall_ms", C.c_double),
-                ("shadow_bytes", C.c_uint64)]
+                ("shadow_bytes", C.c_uint64), ("barrier_ms", C.c_double),
+                ("host_pre_ms", C.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
@@ -55,6 +56,20 @@ class IoStats(C.Structure):
         d = {k: getattr(self, k) for k, _ in self._fields_}
         d["direct"] = bool(d["direct"])
         d["GBps"] = self.bytes / (self.ms * 1e6) if self.ms > 0 else 0.0
+        return d
+
+
+class VerifyReport(C.Structure):
+    _fields_ = [("sections_checked", C.c_uint64), ("crc_bytes", C.c_uint64),
+                ("payloads_compared", C.c_uint64), ("payload_bytes_compared", C.c_uint64),
+                ("mismatched_payloads", C.c_uint64), ("first_bad_id", C.c_uint64),
+                ("bad_sections", C.c_uint32), ("threads", C.c_uint32), ("ms", C.c_double)]
+
+    def as_dict(self) -> dict:
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["ok"] = self.bad_sections == 0 and self.mismatched_payloads == 0
+        if d["first_bad_id"] == 2**64 - 1:
+            d["first_bad_id"] = None
         return d
 
 
@@ -99,6 +114,14 @@ _SIGS = {
     "crac_checkpoint_precopy_finish": (C.c_int, [_P, C.POINTER(Stats)]),
     "crac_reserve_shadow_on": (C.c_int, [_P, _U64, C.c_int]),
     "crac_crc32_host": (C.c_uint32, [_P, _U64, _U32]),
+    "crac_session_set_barrier": (C.c_int, [_P, _P, _P]),
+    "crac_image_verify": (C.c_int, [_P, _U64, _U32, _U64, C.c_int, C.POINTER(VerifyReport)]),
+    "crac_session_verify_synthetic": (C.c_int, [_P, _U64, _PU64, _PU64]),
+    "crac_barrier_open": (C.c_int, [C.c_char_p, _U32, _U32, _U32, C.POINTER(_P)]),
+    "crac_barrier_wait": (C.c_int, [_P]),
+    "crac_barrier_hook": (C.c_int, [_P, C.c_int]),
+    "crac_barrier_generation": (_U64, [_P]),
+    "crac_barrier_close": (None, [_P, C.c_int]),
     "crac_peek_cuda_error": (C.c_int, []),
     "crac_drop_arena_cache": (C.c_int, [C.c_int]),
     "crac_stream_handle": (C.c_int, [_P, _U64, C.POINTER(_P)]),
@@ -148,6 +171,7 @@ _SIGS = {
     "crac_diff_compact": (C.c_int, [_P, _P, _U64, _P, _P, _P, _P]),
     "crac_gather_chunks": (C.c_int, [_P, _P, _U32, _U32, _P, _U64, _U64, _P, _P]),
     "crac_fill_synth": (C.c_int, [_P, _U64, _U64, _U64, _U64, _P]),
+    "crac_verify_synth": (C.c_int, [_P, _U64, _U64, _U64, _P, _P]),
     "crac_mutate_chunks": (C.c_int, [_P, _P, _P, _U32, _U32, _U64, _U64, _U64, _U64, _P]),
 }
 
@@ -223,6 +247,39 @@ class Image:
     def close(self):
         if getattr(self, "_h", None):
             lib().crac_image_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# CRAC_PHASE_* (crac_engine.h): when a session's global-checkpoint hook runs
+PHASE_QUIESCED, PHASE_IMAGE_COMPLETE, PHASE_PERSISTED = 0, 1, 2
+BARRIER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int)
+
+
+class Barrier:
+    """The node-local global-checkpoint barrier (crac_barrier_open): every rank
+    of the job opens the same name with the same world size."""
+
+    def __init__(self, name: str, world: int, rank: int, timeout_ms: int = 60000):
+        h = C.c_void_p()
+        _check(lib().crac_barrier_open(name.encode(), world, rank, timeout_ms, C.byref(h)))
+        self._h = h
+        self.name, self.world, self.rank = name, world, rank
+
+    def wait(self) -> None:
+        _check(lib().crac_barrier_wait(self._h))
+
+    def generation(self) -> int:
+        return lib().crac_barrier_generation(self._h)
+
+    def close(self, unlink: bool = False) -> None:
+        if getattr(self, "_h", None):
+            lib().crac_barrier_close(self._h, int(unlink))
             self._h = None
 
     def __del__(self):
@@ -317,6 +374,21 @@ class Session:
     def set_app_state(self, data) -> None:
         p, n, keep = _buf(data)
         _check(lib().crac_set_app_state(self._h, p, n))
+
+    # ---- global checkpoint ----
+    def set_barrier(self, barrier: Optional[Barrier]) -> None:
+        """Installs the node-local shared-memory barrier as this session's
+        global-checkpoint hook (None removes it)."""
+        fn = C.cast(lib().crac_barrier_hook, C.c_void_p) if barrier else None
+        _check(lib().crac_session_set_barrier(self._h, fn, barrier._h if barrier else None))
+        self._barrier_keep = barrier
+
+    def set_barrier_hook(self, hook) -> None:
+        """Installs a Python callable hook(phase) -> int as the global-checkpoint
+        hook (an MPI/gloo barrier, or a test probe); None removes it."""
+        cb = BARRIER_FN(lambda _ctx, phase: int(hook(phase) or 0)) if hook else None
+        _check(lib().crac_session_set_barrier(self._h, C.cast(cb, C.c_void_p) if cb else None, None))
+        self._barrier_keep = cb
 
     # ---- engine ----
     def checkpoint(self, image: Optional[Image] = None) -> tuple[bytes, dict]:
@@ -433,6 +505,13 @@ class Session:
         _check(lib().crac_mutate_device(self._h, seed, epoch, threshold, C.byref(n)))
         return n.value
 
+    def verify_synthetic(self, seed: int) -> dict:
+        """Every live Device allocation compared on the GPU with the synthetic
+        content fill_synthetic(id, seed) wrote."""
+        bad, nb = C.c_uint64(), C.c_uint64()
+        _check(lib().crac_session_verify_synthetic(self._h, seed, C.byref(bad), C.byref(nb)))
+        return {"bad_allocations": bad.value, "bytes_checked": nb.value}
+
     def hash_only(self) -> dict:
         st = Stats()
         _check(lib().crac_hash_session(self._h, C.byref(st)))
@@ -454,6 +533,21 @@ class Session:
             self.close()
         except Exception:
             pass
+
+
+def verify_image(image=None, synth_seed: Optional[int] = None, threads: int = 0,
+                 address: Optional[tuple[int, int]] = None) -> dict:
+    """crac_image_verify: host-only check of an image (section CRCs recomputed
+    on `threads` cores; with synth_seed, Device payloads against regenerated
+    synthetic content).  `address` = (ptr, size) checks an image in place."""
+    if address is not None:
+        p, n, keep = C.c_void_p(address[0]), address[1], None
+    else:
+        p, n, keep = _buf(image)
+    rep = VerifyReport()
+    _check(lib().crac_image_verify(p, n, threads, synth_seed or 0, int(synth_seed is not None),
+                                   C.byref(rep)))
+    return rep.as_dict()
 
 
 def restart(image, mode: int = DIRECT) -> tuple[Session, dict]:

@@ -16,7 +16,7 @@ ROOT = Path(__file__).resolve().parent.parent
 
 def declared(header: str) -> set[str]:
     text = (ROOT / "include" / header).read_text()
-    return set(re.findall(r"^\s*(?:int|void|uint32_t|const char\*)\s+(crac_\w+)\s*\(", text, re.M))
+    return set(re.findall(r"^\s*(?:int|void|uint32_t|uint64_t|const char\*)\s+(crac_\w+)\s*\(", text, re.M))
 
 
 @pytest.fixture(scope="module")

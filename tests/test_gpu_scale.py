@@ -113,3 +113,32 @@ def test_restart_refuses_wrapping_sizes(eng, kind, size, pay, uvm):
     with pytest.raises(eng.CracError) as e:
         eng.restart(img)
     assert e.value.errc == "ImageCorrupt"
+
+
+def test_restart_checked_against_regenerated_content(eng):
+    """The bench's independent checks (crac_image_verify on the host image,
+    verify_synthetic on the restarted device state) agree with a clean round
+    trip, and catch a payload change whose section CRC was re-stamped (the
+    image is self-consistent, so the refill's K1 verify accepts it)."""
+    n, size = 24, 4 * MIB + 48
+    s = eng.Session(seed=1, arena_bytes=n * (size + 256) // MIB * MIB + 2 * MIB)
+    workloads.build_regions(s, n, lambda r: size, seed=1)
+    img, _ = s.checkpoint()
+    s.close()
+    eng.drop_arena_cache()  # cold: the restart maps fresh physical memory
+    rep = eng.verify_image(img, synth_seed=1)
+    assert rep["ok"] and rep["payloads_compared"] == n
+    rs, _ = eng.restart(img)
+    v = rs.verify_synthetic(1)
+    assert v == {"bad_allocations": 0, "bytes_checked": n * size}
+    rs.close()
+    bad = bytearray(img)
+    off3, n3, _ = _sections(img)[2]
+    bad[off3 + 16 + (n // 2) * (16 + size) + 12345] ^= 0x10
+    struct.pack_into("<I", bad, off3 + n3, zlib.crc32(memoryview(bad)[off3:off3 + n3]))
+    rep = eng.verify_image(bytes(bad), synth_seed=1)
+    assert rep["bad_sections"] == 0 and rep["mismatched_payloads"] == 1
+    eng.drop_arena_cache()
+    rs, _ = eng.restart(bytes(bad))
+    assert rs.verify_synthetic(1)["bad_allocations"] == 1
+    rs.close()

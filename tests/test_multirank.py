@@ -56,3 +56,26 @@ def test_reference_arm_nonzero_ranks_exit_without_work(capsys):
 
     bench.run_reference(A, world=2, rank=1)
     assert capsys.readouterr().out == ""
+
+
+def test_bench_gpus_2_spawns_two_ranks_on_distinct_devices():
+    """`bench.py --gpus 2` outside torchrun launches the two ranks itself,
+    each pinned to its own device, joined by gloo and by the product's
+    shared-memory checkpoint barrier (dry run: no GPU work)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "MASTER_PORT",
+                        "CUDA_VISIBLE_DEVICES")}
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--dry-run"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert sorted(d["rank"] for d in lines) == [0, 1]
+    assert all(d["world"] == 2 and d["dry_run"] for d in lines)
+    devs = {d["rank"]: d["cuda_visible_devices"] for d in lines}
+    assert devs == {0: "0", 1: "1"}
+    assert all(d["barrier_generation"] == 1 for d in lines)
