@@ -474,8 +474,12 @@ def ncu_traffic(kernel):
     ratio instead (DRAM bytes per algorithmic byte) for the caller to scale."""
     if not kernel:
         return None, None
-    # the kernel variant each bench key times (ncu names template instances)
-    exact = {"k1_chunk_crc": "void k1_chunk_crc<16, 0>"}.get(kernel.split(" ")[0])
+    # the kernel variant each bench key times (ncu names template instances):
+    # round 2 names first (paired chains: the drain's K1 with the key lane, the
+    # refill verify CRC only), then round 1's
+    exact = {"k1_chunk_crc": ("void k1_chunk_crc<4, 0, true, true>", "void k1_chunk_crc<16, 0>"),
+             "k1_chunk_crc (refill verify)": ("void k1_chunk_crc<8, 0, false, true>",
+                                              "void k1_chunk_crc<16, 0>")}.get(kernel)
     name = kernel.split(" ")[0]
     units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     for path in sorted(Path(__file__).parent.glob("profiles/*/ncu_full.json"), reverse=True):
@@ -487,7 +491,7 @@ def ncu_traffic(kernel):
         if (path.parent / "ncu_meta.json").exists():
             meta = json.loads((path.parent / "ncu_meta.json").read_text())
         for key, m in full.items():
-            if (exact and key != exact) or name not in key:
+            if (exact and key not in exact) or name not in key:
                 continue
             total = 0.0
             for metric in ("dram__bytes_read.sum", "dram__bytes_write.sum"):

@@ -55,6 +55,10 @@ class Session {
   std::vector<uint8_t>& app_state() { return app_state_; }
   const SessionConfig& config() const { return cfg_; }
   DrainEngine& drain_engine();
+  // true once drain_engine() has been acquired (its acquisition allocates
+  // device and pinned memory, which must not happen before a quiesce: a
+  // pinned allocation waits for a kernel stuck on the device)
+  bool has_drain_engine() const { return drain_ != nullptr; }
   // Global-checkpoint hook (global_barrier.hpp); called by every checkpoint
   // entry point at kPhaseQuiesced and kPhaseImageComplete.
   void set_barrier(GlobalBarrier b) { barrier_ = b; }

@@ -33,6 +33,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <optional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -731,8 +732,43 @@ void plan_host_runs(ImagePlan& P, uint64_t limit) {
     for (size_t k = i; k < j; ++k) P.host_pages[k].own_frame = skip;
     i = j;
   }
+  // pinned-host payloads: content moved by host threads (pinned_runs), the
+  // frame stays in the window stream
+  P.pinned_runs.clear();
+  for (size_t k = 0; k < P.pay_spans.size(); ++k) {
+    if (P.pay_kind[k] != uint8_t(AllocationKind::PinnedHost)) continue;
+    const uint64_t lo = P.pay_rec_off[k], hi = lo + P.pay_spans[k].len;
+    if (hi - lo < kSkipMin || hi > limit) continue;
+    P.pinned_runs.push_back(ImagePlan::PinnedRun{lo, hi, P.pay_spans[k].ptr});
+    P.recs[k].ptr = 0;  // pack emits zeros / scatter skips: host-filled content
+  }
+  if (!P.pinned_runs.empty()) {
+    std::vector<std::pair<uint64_t, uint64_t>> runs;
+    runs.reserve(P.pinned_runs.size() + P.host_runs.size());
+    for (const auto& r : P.pinned_runs) runs.emplace_back(r.lo, r.hi);
+    runs.insert(runs.end(), P.host_runs.begin(), P.host_runs.end());  // UVM part: after
+    P.host_runs = std::move(runs);
+  }
   P.direct_runs.clear();
   P.skip_runs = P.host_runs;
+}
+
+// Host threads move the pinned-host payload contents: allocation -> image
+// (drain) or image -> allocation (refill), in 4 MiB pieces.
+void copy_pinned_runs(const ImagePlan& P, uint8_t* stream, bool drain) {
+  if (P.pinned_runs.empty()) return;
+  constexpr uint64_t kPiece = 4ull << 20;
+  std::vector<std::pair<size_t, uint64_t>> pieces;  // (run, offset in run)
+  for (size_t r = 0; r < P.pinned_runs.size(); ++r)
+    for (uint64_t o = 0; o < P.pinned_runs[r].hi - P.pinned_runs[r].lo; o += kPiece)
+      pieces.emplace_back(r, o);
+  parallel_for(pieces.size(), [&](uint64_t i) {
+    const auto& run = P.pinned_runs[pieces[i].first];
+    const uint64_t o = pieces[i].second, n = std::min(kPiece, run.hi - run.lo - o);
+    uint8_t* host = reinterpret_cast<uint8_t*>(run.host) + o;
+    if (drain) std::memcpy(stream + run.lo + o, host, n);
+    else std::memcpy(host, stream + run.lo + o, n);
+  }, /*min_parallel=*/2);
 }
 
 // Direct runs: the interior of every Device payload of at least
@@ -746,7 +782,7 @@ void plan_host_runs(ImagePlan& P, uint64_t limit) {
 constexpr uint64_t kTile = CRAC_TILE_BYTES;
 constexpr uint64_t kDirectMinTiles = 4;
 
-void plan_direct_runs(ImagePlan& P, uint64_t limit, bool drain) {
+void plan_direct_runs(ImagePlan& P, uint64_t limit, bool drain, uint64_t from = 0) {
   P.direct_runs.clear();
   // CRAC_DIRECT = 0 | drain | refill (default) | both.  Measured on C4
   // (tools/ab_direct2.sh, 3 rounds): the refill gains with direct H2D (55.0
@@ -765,7 +801,8 @@ void plan_direct_runs(ImagePlan& P, uint64_t limit, bool drain) {
       if (P.pay_kind[k] != uint8_t(AllocationKind::Device)) continue;
       const uint64_t a = P.pay_rec_off[k], b = std::min(a + P.pay_spans[k].len, limit);
       if (b < a + 64 + (kDirectMinTiles + 2) * kTile) continue;
-      const uint64_t lo = (a + 64 + kTile - 1) / kTile * kTile, hi = (b - 64) / kTile * kTile;
+      const uint64_t lo = std::max(from, (a + 64 + kTile - 1) / kTile * kTile),
+                     hi = (b - 64) / kTile * kTile;
       if (hi < lo + kDirectMinTiles * kTile) continue;
       P.direct_runs.push_back(ImagePlan::DirectRun{lo, hi, P.pay_spans[k].ptr + (lo - a)});
     }
@@ -1126,9 +1163,10 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   std::atomic<int64_t> recorded{-1};
   std::exception_ptr host_err;
   std::thread host_pass;
-  if (!P.host_pages.empty())
+  if (!P.host_pages.empty() || !P.pinned_runs.empty())
     host_pass = std::thread([&] {
       try {
+        copy_pinned_runs(P, img + s3, true);  // before the app resumes (join below)
         host_pages_drain(E, P, img + s3, head, recorded);
       } catch (...) {
         host_err = std::current_exception();
@@ -1315,6 +1353,7 @@ void commit_pending(Session& session) {
 }
 
 void finish_pending(Session& session) {
+  if (!session.has_drain_engine()) return;  // nothing pending; acquired under the gate
   if (session.drain_engine().pending.precopy) {
     precopy_wait(session, nullptr);
     return;
@@ -1440,6 +1479,42 @@ void hash_only(Session& session, DrainStats* stats) {
 // ---------------------------------------------------------------------------
 // refill
 // ---------------------------------------------------------------------------
+namespace {
+
+// META and the bulk stream's place, read from the first section headers
+// without any validation beyond bounds (the early start of restart_image).
+struct StreamPeek {
+  bool ok = false;
+  uint64_t seed = 0, arena_bytes = 0, s3 = 0, stream_len = 0;
+};
+
+StreamPeek peek_stream(std::span<const uint8_t> raw) {
+  StreamPeek k;
+  auto u64 = [&](uint64_t at, uint64_t& v) {
+    if (at > raw.size() || raw.size() - at < 8) return false;
+    std::memcpy(&v, raw.data() + at, 8);
+    return true;
+  };
+  uint64_t len1 = 0, len2 = 0, len3 = 0, len4 = 0;
+  if (raw.size() < 16 || std::memcmp(raw.data(), kImageMagic, 8) != 0) return k;
+  if (!u64(24, len1) || len1 != 24 || !u64(32, k.seed) || !u64(40, k.arena_bytes)) return k;
+  uint32_t crc1 = 0;  // META is used before the parse: only with its CRC intact
+  if (raw.size() < 60) return k;
+  std::memcpy(&crc1, raw.data() + 56, 4);
+  if (crc32_host(raw.data() + 32, 24) != crc1) return k;
+  const uint64_t h2 = 16 + 20 + len1;
+  if (!u64(h2 + 8, len2) || len2 > raw.size()) return k;
+  k.s3 = h2 + 20 + len2 + 16;
+  if (!u64(k.s3 - 8, len3) || len3 > raw.size() || k.s3 + len3 + 20 > raw.size()) return k;
+  if (!u64(k.s3 + len3 + 4 + 8, len4) || len4 > raw.size() - (k.s3 + len3 + 20)) return k;
+  k.stream_len = len3 + 20 + len4;
+  // a session must be constructible from META (DeviceContext's own checks)
+  k.ok = k.arena_bytes > 0 && k.arena_bytes % kAlign == 0 && k.stream_len > 20;
+  return k;
+}
+
+}  // namespace
+
 Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catalog, TableMode mode,
                       std::chrono::milliseconds quiesce_timeout, DrainStats* stats) {
   if (stats) *stats = DrainStats{};
@@ -1449,18 +1524,71 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   PhaseTrace tr("refill");
   std::vector<uint8_t> storage;
   const std::span<const uint8_t> raw = unwrap(image, storage, nullptr);
-  ParsedImage p = parse_image(raw, /*verify_bulk=*/false);
-  tr.mark("parse");
+  constexpr uint64_t W = DrainEngine::kWindow;
 
+  // Early start: META and the position of the bulk stream need only the first
+  // section headers, so the refill session is set up and the first ring
+  // windows' H2D is queued before the full parse and the plan (C2: ~1 ms of
+  // host work that used to precede the first copy).  The speculative windows
+  // carry every byte of their range; the scatter handles them whole (no
+  // direct runs start below them).  Nothing is trusted from the peek: the
+  // full parse below decides validity, and an image it refuses unwinds the
+  // session after the copies (which only write the engine's ring) complete.
+  const StreamPeek pk = peek_stream(raw);
+  std::optional<Session> holder;
   SessionConfig cfg;
-  cfg.seed = p.meta.seed;
-  cfg.arena_bytes = p.meta.arena_bytes;
   cfg.mode = mode;
   cfg.quiesce_timeout = quiesce_timeout;
-  Session session(cfg);
+  uint64_t n_spec = 0;
+  auto open_session = [&](uint64_t seed, uint64_t arena) {
+    cfg.seed = seed;
+    cfg.arena_bytes = arena;
+    holder.emplace(cfg);
+    DrainEngine& e = holder->drain_engine();
+    check_cuda(cudaEventRecord(e.ev_t0, e.s_pack), "event");
+  };
+  if (pk.ok) {
+    try {
+      open_session(pk.seed, pk.arena_bytes);
+    } catch (const Error&) {
+      holder.reset();  // whatever failed is reported in order, after the parse
+    }
+  }
+  if (holder) {
+    DrainEngine& e = holder->drain_engine();
+    n_spec = std::min<uint64_t>(DrainEngine::kSlots, (pk.stream_len + W - 1) / W);
+    check_cuda(cudaEventRecord(e.ev_c0, e.s_copy), "event");
+    for (uint64_t w = 0; w < n_spec; ++w) {
+      const uint64_t off = w * W, n = std::min(W + 16, pk.stream_len - off);
+      uint8_t* buf = e.d_ring + w * (W + 64);
+      for (uint64_t c = 0; c < n; c += DrainEngine::kCopyChunk)
+        check_cuda(cudaMemcpyAsync(buf + c, raw.data() + pk.s3 + off + c,
+                                   std::min(DrainEngine::kCopyChunk, n - c), cudaMemcpyHostToDevice,
+                                   e.s_copy),
+                   "H2D (early)");
+      check_cuda(cudaEventRecord(e.ev_ready[w], e.s_copy), "event");
+    }
+  }
+  tr.mark("early");
+  ParsedImage p;
+  try {
+    p = parse_image(raw, /*verify_bulk=*/false);
+  } catch (...) {
+    if (holder) cudaStreamSynchronize(holder->drain_engine().s_copy);
+    throw;
+  }
+  tr.mark("parse");
+  if (holder && (p.meta.seed != pk.seed || p.meta.arena_bytes != pk.arena_bytes ||
+                 p.sec[2].payload_off != pk.s3)) {
+    // (cannot happen for an image the parse accepts; kept as a guard)
+    cudaStreamSynchronize(holder->drain_engine().s_copy);
+    holder.reset();
+    n_spec = 0;
+  }
+  if (!holder) open_session(p.meta.seed, p.meta.arena_bytes);
+  Session& session = *holder;
   DeviceContext& ctx = session.device();
   DrainEngine& E = session.drain_engine();
-  check_cuda(cudaEventRecord(E.ev_t0, E.s_pack), "event");
   const double host_pre_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_entry).count();
   tr.mark("session");
@@ -1492,7 +1620,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   auto plan = [&](const std::vector<BulkItem>& items) {
     build_plan(items, P);
     plan_host_runs(P, P.stream_len);
-    plan_direct_runs(P, P.stream_len, false);
+    plan_direct_runs(P, P.stream_len, false, n_spec * W);  // none inside the early windows
     P.log_len = p.log.size();
     if (P.len3 != p.sec[2].length || P.len4 != p.sec[3].length ||
         s3 + P.stream_len != p.sec[3].payload_off + p.sec[3].length)
@@ -1525,25 +1653,15 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
 
   std::vector<uint64_t> live;
   live.reserve(p.facts.active.size());
-  // Every live Device extent is mapped before the replay, in coalesced runs,
-  // so the replay itself makes no driver calls.  The runs come from a bitmap
-  // of the 2 MiB blocks the extents touch, in address order (first fit hands
-  // out low addresses again after frees, so id order is not address order),
-  // without sorting the extents (C2: 16 k); one-block gaps are bridged.  The
-  // runs are mapped in pieces of at most kMapPiece in address order: the early
-  // data path maps, before it enqueues a window, the prefix of pieces that
-  // covers every destination the window writes, so a cold restart's physical
-  // allocation (cuMemCreate + map + access: ~1 ms per GiB) overlaps the H2D of
-  // the windows before it instead of preceding the first one.
-  constexpr uint64_t kMapPiece = 1ull << 30;
-  std::vector<std::pair<uint64_t, uint64_t>> map_pieces;  // arena offsets [lo, hi)
-  size_t mapped_pieces = 0;
-  auto map_upto = [&](uint64_t off_hi) {  // maps the pieces starting below off_hi
-    while (mapped_pieces < map_pieces.size() && map_pieces[mapped_pieces].first < off_hi) {
-      const auto& [lo, hi] = map_pieces[mapped_pieces++];
-      ctx.premap(kArenaBase + lo, hi - lo);
-    }
-  };
+  // map every live Device extent up front in coalesced runs, so the replay
+  // itself makes no driver calls (and the early data path below has its
+  // destinations).  The runs come from a bitmap of the 2 MiB blocks the
+  // extents touch, in address order (first fit hands out low addresses
+  // again after frees, so id order is not address order), without
+  // sorting the extents (C2: 16 k); one-block gaps are bridged.  Mapping in
+  // pieces interleaved with the windows' H2D was measured slower (C4 cold
+  // restart 2681 vs 2462 ms, profiles/r02/lazy_premap.txt): the VMM calls
+  // wait for the copies already queued.
   {
     constexpr uint64_t kBlock = 2ull << 20;
     std::vector<uint8_t> need((cfg.arena_bytes + kBlock - 1) / kBlock, 0);
@@ -1570,13 +1688,10 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       uint64_t e = b + 1;
       while (e < nb && (need[e] || (e + 1 < nb && need[e + 1]))) ++e;
       const uint64_t hi = std::min(e * kBlock, cfg.arena_bytes);
-      for (uint64_t lo = b * kBlock; lo < hi; lo += kMapPiece)
-        map_pieces.emplace_back(lo, std::min(hi, lo + kMapPiece));
+      ctx.premap(kArenaBase + b * kBlock, hi - b * kBlock);
       b = e;
     }
   }
-  if (!early) map_upto(~0ull);
-  else map_upto(1);  // the first piece now, beside the plan thread
   tr.mark("premap");
 
   uint64_t windows = 0, verifies = 0, scattered = 0;
@@ -1585,13 +1700,12 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   auto enqueue_data_path = [&] {
     if (P.stream_len <= 20) return;
     upload_plan(E, P, E.s_pack);
-    check_cuda(cudaEventRecord(E.ev_ready[0], E.s_pack), "event");
-    check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_ready[0], 0), "wait");
+    check_cuda(cudaEventRecord(E.ev_join[0], E.s_pack), "event");
+    check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_join[0], 0), "wait");
     windows = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
     if (stats) E.ensure_window_events(windows);
-    check_cuda(cudaEventRecord(E.ev_c0, E.s_copy), "event");
-    size_t spans_done = 0, run_i = 0, krun_i = 0, drun_i = 0, rec_i = 0;
-    uint64_t dst_hi = 0;  // highest arena offset written by the windows enqueued so far
+    if (!n_spec) check_cuda(cudaEventRecord(E.ev_c0, E.s_copy), "event");
+    size_t spans_done = 0, run_i = 0, krun_i = 0, drun_i = 0;
     std::vector<std::pair<uint64_t, uint64_t>> kr;
     constexpr uint64_t kVerifyBatch = 32768;  // 2 GiB of 64 KiB chunks: big enough to keep
                                               // K1 efficient beside the H2D; the tail
@@ -1602,21 +1716,15 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       const uint64_t off = w * DrainEngine::kWindow;
       const uint64_t len = std::min(DrainEngine::kWindow, P.stream_len - off);
       const uint64_t with_ahead = std::min(len + 16, P.stream_len - off);
-      if (early) {  // destinations of this window mapped before anything targets them
-        while (rec_i < P.recs.size() && P.recs[rec_i].out_off < off + len) {
-          const crac_record_t& r = P.recs[rec_i++];
-          if (r.len && r.ptr >= kArenaBase)
-            dst_hi = std::max(dst_hi, r.ptr - kArenaBase + std::max(r.len, r.ext));
-        }
-        map_upto(dst_hi);
+      if (w >= n_spec) {  // (the early windows are in their slots already)
+        if (w >= uint64_t(DrainEngine::kSlots))
+          check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_free[slot], 0), "wait");
+        copy_window(P, run_i, off, off + with_ahead, buf, const_cast<uint8_t*>(raw.data() + s3),
+                    false, E.s_copy);
+        copy_direct(P, drun_i, off, off + len, const_cast<uint8_t*>(raw.data() + s3), false,
+                    E.s_copy);
+        check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_copy), "event");
       }
-      if (w >= uint64_t(DrainEngine::kSlots))
-        check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_free[slot], 0), "wait");
-      copy_window(P, run_i, off, off + with_ahead, buf, const_cast<uint8_t*>(raw.data() + s3),
-                  false, E.s_copy);
-      copy_direct(P, drun_i, off, off + len, const_cast<uint8_t*>(raw.data() + s3), false,
-                  E.s_copy);
-      check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_copy), "event");
       check_cuda(cudaStreamWaitEvent(E.s_pack, E.ev_ready[slot], 0), "wait");
       if (stats) cudaEventRecord(E.ev_w0[w], E.s_pack);
       kernel_ranges(P, krun_i, off, off + len, kr);
@@ -1672,8 +1780,6 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     if (plan_err) std::rethrow_exception(plan_err);
     tr.mark("plan");
     enqueue_data_path();
-    map_upto(~0ull);  // extents no window wrote (empty payloads)
-    tr.mark("premap-rest");
   }
   ctx.begin_replay(live);
   try {
@@ -1738,6 +1844,8 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   } joiner{host_fill};
   tr.mark("place");
 
+  // pinned-host payload contents land before the data path's verify reads them
+  copy_pinned_runs(P, const_cast<uint8_t*>(raw.data() + s3), false);
   if (!early) enqueue_data_path();
   if (P.stream_len > 20) {
     host_fill.join();  // the host-resident pages' CRCs
@@ -1777,7 +1885,11 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       stats->pack_launches = windows;
       stats->pack_bytes = scattered;
       stats->pack_ms = median_window_ms(E, windows);
-      stats->h2d_bytes = P.stream_len - host_run_bytes(P);
+      // the early windows carried the host-run bytes of their range too
+      uint64_t early_host = 0;
+      for (const auto& [lo, hi] : P.host_runs)
+        if (lo < n_spec * W) early_host += std::min(hi, n_spec * W) - lo;
+      stats->h2d_bytes = P.stream_len - host_run_bytes(P) + early_host;
       stats->hash_bytes = hashed_bytes(P);
       stats->hash_launches = verifies;
       for (uint64_t v = 0; v < verifies; ++v) stats->hash_ms += elapsed(E.ev_v0[v], E.ev_v1[v]);
@@ -1785,7 +1897,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     stats->image_bytes = raw.size();
     stats->total_chunks = P.pay_first.back() + P.n_dev_pages + P.host_pages.size();
   }
-  return session;
+  return std::move(session);
 }
 
 // ---------------------------------------------------------------------------
@@ -1889,6 +2001,10 @@ void checkpoint_incremental(Session& session, PinnedImage& image, DrainStats* st
   // previous image of this session is unchanged (same log, same bulk
   // records, no managed allocations, same tail size) and `image` is that
   // image; otherwise this is a full drain.
+  if (!session.has_drain_engine()) {  // no previous image: a full drain
+    full_drain(session, image, stats, true);
+    return;
+  }
   finish_pending(session);
   DrainEngine& E = session.drain_engine();
   const ImagePlan& P = E.plan;

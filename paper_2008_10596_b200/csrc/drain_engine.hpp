@@ -122,6 +122,15 @@ struct ImagePlan {
   };
   std::vector<DirectRun> direct_runs;
   std::vector<std::pair<uint64_t, uint64_t>> skip_runs;  // host ∪ direct, sorted
+  // Pinned-host payload contents of at least kSkipMin (plan_host_runs): they
+  // live in host memory, so host threads copy them between the allocation and
+  // the image; no window copy, pack or scatter touches them (their records
+  // carry ptr 0) and they never cross PCIe for the move.  Also in host_runs.
+  struct PinnedRun {
+    uint64_t lo, hi;  // stream range of the content
+    uint64_t host;    // the allocation's host address of stream byte lo
+  };
+  std::vector<PinnedRun> pinned_runs;
   std::vector<uint8_t> pay_kind;  // AllocationKind of each payload record
   uint64_t log_len = 0;
   uint64_t tail_bytes = 0;  // STREAMS + APPSTATE + KERNEL_REGISTRY, framed

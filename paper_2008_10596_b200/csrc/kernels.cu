@@ -43,6 +43,8 @@ constexpr uint32_t kRowGap = 496;             // bytes between a lane's words
 // in-flight rows of the K1 variants that also compute the dirty-key lane: 16
 // (the CRC-only depth) spills the key's registers (ptxas -v), 8 does not
 constexpr int kKeyRows = 8;
+// rows per chain of the paired (two chunks per warp) key-lane variants
+constexpr int kKeyPairRows = 4;
 
 __device__ uint32_t g_tab[kTabWords];  // smem image of the lookup tables
 __device__ uint32_t g_t0[256];         // plain byte table
@@ -378,7 +380,7 @@ struct HashDrain {
   const uint64_t* dst_off;       // per span: image offset of its first payload byte
   uint8_t* host;                 // pinned image (UVA)
   unsigned long long* counters;  // [0] dirty chunks, [1] dirty bytes
-  // kMode 4 (split drain): the first n_writers CTAs write the dirty chunks the
+  // kMode 4 (split drain): the last n_writers CTAs write the dirty chunks the
   // others push into `queue` (chunk index + 1, 0 = not yet); qctl[0] pushed,
   // qctl[1] claimed by writers, qctl[2] hasher warps finished
   unsigned long long* queue;
@@ -478,13 +480,16 @@ __global__ void __launch_bounds__(kK1Threads, 1)
   __syncthreads();
 
   const uint32_t lane = threadIdx.x & 31;
+  // split drain: the writers are the LAST n_wr CTAs, so hashers (which never
+  // wait) are dispatched first; a writer only spins once every hasher CTA
+  // has been placed (crac_hash_drain_split checks they all fit at once)
   const uint32_t n_wr = kMode == 4 ? hd.n_writers : 0;
-  if (kMode == 4 && blockIdx.x < n_wr) {
+  if (kMode == 4 && blockIdx.x >= gridDim.x - n_wr) {
     drain_writer(spans, chunk_first, n_spans, chunk_bytes, hd, (gridDim.x - n_wr) * kK1Warps, lane);
     return;
   }
   const LaneLut lut = make_lut(static_cast<uint32_t>(__cvta_generic_to_shared(s_tab)), lane);
-  const uint64_t gw = (blockIdx.x - n_wr) * uint64_t(kK1Warps) + (threadIdx.x >> 5);
+  const uint64_t gw = blockIdx.x * uint64_t(kK1Warps) + (threadIdx.x >> 5);
   const uint64_t tw = (gridDim.x - n_wr) * uint64_t(kK1Warps);
   const uint64_t total_chunks = c_hi - c_lo;
   const uint64_t c_begin = c_lo + total_chunks * gw / tw, c_end = c_lo + total_chunks * (gw + 1) / tw;
@@ -1313,6 +1318,11 @@ int sm_count() {
   return n;
 }
 
+bool getenv_flag(const char* name) {
+  const char* e = std::getenv(name);
+  return e && e[0] && e[0] != '0';
+}
+
 uint32_t k_full_for(uint32_t chunk_bytes) {
   std::lock_guard<std::mutex> lk(g_kfull_mu);
   if (g_k_full_cache_bytes != chunk_bytes) {
@@ -1343,6 +1353,7 @@ int crac_gpu_init(void) {
                    k1_chunk_crc<16, 2, false>, k1_chunk_crc<8, 3, false>,
                    k1_chunk_crc<kKeyRows, 2, true>, k1_chunk_crc<8, 3, true>,
                    k1_chunk_crc<kKeyRows, 4, true>, k1_chunk_crc<4, 0, true, true>,
+                   k1_chunk_crc<kKeyPairRows, 4, true, true>,
                    k1_chunk_crc<8, 0, true, true>, k1_chunk_crc<4, 0, false, true>,
                    k1_chunk_crc<8, 0, false, true>})
       if (!e) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTabBytes));
@@ -1407,26 +1418,30 @@ int crac_chunk_key_range(const crac_span_t* d_spans, const uint64_t* d_chunk_fir
           d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, kf);
     return int(cudaGetLastError());
   }
-  // with the key lane, the key's registers beside 2 x 16 in-flight rows
-  // spill (ptxas: 136 B at 16 rows); CRAC_K1_KEY_ROWS picks the depth then
+  // Default: two chunks per warp (two independent CRC chains per lane, see
+  // k1_rows2), 8 rows in flight per chain for the CRC alone and 4 with the key
+  // lane (8 spills); 32 GiB hash-only on one B200: 6875 / 6136 GB/s against
+  // 6277 / 5518 for one chain (profiles/r02/k1_pair_chains.txt).
+  // CRAC_K1_PAIR=0 selects the one-chain kernels (CRAC_K1_ROWS /
+  // CRAC_K1_KEY_ROWS their depth), =4|8 the chain depth.
   static const int forced_key = [] {
     const char* e = std::getenv("CRAC_K1_KEY_ROWS");
     return e ? std::atoi(e) : 0;
   }();
+  static const int pair_env = [] {
+    const char* e = std::getenv("CRAC_K1_PAIR");
+    return e ? std::atoi(e) : -1;
+  }();
+  const int pair = pair_env >= 0 ? pair_env : (d_key ? 4 : 8);
   const int rows_nokey = forced ? forced : (chunk_bytes >= 32 * 512 ? 16 : chunk_bytes >= 8 * 512 ? 8 : 4);
   const int rows = d_key ? (forced_key ? forced_key : kKeyRows) : rows_nokey;
-  // paired chunks (two CRC chains per lane): CRAC_K1_PAIR=<rows per chain>
-  static const int pair = [] {
-    const char* e = std::getenv("CRAC_K1_PAIR");
-    return e ? std::atoi(e) : 0;
-  }();
   auto kern = d_key ? (rows == 4 ? k1_chunk_crc<4, 0, true>
                        : rows == 16 ? k1_chunk_crc<16, 0, true>
                        : rows == 12 ? k1_chunk_crc<12, 0, true> : k1_chunk_crc<8, 0, true>)
                     : (rows == 4 ? k1_chunk_crc<4, 0, false>
                        : rows == 16 ? k1_chunk_crc<16, 0, false> : k1_chunk_crc<8, 0, false>);
   if (pair && chunk_bytes >= 8 * 512)
-    kern = d_key ? (pair == 4 ? k1_chunk_crc<4, 0, true, true> : k1_chunk_crc<8, 0, true, true>)
+    kern = d_key ? (pair == 8 ? k1_chunk_crc<8, 0, true, true> : k1_chunk_crc<4, 0, true, true>)
                  : (pair == 4 ? k1_chunk_crc<4, 0, false, true> : k1_chunk_crc<8, 0, false, true>);
   kern<<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
       d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, d_key,
@@ -1445,6 +1460,7 @@ int crac_hash_drain_range(const crac_span_t* d_spans, const uint64_t* d_chunk_fi
   uint64_t blocks = (c_hi - c_lo + kK1Warps - 1) / kK1Warps;
   if (blocks > uint64_t(sm_count())) blocks = sm_count();
   if (!d_crc_prev || !d_counters || (!d_key) != (!d_key_prev)) return int(cudaErrorInvalidValue);
+  // (not paired: the inline chunk copy beside two chains spills 468 B)
   k1_chunk_crc<kKeyRows, 1, true><<<unsigned(blocks), kK1Threads, kTabBytes, cudaStream_t(stream)>>>(
       d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, d_key,
       k_full_for(chunk_bytes),
@@ -1470,9 +1486,21 @@ int crac_hash_drain_split(const crac_span_t* d_spans, const uint64_t* d_chunk_fi
   uint64_t hashers = (c_hi - c_lo + kK1Warps - 1) / kK1Warps;
   if (hashers > sms - n_writers) hashers = sms - n_writers;
   cudaStream_t st = cudaStream_t(stream);
+  // every CTA must be resident at once (writers spin until the hashers are
+  // done): if this context cannot hold the grid (MPS / green-context SM
+  // limits, 128 KiB of tables per CTA), drain fused instead
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, k1_chunk_crc<kKeyPairRows, 4, true, true>, kK1Threads, kTabBytes) != cudaSuccess ||
+      uint64_t(per_sm) * sms < hashers + n_writers || getenv_flag("CRAC_FORCE_FUSED")) {
+    cudaGetLastError();
+    return crac_hash_drain_range(d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc,
+                                 d_crc_prev, d_key, d_key_prev, d_dst_off, host_image, d_counters,
+                                 stream);
+  }
   const uint64_t q = c_hi - c_lo + uint64_t(n_writers) * kK1Warps + 1;
   if (cudaError_t e = cudaMemsetAsync(d_queue, 0, q * 8, st); e != cudaSuccess) return int(e);
-  k1_chunk_crc<kKeyRows, 4, true><<<unsigned(hashers + n_writers), kK1Threads, kTabBytes, st>>>(
+  k1_chunk_crc<kKeyPairRows, 4, true, true><<<unsigned(hashers + n_writers), kK1Threads, kTabBytes, st>>>(
       d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, d_key,
       k_full_for(chunk_bytes),
       HashDrain{d_crc_prev, d_key_prev, d_dst_off, host_image, d_counters, d_queue, d_counters + 2,

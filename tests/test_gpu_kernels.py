@@ -382,3 +382,21 @@ def test_forged_crc_collision_is_resent_with_keys(eng, split):
     img = bytes(image.numpy())
     assert img[16 + c * chunk:16 + (c + 1) * chunk] == bytes(piece)
     assert img[16:16 + c * chunk] == bytes(c * chunk)
+
+
+@pytest.mark.parametrize("env", [{"CRAC_FORCE_FUSED": "1"}, {"CRAC_K1_PAIR": "0"},
+                                 {"CRAC_K1_PAIR": "8"}], ids=["fused", "one-chain", "pair8-key"])
+def test_alternative_kernel_selections_drain_the_same_bytes(env):
+    """The fallbacks behind the defaults (the fused incremental drain the
+    split one falls back to when its grid cannot be co-resident; the
+    one-chain K1; 8-row chains with the key lane) drain the same bytes on
+    every path of tools/sanitize_paths.py (each asserts path == full drain)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    r = subprocess.run([sys.executable, str(root / "tools" / "sanitize_paths.py")],
+                       env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "sanitize paths ok" in r.stdout

@@ -432,6 +432,45 @@ def test_c3_host_runs_skip_the_link_and_match_reference(eng):
     assert rs.checkpoint()[0] == img
 
 
+@pytest.mark.parametrize("shadow", [0, 1, 64], ids=["sync", "ring+shadow", "all-shadow"])
+def test_pinned_payloads_move_on_the_host_and_match_reference(eng, shadow):
+    """Pinned-host payloads of >= 256 KiB are moved by host threads between
+    the allocation and the image (their bytes never cross PCIe for the move:
+    d2h / h2d exclude them); small ones ride the windows.  Byte-equal to the
+    reference for the synchronous and the stall-reduced drains, and through
+    the restart."""
+    MIB = 1 << 20
+    s = eng.Session(seed=6, arena_bytes=512 * MIB)
+    r = ref.RefSession(seed=6, arena_bytes=512 * MIB)
+    big = [5 * MIB + 3, 70 * MIB + 4096 + 5, 256 * 1024, 3 * MIB]
+    small = [1000, 255 * 1024]
+    for api in (s, r):
+        for k, size in enumerate(big + small):
+            i, _ = api.alloc(workloads.PINNED, size)
+            api.fill_synthetic(i, 20 + k)
+            d, _ = api.alloc(workloads.DEVICE, MIB + 17 * k)
+            api.fill_synthetic(d, 40 + k)
+    want = r.checkpoint()[0]
+    if shadow:
+        s.reserve_shadow(shadow * MIB)
+        img = eng.Image()
+        s.checkpoint_begin(img)
+        st = s.checkpoint_finish()
+        got = img.tobytes()
+        s.reserve_shadow(0)
+    else:
+        got, st = s.checkpoint()
+    assert got == want
+    assert st["d2h_bytes"] <= len(got) - sum(big)
+    rs, rst = eng.restart(got)
+    assert rst["h2d_bytes"] <= len(got) - sum(big)
+    assert _state(rs) == _state(s)
+    assert rs.checkpoint()[0] == want
+    rs.close()
+    s.close()
+    r.close()
+
+
 # ---------------------------------------------------------------------------
 # edge shapes and error parity (test_device_core.cpp / test_shim.cpp cases)
 # ---------------------------------------------------------------------------
