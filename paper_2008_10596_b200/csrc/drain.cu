@@ -1485,7 +1485,7 @@ namespace {
 // without any validation beyond bounds (the early start of restart_image).
 struct StreamPeek {
   bool ok = false;
-  uint64_t seed = 0, arena_bytes = 0, s3 = 0, stream_len = 0;
+  uint64_t seed = 0, arena_bytes = 0, s3 = 0, stream_len = 0, len4 = 0;
 };
 
 StreamPeek peek_stream(std::span<const uint8_t> raw) {
@@ -1508,6 +1508,7 @@ StreamPeek peek_stream(std::span<const uint8_t> raw) {
   if (!u64(k.s3 - 8, len3) || len3 > raw.size() || k.s3 + len3 + 20 > raw.size()) return k;
   if (!u64(k.s3 + len3 + 4 + 8, len4) || len4 > raw.size() - (k.s3 + len3 + 20)) return k;
   k.stream_len = len3 + 20 + len4;
+  k.len4 = len4;
   // a session must be constructible from META (DeviceContext's own checks)
   k.ok = k.arena_bytes > 0 && k.arena_bytes % kAlign == 0 && k.stream_len > 20;
   return k;
@@ -1540,14 +1541,19 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   cfg.mode = mode;
   cfg.quiesce_timeout = quiesce_timeout;
   uint64_t n_spec = 0;
+  double host_pre_ms = 0;  // entry -> the first device event (ev_t0)
   auto open_session = [&](uint64_t seed, uint64_t arena) {
     cfg.seed = seed;
     cfg.arena_bytes = arena;
     holder.emplace(cfg);
     DrainEngine& e = holder->drain_engine();
     check_cuda(cudaEventRecord(e.ev_t0, e.s_pack), "event");
+    host_pre_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_entry).count();
   };
-  if (pk.ok) {
+  // (only without managed pages: the early windows would carry the host
+  // runs the H2D otherwise skips, and a UVM refill is not link-bound)
+  if (pk.ok && pk.len4 == 0) {
     try {
       open_session(pk.seed, pk.arena_bytes);
     } catch (const Error&) {
@@ -1589,8 +1595,6 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   Session& session = *holder;
   DeviceContext& ctx = session.device();
   DrainEngine& E = session.drain_engine();
-  const double host_pre_ms =
-      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_entry).count();
   tr.mark("session");
 
   std::map<uint64_t, std::vector<KernelDescriptor>> binaries;
