@@ -477,8 +477,8 @@ def ncu_traffic(kernel):
     # the kernel variant each bench key times (ncu names template instances):
     # round 2 names first (paired chains: the drain's K1 with the key lane, the
     # refill verify CRC only), then round 1's
-    exact = {"k1_chunk_crc": ("void k1_chunk_crc<4, 0, true, true>", "void k1_chunk_crc<16, 0>"),
-             "k1_chunk_crc (refill verify)": ("void k1_chunk_crc<8, 0, false, true>",
+    exact = {"k1_chunk_crc": ("void k1_chunk_crc<4, 0, 1, 1>", "void k1_chunk_crc<16, 0>"),
+             "k1_chunk_crc (refill verify)": ("void k1_chunk_crc<8, 0, 0, 1>",
                                               "void k1_chunk_crc<16, 0>")}.get(kernel)
     name = kernel.split(" ")[0]
     units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
@@ -560,6 +560,11 @@ def run_c5(args, engine, sess, image, live, group, rank, world, peaks) -> None:
     """Incremental sequence (config C5): per dirty fraction, the hash-only pass
     and the incremental drain, both device-timed."""
     sess.checkpoint_into(image)  # full image; seeds the previous-epoch CRCs
+    verified = None
+    if not args.no_verify:  # the full image against regenerated content
+        rep0 = engine.verify_image(address=image.address(), synth_seed=rank + 1)
+        verified = {"full_image": {k: rep0[k] for k in ("ok", "payloads_compared",
+                                                        "payload_bytes_compared", "bad_sections")}}
     rows = {}
     epoch = 0
     for pct in (1, 5, 25):
@@ -586,6 +591,14 @@ def run_c5(args, engine, sess, image, live, group, rank, world, peaks) -> None:
             "drain_roofline_ms": round(max(live / peaks["hbm_gbs"] / 1e6,
                                            dirty / (peaks["pcie"]["d2h"] * 1e6)), 3),
             "state_GBps": round(live * world / (d_ms * 1e-3) / 1e9, 1)}
+    if verified is not None:  # the last incremental image: every section CRC recomputed
+        rep1 = engine.verify_image(address=image.address())
+        verified["last_incremental_image"] = {k: rep1[k] for k in ("ok", "crc_bytes", "bad_sections")}
+        verified["ok"] = bool(max(group.max(0.0 if verified["full_image"]["ok"] and rep1["ok"]
+                                            else 1.0), 0) == 0)
+        verified["method"] = ("crac_image_verify on the host cores: the first full image's Device "
+                              "payloads against regenerated f(seed, id, offset) and its CRCs; the "
+                              "last incremental image's section CRCs recomputed")
     import torch
     sync_ms = sess.checkpoint_into(image)["total_ms"]
     stall = None if args.no_stall else measure_stall(
@@ -602,7 +615,7 @@ def run_c5(args, engine, sess, image, live, group, rank, world, peaks) -> None:
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": WORKLOAD_NAMES["c5"], "live_bytes_per_gpu": live,
                        "chunk_bytes": 65536},
-            "incremental": rows, "stall_reduced": stall}), flush=True)
+            "incremental": rows, "stall_reduced": stall, "verified": verified}), flush=True)
 
 
 def dd_ceiling(path: Path, nbytes: int, streams: int = 8) -> dict:
@@ -954,6 +967,14 @@ def main() -> None:
         if args.workload == "c4":
             stall["precopy"] = measure_precopy(sess, image, drain_ms, args, rank)
 
+    # the refill floor of managed memory on this box (C3): fresh managed
+    # memory of the state's size, split residence populated from both sides
+    populate_ms = None
+    if args.workload == "c3":
+        sess.close()
+        sess = None
+        populate_ms = engine.probe_managed_populate(live)
+
     # reported CPU baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c4":
@@ -965,7 +986,16 @@ def main() -> None:
         launches = sum(d["hash_launches"] + d["pack_launches"] for d in drains) + \
             sum(r["hash_launches"] + r["pack_launches"] for r in refills)
         pd, ph = peaks["pcie"]["d2h"], peaks["pcie"]["h2d"]
-        link = 2 / (1 / pd + 1 / ph)  # one drain + one refill of the same bytes
+        # the step's floor: its D2H bytes at the D2H peak, then its H2D bytes
+        # at the H2D peak or, for managed memory, the measured populate
+        # ceiling of fresh managed memory with split residence if slower
+        # (C3: GPU faults + host first-touch faults, crac_probe_managed_populate)
+        d2h_b, h2d_b = drains[-1]["d2h_bytes"], refills[-1]["h2d_bytes"]
+        refill_floor_ms = max(h2d_b / (ph * 1e6), populate_ms or 0.0)
+        roof_ms = d2h_b / (pd * 1e6) + refill_floor_ms
+        link = 2 * live / (roof_ms * 1e6)  # state GB/s at the floor (C4: the harmonic link mean)
+        bound = "pcie" if not populate_ms or populate_ms <= h2d_b / (ph * 1e6) else \
+            "pcie (drain) + managed populate (refill)"
         d2h = drains[-1]["d2h_bytes"] / (mean("copy_ms", drains) * 1e-3) / 1e9 if mean("copy_ms", drains) else 0
         h2d = refills[-1]["h2d_bytes"] / (mean("copy_ms", refills) * 1e-3) / 1e9 if mean("copy_ms", refills) else 0
         per_gpu = value / world
@@ -986,13 +1016,18 @@ def main() -> None:
                         "checkpoint_ms": round(drain_ms, 3), "restart_ms": round(refill_ms, 3),
                         "restart_host_pre_ms": round(mean("host_pre_ms", refills), 3),
                         "image_bytes": drains[-1]["image_bytes"], "warm_restart": warm},
-            "roofline": {"bound": "pcie", "achieved": round(per_gpu, 3), "peak": round(link, 2),
+            "roofline": {"bound": bound, "achieved": round(per_gpu, 3), "peak": round(link, 2),
                          "unit": "GB/s", "frac": round(per_gpu / link, 4),
-                         "traffic": drains[-1]["d2h_bytes"] + refills[-1]["h2d_bytes"],
+                         "traffic": d2h_b + h2d_b,
                          "how": "state bytes per GPU per second of drain + refill against the "
-                                "harmonic mean of this GPU's measured D2H and H2D copy-engine "
-                                "peaks (every state byte crosses the link once each way); "
-                                "traffic = link bytes per step",
+                                "step's floor: its D2H bytes at this GPU's measured D2H peak plus "
+                                "its H2D bytes at the measured H2D peak (C4: the harmonic mean of "
+                                "the two peaks, every state byte crosses the link once each way), "
+                                "or the measured managed-populate time if longer; traffic = link "
+                                "bytes per step",
+                         "floor_ms": {"d2h": round(d2h_b / (pd * 1e6), 3),
+                                      "h2d": round(h2d_b / (ph * 1e6), 3),
+                                      "managed_populate": round(populate_ms, 3) if populate_ms else None},
                          "peak_source": "measured in this run (best of 5 passes of 2 GiB in 16 and "
                                         "64 MiB pinned copies)",
                          "d2h_GBps": round(d2h, 2), "h2d_GBps": round(h2d, 2),
@@ -1029,7 +1064,8 @@ def main() -> None:
             "setup_s": round(setup_s, 1), "warmup_s": round(warm_s, 1),
         }
         print(json.dumps(line), flush=True)
-    sess.close()
+    if sess is not None:
+        sess.close()
     if gbar:
         barrier()
         gbar.close(unlink=rank == 0)

@@ -135,6 +135,13 @@ int crac_image_verify(const void* image, uint64_t size, uint32_t threads, uint64
 int crac_session_verify_synthetic(crac_session_t* s, uint64_t seed, uint64_t* bad_allocations,
                                   uint64_t* bytes_checked);
 
+/* The ceiling of a managed-memory refill on this box (C3): fresh
+ * cudaMallocManaged memory of `bytes`, alternating `run`-byte runs first
+ * touched on the GPU (even runs, one kernel) and by `threads` host threads
+ * (odd runs, memcpy from page-locked memory) at the same time, as the refill
+ * restores split residence.  *ms = wall time of both; the memory is freed. */
+int crac_probe_managed_populate(uint64_t bytes, uint64_t run, uint32_t threads, double* ms);
+
 int crac_reserve_shadow(crac_session_t* s, uint64_t bytes);
 /* The shadow in another GPU's HBM (SURVEY §8f.3 buddy copy): reachable by
  * peer access (InvalidArgument otherwise); `device` = this session's GPU is

@@ -192,6 +192,9 @@ int crac_gather_chunks(const crac_span_t* d_spans, const uint64_t* d_chunk_first
  * Word k of allocation `id`: mix64(k + 0x1000003*id + (seed << 56)), LE. */
 int crac_fill_synth(uint8_t* d_dst, uint64_t len, uint64_t seed, uint64_t id,
                     uint64_t word_offset, void* stream);
+/* First touch on the GPU of the even `run`-byte runs of [d_managed, +len)
+ * (the managed-populate ceiling probe). */
+int crac_touch_even_runs(uint8_t* d_managed, uint64_t len, uint64_t run, void* stream);
 /* Sets *d_flag = 1 if any byte of [d_src, +len) differs from the synthetic
  * content of crac_fill_synth(seed, id, word offset 0); leaves it otherwise. */
 int crac_verify_synth(const uint8_t* d_src, uint64_t len, uint64_t seed, uint64_t id,

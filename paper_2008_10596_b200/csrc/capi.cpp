@@ -2,6 +2,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <algorithm>
+#include <vector>
+#include <chrono>
+#include <atomic>
+#include <thread>
 #include <cstring>
 #include <memory>
 
@@ -289,6 +294,37 @@ int crac_session_verify_synthetic(crac_session_t* s, uint64_t seed, uint64_t* ba
     for (size_t k = 0; k < dev.size(); ++k) bad += h[k] != 0;
     *bad_allocations = bad;
     *bytes_checked = bytes;
+  });
+}
+
+int crac_probe_managed_populate(uint64_t bytes, uint64_t run, uint32_t threads, double* ms) {
+  return guard([&] {
+    if (!bytes || !run || run % 16 || !ms) raise(Errc::InvalidArgument, "populate probe arguments");
+    if (threads == 0) threads = std::max(1u, std::thread::hardware_concurrency());
+    uint8_t* m = nullptr;
+    check_cuda(cudaMallocManaged(&m, bytes, cudaMemAttachGlobal), "probe managed");
+    std::unique_ptr<uint8_t, decltype(&cudaFree)> keep_m(m, &cudaFree);
+    uint8_t* src = nullptr;
+    check_cuda(cudaHostAlloc(&src, run, cudaHostAllocDefault), "probe pinned");
+    std::unique_ptr<uint8_t, decltype(&cudaFreeHost)> keep_s(src, &cudaFreeHost);
+    std::memset(src, 3, run);
+    cudaStream_t st = nullptr;
+    check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "probe stream");
+    const auto t0 = std::chrono::steady_clock::now();
+    check_cuda(cudaError_t(crac_touch_even_runs(m, bytes, run, st)), "probe kernel");
+    std::atomic<uint64_t> next{1};
+    std::vector<std::thread> pool;
+    const uint64_t runs = (bytes + run - 1) / run;
+    for (uint32_t t = 0; t < threads; ++t)
+      pool.emplace_back([&] {
+        for (uint64_t r; (r = next.fetch_add(2)) < runs;)
+          std::memcpy(m + r * run, src, std::min(run, bytes - r * run));
+      });
+    for (auto& t : pool) t.join();
+    const cudaError_t e = cudaStreamSynchronize(st);
+    *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    cudaStreamDestroy(st);
+    check_cuda(e, "probe sync");
   });
 }
 

@@ -1560,7 +1560,12 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       holder.reset();  // whatever failed is reported in order, after the parse
     }
   }
-  if (holder) {
+  // ... and only into an arena that came mapped: the premap's VMM calls
+  // (cold arena) wait for copies already queued (profiles/r02/lazy_premap.txt;
+  // C2 cold restart 17.9 ms with early windows, r02j)
+  if (holder && !holder->device().arena_premapped()) {
+    // keep the session; no early windows
+  } else if (holder) {
     DrainEngine& e = holder->drain_engine();
     n_spec = std::min<uint64_t>(DrainEngine::kSlots, (pk.stream_len + W - 1) / W);
     check_cuda(cudaEventRecord(e.ev_c0, e.s_copy), "event");
@@ -1684,6 +1689,8 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       for (uint64_t b = off / kBlock; b <= b1; ++b) need[b] = 1;
     }
     const uint64_t nb = need.size();
+    std::vector<std::pair<uint64_t, uint64_t>> runs;  // block ranges
+    uint64_t touched = 0;
     for (uint64_t b = 0; b < nb;) {
       if (!need[b]) {
         ++b;
@@ -1691,9 +1698,23 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       }
       uint64_t e = b + 1;
       while (e < nb && (need[e] || (e + 1 < nb && need[e + 1]))) ++e;
+      runs.emplace_back(b, e);
+      touched += e - b;
+      b = e;
+    }
+    // a cold arena pays ~3 driver calls per run (create, map, access): many
+    // runs over a mostly touched span (C2: 16 k small extents) are mapped as
+    // one run instead (the holes get memory too, at most 1/4 of the span)
+    static const bool single = [] {
+      const char* e = std::getenv("CRAC_PREMAP_SINGLE");
+      return !(e && e[0] == '0');
+    }();
+    if (single && !ctx.arena_premapped() && runs.size() > 8 &&
+        4 * touched >= 3 * (runs.back().second - runs.front().first))
+      runs = {{runs.front().first, runs.back().second}};
+    for (const auto& [b, e] : runs) {
       const uint64_t hi = std::min(e * kBlock, cfg.arena_bytes);
       ctx.premap(kArenaBase + b * kBlock, hi - b * kBlock);
-      b = e;
     }
   }
   tr.mark("premap");

@@ -1280,6 +1280,14 @@ __global__ void k_verify_synth(const uint8_t* __restrict__ src, uint64_t len, ui
   if (__syncthreads_or(diff != 0) && threadIdx.x == 0) *flag = 1u;
 }
 
+// Managed-populate ceiling probe (crac_probe_managed_populate): writes the
+// even `run`-byte runs of a fresh managed range (first touch on the GPU).
+__global__ void k_touch_even_runs(uint8_t* p, uint64_t n, uint64_t run) {
+  for (uint64_t i = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) * 16; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x * 16)
+    if (((i / run) & 1) == 0) *reinterpret_cast<uint4*>(p + i) = make_uint4(1, 2, 3, 4);
+}
+
 __global__ void k_mutate(const crac_span_t* __restrict__ spans, const uint64_t* __restrict__ ids,
                          const uint64_t* __restrict__ chunk_first, uint32_t n_spans,
                          uint32_t chunk_bytes, uint64_t total_chunks, uint64_t seed,
@@ -1645,6 +1653,12 @@ int crac_verify_synth(const uint8_t* d_src, uint64_t len, uint64_t seed, uint64_
   const uint64_t pairs = std::max<uint64_t>(1, len / 16);
   const uint64_t blocks = std::min<uint64_t>((pairs + 255) / 256, uint64_t(sm_count()) * 8);
   k_verify_synth<<<unsigned(blocks), 256, 0, cudaStream_t(stream)>>>(d_src, len, seed, id, d_flag);
+  return int(cudaGetLastError());
+}
+
+int crac_touch_even_runs(uint8_t* d_managed, uint64_t len, uint64_t run, void* stream) {
+  if (!len || !run || run % 16) return int(cudaErrorInvalidValue);
+  k_touch_even_runs<<<unsigned(sm_count() * 8), 256, 0, cudaStream_t(stream)>>>(d_managed, len, run);
   return int(cudaGetLastError());
 }
 

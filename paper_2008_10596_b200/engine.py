@@ -115,6 +115,7 @@ _SIGS = {
     "crac_reserve_shadow_on": (C.c_int, [_P, _U64, C.c_int]),
     "crac_crc32_host": (C.c_uint32, [_P, _U64, _U32]),
     "crac_session_set_barrier": (C.c_int, [_P, _P, _P]),
+    "crac_probe_managed_populate": (C.c_int, [_U64, _U64, _U32, C.POINTER(C.c_double)]),
     "crac_image_verify": (C.c_int, [_P, _U64, _U32, _U64, C.c_int, C.POINTER(VerifyReport)]),
     "crac_session_verify_synthetic": (C.c_int, [_P, _U64, _PU64, _PU64]),
     "crac_barrier_open": (C.c_int, [C.c_char_p, _U32, _U32, _U32, C.POINTER(_P)]),
@@ -171,6 +172,7 @@ _SIGS = {
     "crac_diff_compact": (C.c_int, [_P, _P, _U64, _P, _P, _P, _P]),
     "crac_gather_chunks": (C.c_int, [_P, _P, _U32, _U32, _P, _U64, _U64, _P, _P]),
     "crac_fill_synth": (C.c_int, [_P, _U64, _U64, _U64, _U64, _P]),
+    "crac_touch_even_runs": (C.c_int, [_P, _U64, _U64, _P]),
     "crac_verify_synth": (C.c_int, [_P, _U64, _U64, _U64, _P, _P]),
     "crac_mutate_chunks": (C.c_int, [_P, _P, _P, _U32, _U32, _U64, _U64, _U64, _U64, _P]),
 }
@@ -548,6 +550,14 @@ def verify_image(image=None, synth_seed: Optional[int] = None, threads: int = 0,
     _check(lib().crac_image_verify(p, n, threads, synth_seed or 0, int(synth_seed is not None),
                                    C.byref(rep)))
     return rep.as_dict()
+
+
+def probe_managed_populate(nbytes: int, run: int = 1 << 20, threads: int = 0) -> float:
+    """crac_probe_managed_populate: ms to first-touch fresh managed memory with
+    split residence (GPU: even runs, host threads: odd runs), both at once."""
+    ms = C.c_double()
+    _check(lib().crac_probe_managed_populate(nbytes, run, threads, C.byref(ms)))
+    return ms.value
 
 
 def restart(image, mode: int = DIRECT) -> tuple[Session, dict]:

@@ -19,7 +19,7 @@ for k in k_pack_records k_scatter_records; do
 done
 # the split incremental drain (C5 shape at 16 GiB, 5 % dirty)
 timeout 900 $NCU --set full --clock-control none --import-source on \
-  --kernel-name-base demangled -k "regex:k1_chunk_crc<4, 4" -s 1 -c 1 \
+  --kernel-name-base demangled -k "regex:k1_chunk_crc<\(int\)4, \(int\)4" -s 1 -c 1 \
   -o $OUT/prof_k1_split python bench.py --workload c5 --c5-footprint-gib 16 --steps 1 --warmup 1 \
   --no-stall > $OUT/prof_k1_split.log 2>&1
 timeout 3000 $NCU --metrics gpu__time_duration.sum --clock-control none -c 60000 --csv \
