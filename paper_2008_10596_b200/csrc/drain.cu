@@ -735,11 +735,13 @@ void plan_host_runs(ImagePlan& P, uint64_t limit) {
   // pinned-host payloads: content moved by host threads (pinned_runs), the
   // frame stays in the window stream
   P.pinned_runs.clear();
+  P.pinned_chunks = 0;
   for (size_t k = 0; k < P.pay_spans.size(); ++k) {
     if (P.pay_kind[k] != uint8_t(AllocationKind::PinnedHost)) continue;
     const uint64_t lo = P.pay_rec_off[k], hi = lo + P.pay_spans[k].len;
     if (hi - lo < kSkipMin || hi > limit) continue;
-    P.pinned_runs.push_back(ImagePlan::PinnedRun{lo, hi, P.pay_spans[k].ptr});
+    P.pinned_runs.push_back(ImagePlan::PinnedRun{lo, hi, P.pay_spans[k].ptr, k, P.pinned_chunks});
+    P.pinned_chunks += P.pay_first[k + 1] - P.pay_first[k];
     P.recs[k].ptr = 0;  // pack emits zeros / scatter skips: host-filled content
   }
   if (!P.pinned_runs.empty()) {
@@ -753,11 +755,35 @@ void plan_host_runs(ImagePlan& P, uint64_t limit) {
   P.skip_runs = P.host_runs;
 }
 
+// The second dirty-key lane of one chunk on the host: Key2 of kernels.cu
+// (16-byte word j = lane j % 32 of row j / 32; a partial last word
+// zero-padded; the same 64-bit finalizer).
+uint32_t chunk_key_host(const uint8_t* p, uint32_t len) {
+  uint64_t sum = 0;
+  for (uint32_t j = 0; 16ull * j < len; ++j) {
+    uint32_t w[4] = {0, 0, 0, 0};
+    std::memcpy(w, p + 16ull * j, std::min<uint64_t>(16, len - 16ull * j));
+    const uint32_t k = ((j & 31u) + 1) * 0x27D4EB2Fu + (j >> 5) * 0x9E3779B9u;
+    sum += uint64_t(w[0] + k) * (w[1] + 0x85EBCA6Bu) +
+           uint64_t(w[2] + (k ^ 0xC2B2AE35u)) * (w[3] + 0x165667B1u);
+  }
+  uint64_t x = sum ^ (uint64_t(len) * 0x9E3779B97F4A7C15ull);
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return uint32_t(x) ^ uint32_t(x >> 32);
+}
+
 // Host threads move the pinned-host payload contents: allocation -> image
-// (drain) or image -> allocation (refill), in 4 MiB pieces.
-void copy_pinned_runs(const ImagePlan& P, uint8_t* stream, bool drain) {
+// (drain) or image -> allocation (refill), in 64 KiB-chunk-aligned 4 MiB
+// pieces, and hash what they moved: every chunk's CRC (and, draining, its
+// dirty key) into h_pin_crc / h_pin_key, so no SM reads host memory for them.
+void copy_pinned_runs(DrainEngine& E, const ImagePlan& P, uint8_t* stream, bool drain) {
   if (P.pinned_runs.empty()) return;
-  constexpr uint64_t kPiece = 4ull << 20;
+  constexpr uint64_t kPiece = 4ull << 20;  // a multiple of the 64 KiB chunk
+  static_assert(kPiece % DrainEngine::kChunk == 0);
+  E.h_pin_crc.ensure(P.pinned_chunks);
+  E.h_pin_key.ensure(P.pinned_chunks);
   std::vector<std::pair<size_t, uint64_t>> pieces;  // (run, offset in run)
   for (size_t r = 0; r < P.pinned_runs.size(); ++r)
     for (uint64_t o = 0; o < P.pinned_runs[r].hi - P.pinned_runs[r].lo; o += kPiece)
@@ -766,9 +792,45 @@ void copy_pinned_runs(const ImagePlan& P, uint8_t* stream, bool drain) {
     const auto& run = P.pinned_runs[pieces[i].first];
     const uint64_t o = pieces[i].second, n = std::min(kPiece, run.hi - run.lo - o);
     uint8_t* host = reinterpret_cast<uint8_t*>(run.host) + o;
-    if (drain) std::memcpy(stream + run.lo + o, host, n);
-    else std::memcpy(host, stream + run.lo + o, n);
+    uint8_t* img = stream + run.lo + o;
+    if (drain) std::memcpy(img, host, n);
+    else std::memcpy(host, img, n);
+    for (uint64_t c = 0; c < n; c += DrainEngine::kChunk) {
+      const uint32_t len = uint32_t(std::min<uint64_t>(DrainEngine::kChunk, n - c));
+      const uint64_t slot = run.pin0 + (o + c) / DrainEngine::kChunk;
+      E.h_pin_crc.ptr[slot] = crc32_fast(host + c, len);
+      if (drain) E.h_pin_key.ptr[slot] = chunk_key_host(host + c, len);
+    }
   }, /*min_parallel=*/2);
+}
+
+// Uploads the host-computed chunk CRCs (and keys) of the pinned runs into the
+// payload chunk tables, on `st` (before the fold that reads them).
+void upload_pinned_hashes(DrainEngine& E, const ImagePlan& P, bool keys, cudaStream_t st) {
+  for (const auto& run : P.pinned_runs) {
+    const uint64_t c0 = P.pay_first[run.pay], n = P.pay_first[run.pay + 1] - c0;
+    check_cuda(cudaMemcpyAsync(E.d_pay_crc.ptr + c0, E.h_pin_crc.ptr + run.pin0, n * 4,
+                               cudaMemcpyHostToDevice, st),
+               "pinned crcs");
+    if (keys)
+      check_cuda(cudaMemcpyAsync(E.d_pay_key.ptr + c0, E.h_pin_key.ptr + run.pin0, n * 4,
+                                 cudaMemcpyHostToDevice, st),
+                 "pinned keys");
+  }
+}
+
+// K1 over payload chunks [c_lo, c_hi) minus the chunks of the pinned runs
+// (hashed by the host threads that move them).
+void hash_payloads_skip_pinned(DrainEngine& E, const ImagePlan& P, uint64_t c_lo, uint64_t c_hi,
+                               uint32_t max_ctas, cudaStream_t st, bool with_key) {
+  uint64_t at = c_lo;
+  for (const auto& run : P.pinned_runs) {
+    const uint64_t r0 = P.pay_first[run.pay], r1 = P.pay_first[run.pay + 1];
+    if (r1 <= at || r0 >= c_hi) continue;
+    if (r0 > at) hash_payloads(E, P, at, r0, max_ctas, st, with_key);
+    at = std::max(at, r1);
+  }
+  if (at < c_hi) hash_payloads(E, P, at, c_hi, max_ctas, st, with_key);
 }
 
 // Direct runs: the interior of every Device payload of at least
@@ -1166,7 +1228,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   if (!P.host_pages.empty() || !P.pinned_runs.empty())
     host_pass = std::thread([&] {
       try {
-        copy_pinned_runs(P, img + s3, true);  // before the app resumes (join below)
+        copy_pinned_runs(E, P, img + s3, true);  // before the app resumes (join below)
         host_pages_drain(E, P, img + s3, head, recorded);
       } catch (...) {
         host_err = std::current_exception();
@@ -1205,7 +1267,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
                                              E.d_shadow, E.s_shadow)),
                "frames");
   } else if (P.pay_first.back()) {
-    hash_payloads(E, P, 0, P.pay_first.back(), k1_ctas, E.s_hash);
+    hash_payloads_skip_pinned(E, P, 0, P.pay_first.back(), k1_ctas, E.s_hash, true);
   }
   // pages: the device-resident runs (the host-resident ones are hashed by
   // the host threads that move them)
@@ -1256,6 +1318,8 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   tr.mark("enqueue");
   if (host_pass.joinable()) host_pass.join();
   if (host_err) std::rethrow_exception(host_err);
+  // (fused: K1 hashed the pinned runs too, in place over the link)
+  if (!fused) upload_pinned_hashes(E, P, true, E.s_hash);
   // then K4 folds every CRC
   if (!P.host_pages.empty())
     check_cuda(cudaMemcpyAsync(E.d_page_crc.ptr + P.n_dev_pages, E.h_host_crc.ptr,
@@ -1486,6 +1550,7 @@ namespace {
 struct StreamPeek {
   bool ok = false;
   uint64_t seed = 0, arena_bytes = 0, s3 = 0, stream_len = 0, len4 = 0;
+  bool pinned_big = false;
 };
 
 StreamPeek peek_stream(std::span<const uint8_t> raw) {
@@ -1509,6 +1574,17 @@ StreamPeek peek_stream(std::span<const uint8_t> raw) {
   if (!u64(k.s3 + len3 + 4 + 8, len4) || len4 > raw.size() - (k.s3 + len3 + 20)) return k;
   k.stream_len = len3 + 20 + len4;
   k.len4 = len4;
+  // big pinned-host payloads stay off the link (host threads move them):
+  // the early windows would carry them, so such an image goes without
+  // (LOG records: seq u64, op u8, kind u8, u16, size u64, id u64, addr u64)
+  for (uint64_t at = h2 + 16; at + kLogRecordBytes <= h2 + 16 + len2; at += kLogRecordBytes) {
+    const uint8_t op = raw[at + 8], kind = raw[at + 9];
+    uint64_t size = 0;
+    std::memcpy(&size, raw.data() + at + 12, 8);
+    if (op == uint8_t(LogOp::Alloc) && kind == uint8_t(AllocationKind::PinnedHost) &&
+        size >= kSkipMin)
+      k.pinned_big = true;
+  }
   // a session must be constructible from META (DeviceContext's own checks)
   k.ok = k.arena_bytes > 0 && k.arena_bytes % kAlign == 0 && k.stream_len > 20;
   return k;
@@ -1553,16 +1629,33 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   };
   // (only without managed pages: the early windows would carry the host
   // runs the H2D otherwise skips, and a UVM refill is not link-bound)
-  if (pk.ok && pk.len4 == 0) {
+  if (pk.ok && pk.len4 == 0 && !pk.pinned_big) {
     try {
       open_session(pk.seed, pk.arena_bytes);
     } catch (const Error&) {
       holder.reset();  // whatever failed is reported in order, after the parse
     }
   }
-  // ... and only into an arena that came mapped: the premap's VMM calls
-  // (cold arena) wait for copies already queued (profiles/r02/lazy_premap.txt;
-  // C2 cold restart 17.9 ms with early windows, r02j)
+  // ... and only into an arena that is mapped before they are queued: the
+  // premap's VMM calls wait for copies already queued
+  // (profiles/r02/lazy_premap.txt; C2 cold restart 17.9 ms with early
+  // windows ahead of the premap, r02j).  A cold arena not much larger than
+  // the stream is mapped whole right here, before the parse (the log is not
+  // needed to know its extent); a sparse one keeps the premap from the log
+  // and goes without early windows.
+  static const bool cold_fullmap = [] {
+    const char* e = std::getenv("CRAC_COLD_FULLMAP");
+    return !(e && e[0] == '0');
+  }();
+  if (holder && !holder->device().arena_premapped() && cold_fullmap &&
+      pk.arena_bytes <= 2 * pk.stream_len + (1ull << 30)) {
+    try {
+      holder->device().premap(kArenaBase, pk.arena_bytes);
+    } catch (const Error&) {
+      holder.reset();  // reported in order after the parse, if at all
+    }
+    tr.mark("fullmap");
+  }
   if (holder && !holder->device().arena_premapped()) {
     // keep the session; no early windows
   } else if (holder) {
@@ -1775,7 +1868,8 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
           E.ensure_verify_events(verifies + 1);
           cudaEventRecord(E.ev_v0[verifies], E.s_pack);
         }
-        hash_payloads(E, P, P.pay_first[spans_done], P.pay_first[done], 0, E.s_pack, false);
+        hash_payloads_skip_pinned(E, P, P.pay_first[spans_done], P.pay_first[done], 0, E.s_pack,
+                                  false);
         if (stats) cudaEventRecord(E.ev_v1[verifies], E.s_pack);
         ++verifies;
         spans_done = done;
@@ -1869,8 +1963,9 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   } joiner{host_fill};
   tr.mark("place");
 
-  // pinned-host payload contents land before the data path's verify reads them
-  copy_pinned_runs(P, const_cast<uint8_t*>(raw.data() + s3), false);
+  // pinned-host payload contents: moved and hashed by host threads (the
+  // verify launches skip their chunks; their CRCs join the fold below)
+  copy_pinned_runs(E, P, const_cast<uint8_t*>(raw.data() + s3), false);
   if (!early) enqueue_data_path();
   if (P.stream_len > 20) {
     host_fill.join();  // the host-resident pages' CRCs
@@ -1884,6 +1979,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       check_cuda(cudaMemcpyAsync(E.d_page_crc.ptr + P.n_dev_pages, E.h_host_crc.ptr,
                                  P.host_pages.size() * 4, cudaMemcpyHostToDevice, E.s_pack),
                  "host page crcs");
+    upload_pinned_hashes(E, P, false, E.s_pack);
     enqueue_fold(E, P, E.s_pack);
     tr.mark("enqueue");
     check_cuda(cudaStreamSynchronize(E.s_pack), "refill sync");

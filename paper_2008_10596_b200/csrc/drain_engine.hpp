@@ -129,8 +129,11 @@ struct ImagePlan {
   struct PinnedRun {
     uint64_t lo, hi;  // stream range of the content
     uint64_t host;    // the allocation's host address of stream byte lo
+    uint64_t pay;     // payload index (its chunks: pay_first[pay] .. pay_first[pay + 1])
+    uint64_t pin0;    // first slot of its chunks in h_pin_crc / h_pin_key
   };
   std::vector<PinnedRun> pinned_runs;
+  uint64_t pinned_chunks = 0;  // chunks of all pinned runs
   std::vector<uint8_t> pay_kind;  // AllocationKind of each payload record
   uint64_t log_len = 0;
   uint64_t tail_bytes = 0;  // STREAMS + APPSTATE + KERNEL_REGISTRY, framed
@@ -168,6 +171,9 @@ struct DrainEngine {
   DevArray<uint32_t> d_fold;   // linear parts of crc3 / crc4 (K4)
   HostArray<uint32_t> h_fold;
   HostArray<uint32_t> h_host_crc;          // CRCs of host-resident pages (host threads)
+  // chunk CRCs / keys of the pinned-host payloads the host threads move
+  // (ImagePlan::pinned_runs), uploaded into d_pay_crc / d_pay_key
+  HostArray<uint32_t> h_pin_crc, h_pin_key;
   std::vector<cudaEvent_t> ev_land;        // window w's D2H has landed (host-page copies)
   HostArray<uint64_t> h_count, h_dirty_idx;
 
