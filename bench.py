@@ -98,6 +98,14 @@ def dist_env():
     return world, rank, local, local_world
 
 
+def job_gpu_indices(local_world: int) -> list[str]:
+    """nvidia-smi indices of the GPUs this node's ranks use (before pin_device
+    narrows CUDA_VISIBLE_DEVICES): the clocks are sampled on those only."""
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    devs = vis.split(",") if vis else [str(i) for i in range(64)]
+    return devs[:max(1, local_world)]
+
+
 def pin_device(local: int, world: int) -> None:
     # one process per GPU: each rank sees exactly its own device as cuda:0,
     # in both torch's runtime and libcrac_b200's (statically linked) runtime
@@ -781,6 +789,7 @@ def main() -> None:
     if args.dry_run:
         dry_run(args, world, rank, local)
         return
+    job_gpus = job_gpu_indices(local_world)
     pin_device(local, world)
 
     import torch
@@ -861,7 +870,7 @@ def main() -> None:
         e2e_steps.append(ev0.elapsed_time(ev1))
     wall = time.perf_counter() - wall0
     barrier()
-    clk = clocks.stop() if clocks else None
+    clk = clocks.stop(job_gpus) if clocks else None
 
     # whole box: each step lasts until its slowest rank is done (the ranks
     # start it together), i.e. max end - min start per step, summed

@@ -1101,6 +1101,34 @@ std::vector<BulkItem> live_items(DeviceContext& ctx, const std::vector<Allocatio
   return items;
 }
 
+// The bulk items of a drain straight from the live table (id order, their
+// records in `recs`), with managed page flags; drain_locked checks the
+// records against the log's active set.
+std::vector<BulkItem> table_items(DeviceContext& ctx, std::vector<AllocationRecord>& recs,
+                                  std::vector<std::vector<uint8_t>>& flags) {
+  thread_local std::vector<uint64_t> ptrs;
+  if (!ctx.live_backed(recs, ptrs))
+    raise(Errc::InvalidArgument, "the log's active set does not match the live allocations");
+  std::vector<BulkItem> items(recs.size());
+  size_t n_managed = 0;
+  for (const auto& r : recs) n_managed += r.kind == AllocationKind::Managed;
+  flags.clear();
+  flags.reserve(n_managed);
+  for (size_t k = 0; k < recs.size(); ++k) {
+    const AllocationRecord& rec = recs[k];
+    items[k] = BulkItem{rec.id, rec.kind, rec.size, ptrs[k], nullptr};
+    if (rec.kind == AllocationKind::Managed) {
+      const auto pages = ctx.managed_pages(rec.id);
+      std::vector<uint8_t> f(pages.size());
+      for (size_t i = 0; i < pages.size(); ++i)
+        f[i] = uint8_t((pages[i].device_resident ? 1 : 0) | (pages[i].dirty ? 2 : 0));
+      flags.push_back(std::move(f));
+      items[k].flags = &flags.back();
+    }
+  }
+  return items;
+}
+
 uint64_t tail_bytes(Session& session) {
   DeviceContext& ctx = session.device();
   return (20 + 8 * ctx.live_stream_ids().size()) + (20 + session.app_state().size()) +
@@ -1130,9 +1158,37 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   // the gate is held: the log cannot move, read it in place
   const std::span<const CallLogEntry> log = session.log().quiesced_view();
   tr.mark("log-snapshot");
-  active_set_into(log, E.scratch_active, E.scratch_alive);
-  const std::vector<AllocationRecord>& active = E.scratch_active;
-  tr.mark("active-set");
+  // The log side runs on a helper thread beside the plan: the active set of
+  // the log (the reference's definition of what the image holds, checked
+  // below against the live table the bulk items come from), then, once the
+  // image exists, the LOG section encoded into it with its CRC.  Neither is
+  // needed before the first D2H (C2: ~0.6 ms off the drain's critical path).
+  std::atomic<int> log_stage{0};  // 1: active set ready, 2: image ready, 3: LOG written
+  uint8_t* log_dst = nullptr;
+  std::exception_ptr log_err;
+  std::thread log_side([&] {
+    try {
+      active_set_into(log, E.scratch_active, E.scratch_alive);
+      log_stage.store(1, std::memory_order_release);
+      while (log_stage.load(std::memory_order_acquire) < 2) std::this_thread::yield();
+      if (log_dst) {
+        const uint64_t n = log.size() * kLogRecordBytes;
+        encode_log_into(log_dst + 16, log);
+        put_at<uint32_t>(log_dst + 16 + n, crc32_host(log_dst + 16, n));
+      }
+    } catch (...) {
+      log_err = std::current_exception();
+    }
+    log_stage.store(3, std::memory_order_release);
+  });
+  struct LogJoin {
+    std::thread& t;
+    std::atomic<int>& st;
+    ~LogJoin() {
+      if (st.load() < 2) st.store(2);  // unblock on an early exit
+      if (t.joinable()) t.join();
+    }
+  } log_join{log_side, log_stage};
   const std::vector<uint8_t> sec1 = meta_bytes(meta);
   const uint64_t sec2_len = log.size() * kLogRecordBytes;
   const std::vector<uint8_t> sec5 = streams_bytes(ctx.live_stream_ids());
@@ -1142,11 +1198,25 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
 
   std::vector<std::vector<uint8_t>> flags;
   ImagePlan& P = E.plan;
-  std::vector<BulkItem> items = live_items(ctx, active, flags, true);
+  thread_local std::vector<AllocationRecord> table;
+  std::vector<BulkItem> items = table_items(ctx, table, flags);
   tr.mark("live-items");
   build_plan(items, P);
   P.log_len = log.size();
   tr.mark("plan");
+  // the log's active set must be exactly the live table (what live_items
+  // used to check record by record), before any device work is queued
+  while (log_stage.load(std::memory_order_acquire) < 1) std::this_thread::yield();
+  if (log_err) std::rethrow_exception(log_err);
+  {
+    const std::vector<AllocationRecord>& active = E.scratch_active;
+    bool same = active.size() == table.size();
+    for (size_t k = 0; same && k < table.size(); ++k)
+      same = active[k].id == table[k].id && active[k].kind == table[k].kind &&
+             active[k].size == table[k].size && active[k].address == table[k].address;
+    if (!same) raise(Errc::InvalidArgument, "the log's active set does not match the live allocations");
+  }
+  tr.mark("active-set-check");
 
   // file layout: header | META | LOG | ALLOC hdr | stream | crc4 | STREAMS | APPSTATE | REGISTRY
   const uint64_t s3 = 16 + (20 + sec1.size()) + (20 + sec2_len) + 16;
@@ -1162,12 +1232,12 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   put_at<uint32_t>(img + 12, kSectionCount);
   uint64_t at = 16;
   at += write_section(img + at, 1, sec1);
-  {  // LOG, encoded in place
+  {  // LOG: header here, records + CRC by the log-side thread
     put_at<uint32_t>(img + at, 2);
     put_at<uint32_t>(img + at + 4, 0);
     put_at<uint64_t>(img + at + 8, sec2_len);
-    encode_log_into(img + at + 16, log);
-    put_at<uint32_t>(img + at + 16 + sec2_len, crc32_host(img + at + 16, sec2_len));
+    log_dst = img + at;
+    log_stage.store(2, std::memory_order_release);
     at += 20 + sec2_len;
   }
   put_at<uint32_t>(img + at, 3);
@@ -1191,6 +1261,8 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
     put_at<uint32_t>(img + s3 + 4, 4);
     put_at<uint32_t>(img + s3 + 8, 0);
     put_at<uint64_t>(img + s3 + 12, 0);
+    log_side.join();
+    if (log_err) std::rethrow_exception(log_err);
     Q.active = true;
     check_cuda(cudaEventRecord(E.ev_s1, E.s_pack), "event");
     return;
@@ -1247,8 +1319,10 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   // its stream position right after hashing it: one HBM read of the state
   // instead of two; frames and the UVM_PAGES part are written beside it.
   const bool fused = use_shadow && head == 0 && !P.pay_spans.empty();
+  tr.mark("host-pass-start");
   upload_plan(E, P, E.s_pack);
   if (fused) upload(E.d_pay_soff, P.pay_rec_off, E.s_pack);
+  tr.mark("upload");
   check_cuda(cudaEventRecord(E.ev_ready[0], E.s_pack), "event");
   check_cuda(cudaStreamWaitEvent(E.s_hash, E.ev_ready[0], 0), "wait");
   check_cuda(cudaStreamWaitEvent(E.s_shadow, E.ev_ready[0], 0), "wait");
@@ -1318,6 +1392,8 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   tr.mark("enqueue");
   if (host_pass.joinable()) host_pass.join();
   if (host_err) std::rethrow_exception(host_err);
+  log_side.join();
+  if (log_err) std::rethrow_exception(log_err);
   // (fused: K1 hashed the pinned runs too, in place over the link)
   if (!fused) upload_pinned_hashes(E, P, true, E.s_hash);
   // then K4 folds every CRC
@@ -1639,16 +1715,16 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   // ... and only into an arena that is mapped before they are queued: the
   // premap's VMM calls wait for copies already queued
   // (profiles/r02/lazy_premap.txt; C2 cold restart 17.9 ms with early
-  // windows ahead of the premap, r02j).  A cold arena not much larger than
-  // the stream is mapped whole right here, before the parse (the log is not
-  // needed to know its extent); a sparse one keeps the premap from the log
-  // and goes without early windows.
+  // windows ahead of the premap, r02j).  A cold arena at most ~4x the stream
+  // is mapped whole right here, before the parse (the log is not needed to
+  // know its extent); a sparser one keeps the premap from the log and goes
+  // without early windows.
   static const bool cold_fullmap = [] {
     const char* e = std::getenv("CRAC_COLD_FULLMAP");
     return !(e && e[0] == '0');
   }();
   if (holder && !holder->device().arena_premapped() && cold_fullmap &&
-      pk.arena_bytes <= 2 * pk.stream_len + (1ull << 30)) {
+      pk.arena_bytes <= 4 * pk.stream_len + (1ull << 30)) {
     try {
       holder->device().premap(kArenaBase, pk.arena_bytes);
     } catch (const Error&) {
