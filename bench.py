@@ -70,6 +70,8 @@ def parse_args():
                     help="rank plumbing only (no GPU): every rank prints its device assignment")
     ap.add_argument("--no-verify", action="store_true",
                     help="skip the host-side check of the final image and the restarted state")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="testing: every rank on the same GPU (the N-rank path on a 1-GPU box)")
     return ap.parse_args()
 
 
@@ -789,8 +791,9 @@ def main() -> None:
     if args.dry_run:
         dry_run(args, world, rank, local)
         return
-    job_gpus = job_gpu_indices(local_world)
-    pin_device(local, world)
+    job_gpus = job_gpu_indices(1 if args.share_gpu else local_world)
+    if not args.share_gpu:
+        pin_device(local, world)
 
     import torch
     from paper_2008_10596_b200 import engine
