@@ -701,8 +701,28 @@ def run_file(args, engine, sess, live, group, rank, world, cfg_extra, gbar=None)
     rs = group.max(statistics.mean(r["restart_s"] for r in rows))
     nbytes = rows[-1]["bytes"]
     sess.close()
-    img.close()
     staging.close()
+    # the GPU deflate (CRACSIMZ, compress="gpu") of the last image: its rate and
+    # ratio on this workload's content (synthetic words: incompressible, so
+    # mostly stored blocks), plus a compressible image of the same size
+    gpuz = None
+    if rank == 0:
+        zn, zms = engine.compress_image_gpu(address=img.address(), want_bytes=False)
+        zero = engine.Image()
+        zs = engine.Session(seed=9, arena_bytes=min(live, 4 * GIB) + 64 * MIB)
+        zi, _ = zs.alloc(engine.DEVICE, min(live, 4 * GIB))  # zero-filled state
+        zs.checkpoint_into(zero)
+        z0n, z0ms = engine.compress_image_gpu(address=zero.address(), want_bytes=False)
+        gpuz = {"image_bytes": nbytes, "compressed_bytes": zn, "ms": round(zms, 1),
+                "GBps": round(nbytes / (zms * 1e6), 2),
+                "zero_state": {"image_bytes": zero.address()[1], "compressed_bytes": z0n,
+                               "ms": round(z0ms, 1),
+                               "GBps": round(zero.address()[1] / (z0ms * 1e6), 2)},
+                "how": "crac_compress_image_gpu from the pinned image: H2D, K5 deflate (32 KiB "
+                       "segments, fixed Huffman LZ77, stored fallback), gather, D2H; wall time"}
+        zs.close()
+        zero.close()
+    img.close()
     ceiling = dd_ceiling(path, min(nbytes, 16 * GIB)) if rank == 0 else None
     try:
         path.unlink()
@@ -733,7 +753,7 @@ def run_file(args, engine, sess, live, group, rank, world, cfg_extra, gbar=None)
                     "restart_from_file_GBps": round(live / rs / 1e9, 3),
                     "checkpoint_to_file_s": round(ck, 3), "restart_from_file_s": round(rs, 3),
                     "phases_ms": m, "o_direct": all(r["direct"] for r in rows)},
-        "roofline": roof, "cpu_baseline": cpu}), flush=True)
+        "roofline": roof, "cpu_baseline": cpu, "gpu_deflate": gpuz}), flush=True)
 
 
 def cpu_baseline_file(sample_gib: float, region: int, io_dir: Path) -> dict:

@@ -175,8 +175,16 @@ typedef struct crac_io_stats {
   int32_t direct;     /* 1 if O_DIRECT */
   uint64_t bounced;   /* bytes moved through an aligned bounce buffer */
 } crac_io_stats_t;
+/* compress: 0 none; 1 the reference's CRACSIMZ bytes (zlib compress2 level 6,
+ * host, image.cpp:419-430); 2 the GPU deflate (K5): a different, valid zlib
+ * stream in the same wrapper, which the reference's maybe_decompress inflates
+ * to the exact image. */
 int crac_checkpoint_to_file(crac_session_t* s, crac_image_t* img, const char* path, int compress,
                             crac_stats_t* drain, crac_io_stats_t* io);
+/* The GPU deflate of any image into a CRACSIMZ wrapper (free with
+ * crac_buffer_free); *ms = wall time. */
+int crac_compress_image_gpu(const void* image, uint64_t n, uint8_t** out, uint64_t* out_n,
+                            double* ms);
 int crac_restart_from_file(const char* path, crac_image_t* img, int mode, crac_session_t** out,
                            crac_stats_t* refill, crac_io_stats_t* io);
 /* The parallel file transfer alone, on any host buffer (no GPU needed):

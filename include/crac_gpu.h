@@ -192,6 +192,22 @@ int crac_gather_chunks(const crac_span_t* d_spans, const uint64_t* d_chunk_first
  * Word k of allocation `id`: mix64(k + 0x1000003*id + (seed << 56)), LE. */
 int crac_fill_synth(uint8_t* d_dst, uint64_t len, uint64_t seed, uint64_t id,
                     uint64_t word_offset, void* stream);
+/* K5, GPU deflate (deflate.cu): [d_in, +n) in CRAC_DEFLATE_SEGMENT-byte
+ * segments, one deflate piece each (fixed Huffman LZ77, or a stored block if
+ * that would not shrink it), every piece byte-aligned at both ends (sync
+ * flush), written to its CRAC_DEFLATE_SLOT-byte slot of d_slots; d_len[s] =
+ * its byte length (bit 31 set: a stored piece, built by the gather from the
+ * input), d_adler[s] = the Adler-32 of segment s alone.  With last_is_final
+ * the last piece carries BFINAL.  crac_gather_segments writes the pieces to
+ * d_out at the (host-computed) d_offset. */
+#define CRAC_DEFLATE_SEGMENT 32768u
+#define CRAC_DEFLATE_SLOT (CRAC_DEFLATE_SEGMENT + CRAC_DEFLATE_SEGMENT / 8 + 64u)
+int crac_deflate_segments(const uint8_t* d_in, uint64_t n, uint8_t* d_slots, uint32_t* d_len,
+                          uint32_t* d_adler, int last_is_final, void* stream);
+int crac_gather_segments(const uint8_t* d_in, uint64_t n, const uint8_t* d_slots,
+                         const uint32_t* d_len, const uint64_t* d_offset, uint8_t* d_out,
+                         int last_is_final, void* stream);
+
 /* First touch on the GPU of the even `run`-byte runs of [d_managed, +len)
  * (the managed-populate ceiling probe). */
 int crac_touch_even_runs(uint8_t* d_managed, uint64_t len, uint64_t run, void* stream);

@@ -158,6 +158,24 @@ Session restart_from_file(const std::filesystem::path& path, const KernelCatalog
 // files as the reference's checkpoint_to_file / restart_from_file.
 void checkpoint_to_file(Session& session, PinnedImage& image, const std::filesystem::path& path,
                         bool compress, DrainStats* drain = nullptr, FileIoStats* io = nullptr);
+// Compression of checkpoint_to_file: none, the reference's bytes (zlib
+// compress2 level 6 on the host, compress_image), or the GPU deflate
+// (compress_image_gpu: a different, valid zlib stream that the reference's
+// maybe_decompress inflates to the exact image).
+enum class Compression { None = 0, Zlib6 = 1, Gpu = 2 };
+void checkpoint_to_file(Session& session, PinnedImage& image, const std::filesystem::path& path,
+                        Compression compression, DrainStats* drain = nullptr,
+                        FileIoStats* io = nullptr, double* compress_ms = nullptr);
+// GPU deflate of an image into a CRACSIMZ wrapper (SURVEY §8f.4, K5 in
+// deflate.cu): segments of 32 KiB compressed independently with fixed
+// Huffman codes and joined by sync flushes, Adler-32 folded on the host.
+std::vector<uint8_t> compress_image_gpu(std::span<const uint8_t> image, double* ms = nullptr);
+// The same into caller memory of at least compressed_bound_gpu(n) bytes;
+// returns the bytes written.
+uint64_t compressed_bound_gpu(uint64_t n);
+uint8_t* alloc_compressed_host(uint64_t bytes);  // 2 MiB-aligned, THP; std::free
+uint64_t compress_image_gpu_into(std::span<const uint8_t> image, uint8_t* out, uint64_t cap,
+                                 double* ms = nullptr);
 Session restart_from_file(const std::filesystem::path& path, PinnedImage& staging,
                           const KernelCatalog& catalog, TableMode mode = TableMode::Direct,
                           DrainStats* refill = nullptr, FileIoStats* io = nullptr);

@@ -32,9 +32,9 @@ EXTRA = {
     "std_kernels.cu": ["-fmad=false"],   # reference f32 kernels are built without contraction
     "kernels.cu": ["-Xptxas", "-v"] if os.environ.get("CRAC_PTXAS_V") else [],
 }
-SOURCES = ["kernels.cu", "device_core.cu", "drain.cu", "std_kernels.cu",
+SOURCES = ["kernels.cu", "device_core.cu", "drain.cu", "std_kernels.cu", "deflate.cu",
            "shim.cpp", "image.cpp", "image_io.cpp", "crc_host.cpp", "ckpt_engine.cpp", "capi.cpp",
-           "global_barrier.cpp", "verify.cpp"]
+           "global_barrier.cpp", "verify.cpp", "compress.cu"]
 
 
 def _headers_mtime() -> float:

@@ -434,9 +434,21 @@ int crac_checkpoint_to_file(crac_session_t* s, crac_image_t* img, const char* pa
   return guard([&] {
     DrainStats d;
     FileIoStats f;
-    checkpoint_to_file(s->s, img->img, path, compress != 0, drain ? &d : nullptr, &f);
+    if (compress < 0 || compress > 2) raise(Errc::InvalidArgument, "compress must be 0, 1 or 2");
+    checkpoint_to_file(s->s, img->img, path, static_cast<Compression>(compress),
+                       drain ? &d : nullptr, &f);
     to_c(d, drain);
     to_c(f, io);
+  });
+}
+
+int crac_compress_image_gpu(const void* image, uint64_t n, uint8_t** out, uint64_t* out_n,
+                            double* ms) {
+  return guard([&] {
+    const uint64_t cap = compressed_bound_gpu(n);
+    std::unique_ptr<uint8_t, decltype(&std::free)> buf(alloc_compressed_host(cap), &std::free);
+    *out_n = compress_image_gpu_into({static_cast<const uint8_t*>(image), n}, buf.get(), cap, ms);
+    *out = buf.release();  // (no copy: the caller frees it with crac_buffer_free)
   });
 }
 

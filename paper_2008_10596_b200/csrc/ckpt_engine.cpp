@@ -61,10 +61,27 @@ void checkpoint_to_file(Session& session, const std::filesystem::path& path, boo
 
 void checkpoint_to_file(Session& session, PinnedImage& image, const std::filesystem::path& path,
                         bool compress, DrainStats* drain, FileIoStats* io) {
+  checkpoint_to_file(session, image, path, compress ? Compression::Zlib6 : Compression::None, drain,
+                     io);
+}
+
+void checkpoint_to_file(Session& session, PinnedImage& image, const std::filesystem::path& path,
+                        Compression compression, DrainStats* drain, FileIoStats* io,
+                        double* compress_ms) {
   checkpoint_image(session, image, drain);
-  if (compress) {
+  if (compress_ms) *compress_ms = 0;
+  if (compression == Compression::Zlib6) {
+    const auto t0 = std::chrono::steady_clock::now();
     const std::vector<uint8_t> z = compress_image(image.bytes());
+    if (compress_ms)
+      *compress_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     write_file_parallel(path, z, io);
+  } else if (compression == Compression::Gpu) {
+    const uint64_t cap = compressed_bound_gpu(image.size());
+    std::unique_ptr<uint8_t, decltype(&std::free)> z(alloc_compressed_host(cap), &std::free);
+    const uint64_t zn = compress_image_gpu_into(image.bytes(), z.get(), cap, compress_ms);
+    write_file_parallel(path, {z.get(), zn}, io);
   } else {
     write_file_parallel(path, image.bytes(), io);
   }

@@ -115,6 +115,7 @@ _SIGS = {
     "crac_reserve_shadow_on": (C.c_int, [_P, _U64, C.c_int]),
     "crac_crc32_host": (C.c_uint32, [_P, _U64, _U32]),
     "crac_session_set_barrier": (C.c_int, [_P, _P, _P]),
+    "crac_compress_image_gpu": (C.c_int, [_P, _U64, C.POINTER(_P), _PU64, C.POINTER(C.c_double)]),
     "crac_probe_managed_populate": (C.c_int, [_U64, _U64, _U32, C.POINTER(C.c_double)]),
     "crac_image_verify": (C.c_int, [_P, _U64, _U32, _U64, C.c_int, C.POINTER(VerifyReport)]),
     "crac_session_verify_synthetic": (C.c_int, [_P, _U64, _PU64, _PU64]),
@@ -172,6 +173,8 @@ _SIGS = {
     "crac_diff_compact": (C.c_int, [_P, _P, _U64, _P, _P, _P, _P]),
     "crac_gather_chunks": (C.c_int, [_P, _P, _U32, _U32, _P, _U64, _U64, _P, _P]),
     "crac_fill_synth": (C.c_int, [_P, _U64, _U64, _U64, _U64, _P]),
+    "crac_deflate_segments": (C.c_int, [_P, _U64, _P, _P, _P, C.c_int, _P]),
+    "crac_gather_segments": (C.c_int, [_P, _U64, _P, _P, _P, _P, C.c_int, _P]),
     "crac_touch_even_runs": (C.c_int, [_P, _U64, _U64, _P]),
     "crac_verify_synth": (C.c_int, [_P, _U64, _U64, _U64, _P, _P]),
     "crac_mutate_chunks": (C.c_int, [_P, _P, _P, _U32, _U32, _U64, _U64, _U64, _U64, _P]),
@@ -196,6 +199,13 @@ def lib() -> C.CDLL:
             fn.argtypes = args
         _LIB = L
     return _LIB
+
+
+def _bytes_at(ptr: int, n: int) -> bytes:
+    """Copy of n bytes at ptr (ctypes.string_at takes an int size: wrong past 2 GiB)."""
+    if not n:
+        return b""
+    return bytes(memoryview((C.c_ubyte * n).from_address(ptr)))
 
 
 def _check(rc: int) -> None:
@@ -407,12 +417,15 @@ class Session:
         return st.as_dict()
 
     def checkpoint_to_file(self, path, image: Optional[Image] = None,
-                           compress: bool = False) -> tuple[dict, dict]:
+                           compress=False) -> tuple[dict, dict]:
         """checkpoint_to_file: GPU drain into `image`, then the parallel
-        (O_DIRECT, fdatasync'd) file write.  Returns (drain stats, io stats)."""
+        (O_DIRECT, fdatasync'd) file write.  compress: False, True (the
+        reference's zlib level-6 bytes) or "gpu" (the GPU deflate).  Returns
+        (drain stats, io stats)."""
         img = image or Image()
         st, io = Stats(), IoStats()
-        _check(lib().crac_checkpoint_to_file(self._h, img._h, str(path).encode(), int(compress),
+        mode = 2 if compress == "gpu" else int(bool(compress))
+        _check(lib().crac_checkpoint_to_file(self._h, img._h, str(path).encode(), mode,
                                              C.byref(st), C.byref(io)))
         return st.as_dict(), io.as_dict()
 
@@ -452,7 +465,7 @@ class Session:
         p, n = C.c_void_p(), C.c_uint64()
         _check(lib().crac_checkpoint_value(self._h, C.byref(p), C.byref(n)))
         try:
-            return C.string_at(p, n.value)
+            return _bytes_at(p.value, n.value)
         finally:
             lib().crac_buffer_free(p)
 
@@ -537,6 +550,25 @@ class Session:
             pass
 
 
+def compress_image_gpu(image=None, address: Optional[tuple[int, int]] = None,
+                       want_bytes: bool = True):
+    """crac_compress_image_gpu: (CRACSIMZ bytes from the GPU deflate, ms);
+    `address` = (ptr, size) compresses an image in place (e.g. a pinned one);
+    want_bytes=False returns (compressed size, ms) without copying it out."""
+    if address is not None:
+        p, n, keep = C.c_void_p(address[0]), address[1], None
+    else:
+        p, n, keep = _buf(image)
+    out, on, ms = C.c_void_p(), C.c_uint64(), C.c_double()
+    _check(lib().crac_compress_image_gpu(p, n, C.byref(out), C.byref(on), C.byref(ms)))
+    try:
+        if not want_bytes:
+            return on.value, ms.value
+        return _bytes_at(out.value, on.value), ms.value
+    finally:
+        lib().crac_buffer_free(out)
+
+
 def verify_image(image=None, synth_seed: Optional[int] = None, threads: int = 0,
                  address: Optional[tuple[int, int]] = None) -> dict:
     """crac_image_verify: host-only check of an image (section CRCs recomputed
@@ -608,7 +640,7 @@ def read_file(path, threads: int = 0, chunk_bytes: int = 0, direct: bool = True,
     got, io = C.c_uint64(), IoStats()
     _check(lib().crac_file_read(str(path).encode(), C.c_void_p(base), cap - offset, threads,
                                 chunk_bytes, int(direct), C.byref(got), C.byref(io)))
-    return C.string_at(base, got.value), io.as_dict()
+    return _bytes_at(base, got.value), io.as_dict()
 
 
 def drop_arena_cache(device: int = -1) -> None:
