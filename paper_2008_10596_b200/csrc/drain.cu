@@ -1970,21 +1970,42 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     cudaStreamSynchronize(E.s_pack);
   };
 
+  // the replay (host bookkeeping; the extents are premapped) runs on its own
+  // thread beside the plan join and the data path's enqueue when early
+  std::exception_ptr replay_err;
+  auto do_replay = [&] {
+    ctx.begin_replay(live);
+    try {
+      replay_log_into(ctx, p.log, &binaries, nullptr);
+    } catch (...) {
+      replay_err = std::current_exception();
+    }
+    ctx.end_replay();
+  };
+  std::thread replay_thread;
+  struct ReplayJoin {
+    std::thread& t;
+    ~ReplayJoin() {
+      if (t.joinable()) t.join();
+    }
+  } replay_join{replay_thread};
   if (early) {
+    replay_thread = std::thread([&, dev = E.device] {
+      cudaSetDevice(dev);  // stream creates of the replay land on this device
+      do_replay();
+    });
     early_plan.join();
     if (plan_err) std::rethrow_exception(plan_err);
     tr.mark("plan");
     enqueue_data_path();
+    replay_thread.join();
+  } else {
+    do_replay();
   }
-  ctx.begin_replay(live);
-  try {
-    replay_log_into(ctx, p.log, &binaries, nullptr);
-  } catch (...) {
-    ctx.end_replay();
+  if (replay_err) {
     quiet();
-    throw;
+    std::rethrow_exception(replay_err);
   }
-  ctx.end_replay();
   tr.mark("replay");
   if (ctx.live_stream_ids() != p.streams) {
     quiet();

@@ -71,6 +71,15 @@ struct IdxAlloc {  // DeviceContext's logic over HoleIndex
   }
 };
 
+struct FusedAlloc {  // the one-search forms DeviceContext uses since round 2
+  cracsim::HoleIndex holes;
+  bool alloc(uint64_t need, uint64_t& addr) {
+    uint64_t len = 0;
+    return holes.take_first_fit(need, addr, len);
+  }
+  void free(uint64_t addr, uint64_t len) { holes.release(addr, len); }
+};
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -80,8 +89,10 @@ int main(int argc, char** argv) {
     const uint64_t base = 0x0D0000000000ull, arena = 1ull << (20 + round % 6);
     RefAlloc ref;
     IdxAlloc idx;
+    FusedAlloc fused;
     ref.holes.emplace(base, arena);
     idx.holes.insert(base, arena);
+    fused.holes.insert(base, arena);
     std::vector<std::pair<uint64_t, uint64_t>> live;
     for (int op = 0; op < 4000; ++op) {
       if (!live.empty() && rng() % 100 < 40) {
@@ -90,11 +101,12 @@ int main(int argc, char** argv) {
         live.erase(live.begin() + long(i));
         ref.free(addr, len);
         idx.free(addr, len);
+        fused.free(addr, len);
       } else {
         const uint64_t need = ((1 + rng() % 30000) + 255) / 256 * 256;
-        uint64_t a = 0, b = 0;
-        const bool ra = ref.alloc(need, a), ib = idx.alloc(need, b);
-        if (ra != ib || (ra && a != b)) {
+        uint64_t a = 0, b = 0, c = 0;
+        const bool ra = ref.alloc(need, a), ib = idx.alloc(need, b), fc = fused.alloc(need, c);
+        if (ra != ib || (ra && a != b) || ra != fc || (ra && a != c)) {
           std::printf("FAIL alloc round %d op %d\n", round, op);
           return 1;
         }
@@ -102,7 +114,10 @@ int main(int argc, char** argv) {
       }
       std::vector<std::pair<uint64_t, uint64_t>> want(ref.holes.begin(), ref.holes.end()), got;
       idx.holes.for_each([&](uint64_t k, uint64_t v) { got.emplace_back(k, v); });
-      if (want != got || idx.holes.size() != want.size()) {
+      std::vector<std::pair<uint64_t, uint64_t>> got2;
+      fused.holes.for_each([&](uint64_t k, uint64_t v) { got2.emplace_back(k, v); });
+      if (want != got || idx.holes.size() != want.size() || want != got2 ||
+          fused.holes.size() != want.size()) {
         std::printf("FAIL holes round %d op %d\n", round, op);
         return 1;
       }
