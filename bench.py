@@ -788,10 +788,13 @@ def dry_run(args, world, rank, local) -> None:
     b = engine.Barrier(barrier_name(world), world, rank, timeout_ms=60000)
     b.wait()
     group.barrier()
-    print(json.dumps({"dry_run": True, "rank": rank, "world": world, "local_rank": local,
-                      "cuda_visible_devices": os.environ.get("CUDA_VISIBLE_DEVICES"),
-                      "barrier_generation": b.generation()}), flush=True)
-    group.barrier()
+    gen = b.generation()
+    for r in range(world):  # one line per rank, in rank order (one shared stdout)
+        if r == rank:
+            print(json.dumps({"dry_run": True, "rank": rank, "world": world, "local_rank": local,
+                              "cuda_visible_devices": os.environ.get("CUDA_VISIBLE_DEVICES"),
+                              "barrier_generation": gen}), flush=True)
+        group.barrier()
     b.close(unlink=rank == 0)
     group.close()
 

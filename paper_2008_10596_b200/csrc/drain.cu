@@ -1626,6 +1626,7 @@ namespace {
 struct StreamPeek {
   bool ok = false;
   uint64_t seed = 0, arena_bytes = 0, s3 = 0, stream_len = 0, len4 = 0;
+  uint64_t arena_hi = 0;  // end of the highest Device extent in the LOG (2 MiB rounded)
   bool pinned_big = false;
 };
 
@@ -1644,7 +1645,7 @@ StreamPeek peek_stream(std::span<const uint8_t> raw) {
   std::memcpy(&crc1, raw.data() + 56, 4);
   if (crc32_host(raw.data() + 32, 24) != crc1) return k;
   const uint64_t h2 = 16 + 20 + len1;
-  if (!u64(h2 + 8, len2) || len2 > raw.size()) return k;
+  if (!u64(h2 + 8, len2) || len2 > raw.size() || h2 + 16 + len2 > raw.size()) return k;
   k.s3 = h2 + 20 + len2 + 16;
   if (!u64(k.s3 - 8, len3) || len3 > raw.size() || k.s3 + len3 + 20 > raw.size()) return k;
   if (!u64(k.s3 + len3 + 4 + 8, len4) || len4 > raw.size() - (k.s3 + len3 + 20)) return k;
@@ -1655,12 +1656,16 @@ StreamPeek peek_stream(std::span<const uint8_t> raw) {
   // (LOG records: seq u64, op u8, kind u8, u16, size u64, id u64, addr u64)
   for (uint64_t at = h2 + 16; at + kLogRecordBytes <= h2 + 16 + len2; at += kLogRecordBytes) {
     const uint8_t op = raw[at + 8], kind = raw[at + 9];
-    uint64_t size = 0;
+    if (op != uint8_t(LogOp::Alloc)) continue;
+    uint64_t size = 0, addr = 0;
     std::memcpy(&size, raw.data() + at + 12, 8);
-    if (op == uint8_t(LogOp::Alloc) && kind == uint8_t(AllocationKind::PinnedHost) &&
-        size >= kSkipMin)
-      k.pinned_big = true;
+    std::memcpy(&addr, raw.data() + at + 28, 8);
+    if (kind == uint8_t(AllocationKind::PinnedHost) && size >= kSkipMin) k.pinned_big = true;
+    // the highest extent any allocation ever took (the cold arena's whole map)
+    if (kind == uint8_t(AllocationKind::Device) && addr >= kArenaBase && size < (1ull << 62))
+      k.arena_hi = std::max(k.arena_hi, addr - kArenaBase + round_up_align(size));
   }
+  k.arena_hi = std::min<uint64_t>(k.arena_bytes, (k.arena_hi + (2ull << 20) - 1) & ~((2ull << 20) - 1));
   // a session must be constructible from META (DeviceContext's own checks)
   k.ok = k.arena_bytes > 0 && k.arena_bytes % kAlign == 0 && k.stream_len > 20;
   return k;
@@ -1715,18 +1720,18 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   // ... and only into an arena that is mapped before they are queued: the
   // premap's VMM calls wait for copies already queued
   // (profiles/r02/lazy_premap.txt; C2 cold restart 17.9 ms with early
-  // windows ahead of the premap, r02j).  A cold arena at most ~4x the stream
-  // is mapped whole right here, before the parse (the log is not needed to
-  // know its extent); a sparser one keeps the premap from the log and goes
-  // without early windows.
+  // windows ahead of the premap, r02j).  A cold arena is mapped right here,
+  // before the parse, up to the highest extent the LOG ever placed (a scan
+  // of its records, no parse) when that is at most ~4x the stream; a sparser
+  // one keeps the premap from the active set and goes without early windows.
   static const bool cold_fullmap = [] {
     const char* e = std::getenv("CRAC_COLD_FULLMAP");
     return !(e && e[0] == '0');
   }();
-  if (holder && !holder->device().arena_premapped() && cold_fullmap &&
-      pk.arena_bytes <= 4 * pk.stream_len + (1ull << 30)) {
+  if (holder && !holder->device().arena_premapped() && cold_fullmap && pk.arena_hi &&
+      pk.arena_hi <= 4 * pk.stream_len + (1ull << 30)) {
     try {
-      holder->device().premap(kArenaBase, pk.arena_bytes);
+      holder->device().premap(kArenaBase, pk.arena_hi);
     } catch (const Error&) {
       holder.reset();  // reported in order after the parse, if at all
     }
