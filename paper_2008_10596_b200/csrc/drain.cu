@@ -833,6 +833,20 @@ void hash_payloads_skip_pinned(DrainEngine& E, const ImagePlan& P, uint64_t c_lo
   if (at < c_hi) hash_payloads(E, P, at, c_hi, max_ctas, st, with_key);
 }
 
+// Whether the stream range [g0, g1) (a kernel range, outside every direct
+// run) holds any byte the scatter writes: content of a record with a device
+// destination (frames and host-filled content need no kernel).  `rec` walks
+// P.recs forward across calls (ranges ascend).
+bool range_needs_scatter(const ImagePlan& P, size_t& rec, uint64_t g0, uint64_t g1) {
+  const auto& R = P.recs;
+  while (rec < R.size() && R[rec].out_off + R[rec].frame_len + R[rec].len <= g0) ++rec;
+  for (size_t r = rec; r < R.size() && R[r].out_off < g1; ++r) {
+    const uint64_t c0 = R[r].out_off + R[r].frame_len, c1 = c0 + R[r].len;
+    if (R[r].ptr && R[r].len && c0 < g1 && c1 > g0) return true;
+  }
+  return false;
+}
+
 // Direct runs: the interior of every Device payload of at least
 // kDirectMinTiles + 2 tiles, cut to whole stream tiles 64 bytes clear of the
 // payload's ends, wholly below `limit`.  The copy engines move them straight
@@ -846,6 +860,11 @@ constexpr uint64_t kDirectMinTiles = 4;
 
 void plan_direct_runs(ImagePlan& P, uint64_t limit, bool drain, uint64_t from = 0) {
   P.direct_runs.clear();
+  struct Exact {
+    size_t k;
+    uint64_t a, len;  // the payload's content [a, a + len) in the stream
+  };
+  std::vector<Exact> exact;  // per direct run (refill)
   // CRAC_DIRECT = 0 | drain | refill (default) | both.  Measured on C4
   // (tools/ab_direct2.sh, 3 rounds): the refill gains with direct H2D (55.0
   // against 54.3 GB/s through the ring), the drain loses with direct D2H (54.0
@@ -861,13 +880,43 @@ void plan_direct_runs(ImagePlan& P, uint64_t limit, bool drain, uint64_t from = 
   if (enabled & (drain ? 1 : 2))
     for (size_t k = 0; k < P.pay_spans.size(); ++k) {
       if (P.pay_kind[k] != uint8_t(AllocationKind::Device)) continue;
-      const uint64_t a = P.pay_rec_off[k], b = std::min(a + P.pay_spans[k].len, limit);
+      const uint64_t a = P.pay_rec_off[k], len = P.pay_spans[k].len,
+                     b = std::min(a + len, limit);
       if (b < a + 64 + (kDirectMinTiles + 2) * kTile) continue;
-      const uint64_t lo = std::max(from, (a + 64 + kTile - 1) / kTile * kTile),
-                     hi = (b - 64) / kTile * kTile;
+      uint64_t lo = std::max(from, (a + 64 + kTile - 1) / kTile * kTile),
+               hi = (b - 64) / kTile * kTile;
       if (hi < lo + kDirectMinTiles * kTile) continue;
-      P.direct_runs.push_back(ImagePlan::DirectRun{lo, hi, P.pay_spans[k].ptr + (lo - a)});
+      P.direct_runs.push_back(ImagePlan::DirectRun{lo, hi, P.pay_spans[k].ptr + (lo - a), false});
+      if (!drain) exact.push_back({k, a, len});
     }
+  static const bool exact_runs = [] {
+    const char* e = std::getenv("CRAC_EXACT_DIRECT");
+    return !(e && e[0] == '0');
+  }();
+  if (!drain && exact_runs && !P.direct_runs.empty()) {
+    // Refill: a run may reach its payload's exact head, and its exact end when
+    // the extent has no padding (the scatter zero-fills padding), wherever the
+    // stream between it and its neighbour holds nothing the scatter writes
+    // (only frames): then no scatter is launched there at all (C4: the
+    // windows of big payloads need none).  Gaps the scatter does handle keep
+    // tile-aligned boundaries (the scatter's window offsets are tile-aligned).
+    auto& D = P.direct_runs;
+    for (size_t i = 0; i < D.size(); ++i)  // heads: the gap before ends at a frame
+      if (exact[i].a >= from) {
+        D[i].dev -= D[i].lo - exact[i].a;
+        D[i].lo = exact[i].a;
+      }
+    size_t rec = 0;
+    for (size_t i = 0; i < D.size(); ++i) {  // ends: only before a frame-only gap
+      const uint64_t end = exact[i].a + exact[i].len;
+      if (round_up_align(exact[i].len) != exact[i].len || end > limit) continue;
+      const uint64_t next = i + 1 < D.size() ? D[i + 1].lo : P.stream_len;
+      if (end <= next && !range_needs_scatter(P, rec, end, next)) {
+        D[i].hi = end;
+        D[i].exact_end = true;
+      }
+    }
+  }
   P.skip_runs.clear();
   P.skip_runs.reserve(P.host_runs.size() + P.direct_runs.size());
   for (const auto& d : P.direct_runs) P.skip_runs.emplace_back(d.lo, d.hi);
@@ -915,10 +964,13 @@ void copy_direct(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, ui
   for (; run < D.size() && D[run].lo < end; ++run) {
     const auto& d = D[run];
     // refill: through the end of the destination word straddling `hi` (the
-    // scatter writes only words that start outside the run)
-    const uint64_t hi = d2h ? d.hi : d.hi + 15;
-    for (uint64_t c = d.lo; c < hi; c += kPiece) {
-      const uint64_t n = std::min(kPiece, hi - c);
+    // scatter writes only words that start outside the run), unless `hi` is
+    // the payload's exact end
+    const uint64_t hi = d2h || d.exact_end ? d.hi : d.hi + 15;
+    for (uint64_t c = d.lo, n = 0; c < hi; c += n) {
+      // an exact (unaligned) head goes first on its own, so the big pieces
+      // read / write page-aligned image addresses
+      n = c % kTile ? std::min(hi, (c / kTile + 1) * kTile) - c : std::min(kPiece, hi - c);
       uint8_t* dev = reinterpret_cast<uint8_t*>(d.dev + (c - d.lo));
       const cudaError_t e = d2h ? cudaMemcpyAsync(stream + c, dev, n, cudaMemcpyDeviceToHost, st)
                                 : cudaMemcpyAsync(dev, stream + c, n, cudaMemcpyHostToDevice, st);
@@ -1893,7 +1945,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   }
   tr.mark("premap");
 
-  uint64_t windows = 0, verifies = 0, scattered = 0;
+  uint64_t windows = 0, verifies = 0, scattered = 0, scatter_launches = 0;
   // enqueues H2D windows -> scatter -> K1 verify (payloads as their regions
   // complete, then the device-resident pages); nothing here waits
   auto enqueue_data_path = [&] {
@@ -1904,7 +1956,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     windows = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
     if (stats) E.ensure_window_events(windows);
     if (!n_spec) check_cuda(cudaEventRecord(E.ev_c0, E.s_copy), "event");
-    size_t spans_done = 0, run_i = 0, krun_i = 0, drun_i = 0;
+    size_t spans_done = 0, run_i = 0, krun_i = 0, drun_i = 0, srec_i = 0;
     std::vector<std::pair<uint64_t, uint64_t>> kr;
     constexpr uint64_t kVerifyBatch = 32768;  // 2 GiB of 64 KiB chunks: big enough to keep
                                               // K1 efficient beside the H2D; the tail
@@ -1928,6 +1980,8 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       if (stats) cudaEventRecord(E.ev_w0[w], E.s_pack);
       kernel_ranges(P, krun_i, off, off + len, kr);
       for (const auto& [g0, g1] : kr) {
+        if (!range_needs_scatter(P, srec_i, g0, g1)) continue;
+        ++scatter_launches;
         check_cuda(cudaError_t(crac_scatter_records(E.d_recs.ptr, uint32_t(P.recs.size()),
                                                     E.d_tile_rec.ptr + g0 / CRAC_TILE_BYTES,
                                                     buf + (g0 - off), g0, g1 - g0, E.s_pack)),
@@ -2105,9 +2159,12 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     stats->total_ms = host_pre_ms + elapsed(E.ev_t0, E.ev_t1);
     if (windows) {
       stats->copy_ms = elapsed(E.ev_c0, E.ev_c1);
-      stats->pack_launches = windows;
+      stats->pack_launches = scatter_launches;
       stats->pack_bytes = scattered;
-      stats->pack_ms = median_window_ms(E, windows);
+      // mean per scatter launch (windows of direct runs only launch none)
+      double win_ms = 0;
+      for (uint64_t w = 0; w < windows; ++w) win_ms += elapsed(E.ev_w0[w], E.ev_w1[w]);
+      stats->pack_ms = scatter_launches ? win_ms / double(scatter_launches) : 0.0;
       // the early windows carried the host-run bytes of their range too
       uint64_t early_host = 0;
       for (const auto& [lo, hi] : P.host_runs)

@@ -119,6 +119,7 @@ struct ImagePlan {
   // of stream byte `lo`.
   struct DirectRun {
     uint64_t lo, hi, dev;
+    bool exact_end = false;  // hi is the payload's last byte + 1 (no padding): no straddle
   };
   std::vector<DirectRun> direct_runs;
   std::vector<std::pair<uint64_t, uint64_t>> skip_runs;  // host ∪ direct, sorted
