@@ -1780,16 +1780,46 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     const char* e = std::getenv("CRAC_COLD_FULLMAP");
     return !(e && e[0] == '0');
   }();
+  // The cold map runs on a thread while the early windows are queued and the
+  // image parsed, for arenas up to 16 GiB (C2: cold restart 11.5-12.8 ->
+  // 10.6 ms); a bigger map beside the copies measured ~20 ms slower than
+  // before them (C4, profiles/r02/map_beside.txt).  CRAC_MAP_BESIDE=0|1 forces.
+  static const int map_beside_env = [] {
+    const char* e = std::getenv("CRAC_MAP_BESIDE");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  const bool map_beside = map_beside_env >= 0 ? map_beside_env == 1 : pk.arena_hi <= (16ull << 30);
+  std::thread map_thread;
+  std::exception_ptr map_err;
+  bool mapping = false;
   if (holder && !holder->device().arena_premapped() && cold_fullmap && pk.arena_hi &&
       pk.arena_hi <= 4 * pk.stream_len + (1ull << 30)) {
-    try {
-      holder->device().premap(kArenaBase, pk.arena_hi);
-    } catch (const Error&) {
-      holder.reset();  // reported in order after the parse, if at all
+    if (map_beside) {
+      mapping = true;
+      map_thread = std::thread([&, dev = holder->drain_engine().device] {
+        try {
+          cudaSetDevice(dev);
+          holder->device().premap(kArenaBase, pk.arena_hi);
+        } catch (...) {
+          map_err = std::current_exception();
+        }
+      });
+    } else {
+      try {
+        holder->device().premap(kArenaBase, pk.arena_hi);
+      } catch (const Error&) {
+        holder.reset();  // reported in order after the parse, if at all
+      }
     }
     tr.mark("fullmap");
   }
-  if (holder && !holder->device().arena_premapped()) {
+  struct MapJoin {
+    std::thread& t;
+    ~MapJoin() {
+      if (t.joinable()) t.join();
+    }
+  } map_join{map_thread};
+  if (holder && !mapping && !holder->device().arena_premapped()) {
     // keep the session; no early windows
   } else if (holder) {
     DrainEngine& e = holder->drain_engine();
@@ -1811,8 +1841,18 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   try {
     p = parse_image(raw, /*verify_bulk=*/false);
   } catch (...) {
+    if (map_thread.joinable()) map_thread.join();
     if (holder) cudaStreamSynchronize(holder->drain_engine().s_copy);
     throw;
+  }
+  if (map_thread.joinable()) {
+    map_thread.join();
+    tr.mark("map-join");
+    if (map_err) {  // reported in order below, if at all
+      cudaStreamSynchronize(holder->drain_engine().s_copy);
+      holder.reset();
+      n_spec = 0;
+    }
   }
   tr.mark("parse");
   if (holder && (p.meta.seed != pk.seed || p.meta.arena_bytes != pk.arena_bytes ||
