@@ -6,7 +6,9 @@
                     then the fused form (CRAC_FORCE_FUSED=1 in a 2nd process)
   stall-reduced     K1 hash+copy (mode 2/3) into the shadow, shadow D2H
   pre-copy          K1 hash+copy into the pinned image, incremental finish
-  restart           H2D + k_scatter_records + K1 verify (CRC only, paired)
+  restart           H2D + k_scatter_records + K1 verify (CRC only, paired),
+                    cold: early windows, exact-end direct runs, verify_synth
+  deflate           K5 segments + gather
   managed / pinned  UVM page hashing, host-resident pages, pinned payloads
 
 Exits nonzero on any mismatch against a plain full drain.
@@ -55,11 +57,26 @@ def main():
     s.checkpoint_precopy_finish()
     want2, _ = s.checkpoint()
     assert img.tobytes() == want2, "pre-copy != full"
-    # restart: scatter + verify
+    # restart: scatter + verify; then the same cold, alone (fixed VA: the
+    # early ring windows, exact-end direct runs, threaded map and replay)
     r, _ = engine.restart(want2)
     assert r.checkpoint()[0] == want2, "restart round trip"
     r.close()
     s.close()
+    engine.drop_arena_cache()
+    big = engine.Session(seed=8, arena_bytes=256 * MIB)
+    workloads.build_regions(big, 5, lambda r: (1 + r) * 8 * MIB, 8)
+    bimg, _ = big.checkpoint()
+    big.close()
+    engine.drop_arena_cache()
+    r, _ = engine.restart(bimg)
+    assert r.checkpoint()[0] == bimg, "cold restart round trip"
+    assert r.verify_synthetic(8)["bad_allocations"] == 0, "verify kernel"
+    r.close()
+    # K5: the GPU deflate (compressible and incompressible segments)
+    z, _ = engine.compress_image_gpu(bimg[: 3 * MIB] + bytes(2 * MIB))
+    import zlib
+    assert zlib.decompress(z[16:]) == bimg[: 3 * MIB] + bytes(2 * MIB), "deflate"
     # managed (split residence) + pinned payloads + a random session
     m = engine.Session(seed=2, arena_bytes=16 * MIB)
     i, _ = m.alloc(engine.MANAGED, 3 * MIB + 123)
