@@ -2258,7 +2258,12 @@ void incremental_locked(Session& session, PinnedImage& image, DrainStats* stats)
     const char* e = std::getenv("CRAC_INCR_SPLIT");
     return !(e && !std::strcmp(e, "0"));
   }();
-  const uint32_t writers = uint32_t(std::max(1, std::min(16, E.sm_count / 8)));
+  static const int writers_env = [] {
+    const char* e = std::getenv("CRAC_INCR_WRITERS");
+    return e ? std::atoi(e) : 0;
+  }();
+  const uint32_t writers =
+      uint32_t(writers_env > 0 ? writers_env : std::max(1, std::min(16, E.sm_count / 8)));
   E.d_counters.ensure(5);
   check_cuda(cudaMemsetAsync(E.d_counters.ptr, 0, 40, E.s_pack), "counters");
   if (split) E.d_dirty_idx.ensure(n + uint64_t(writers) * 16 + 1);

@@ -386,6 +386,7 @@ struct HashDrain {
   unsigned long long* queue;
   unsigned long long* qctl;
   uint32_t n_writers;
+  uint32_t bulk_writers;  // 1: writers move chunks with cp.async.bulk (TMA) where aligned
 };
 
 
@@ -416,6 +417,61 @@ __device__ __forceinline__ void chunk_to_host(uint8_t* dst, const uint8_t* src, 
   for (uint32_t i = h + 16 * body + lane; i < len; i += 32) dst[i] = src[i];
 }
 
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+// Bulk shared -> global copy (TMA engine; global may be pinned host memory
+// through UVA) in the CTA's bulk group, and its completion waits.
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_le1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// One dirty chunk through the copy engine of the SM (cp.async.bulk): HBM ->
+// this warp's two staging buffers -> pinned image, lane 0 issuing, the store
+// of one piece overlapping the load of the next.  Needs 16-byte-aligned
+// source, destination and length.
+constexpr uint32_t kWriterPiece = 3584;  // x2 per warp x 16 warps + barriers fit 128 KiB
+__device__ void chunk_to_host_bulk(uint8_t* dst, const uint8_t* src, uint32_t len,
+                                   uint32_t stage0, uint32_t bar0, uint32_t& phase) {
+  for (uint32_t o = 0, i = 0; o < len; o += kWriterPiece, ++i) {
+    const uint32_t b = i & 1, n = min(kWriterPiece, len - o);
+    const uint32_t stage = stage0 + b * kWriterPiece, bar = bar0 + 8 * b;
+    bulk_wait_read_le1();  // the store that last read this buffer is done with it
+    mbar_expect_tx(bar, n);
+    bulk_g2s(stage, src + o, n, bar);
+    mbar_wait(bar, (phase >> b) & 1);
+    phase ^= 1u << b;
+    bulk_s2g(dst + o, stage, n);
+  }
+}
+
 // Split-drain writer warp: claims queue slots in order and copies each dirty
 // chunk into the image; exits once every hasher warp has finished and no
 // pushed slot is left.  Hashers never wait for writers, so the kernel cannot
@@ -423,7 +479,26 @@ __device__ __forceinline__ void chunk_to_host(uint8_t* dst, const uint8_t* src, 
 __device__ void drain_writer(const crac_span_t* __restrict__ spans,
                              const uint64_t* __restrict__ chunk_first, uint32_t n_spans,
                              uint32_t chunk_bytes, const HashDrain& hd, uint32_t hasher_warps,
-                             uint32_t lane) {
+                             uint32_t lane, bool bulk, uint32_t smem) {
+  // bulk (TMA) mode: this warp's staging buffers and mbarriers in the CTA's
+  // dynamic shared memory (writer CTAs never load the CRC tables)
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t stage0 = smem + warp * 2 * kWriterPiece;
+  const uint32_t bar0 = smem + kK1Warps * 2 * kWriterPiece + warp * 16;
+  uint32_t phase = 0;
+  if (bulk && lane == 0) {
+    mbar_init(bar0, 1);
+    mbar_init(bar0 + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  struct Drain {
+    bool on;
+    uint32_t lane;
+    __device__ ~Drain() {
+      if (on && lane == 0) bulk_wait_all();  // staging must outlive its stores
+    }
+  } drain_guard{bulk, lane};
   for (;;) {
     unsigned long long slot = 0;
     if (lane == 0) slot = atomicAdd(&hd.qctl[1], 1ull);
@@ -454,8 +529,14 @@ __device__ void drain_writer(const crac_span_t* __restrict__ spans,
     const uint64_t off = (c - __ldg(chunk_first + s)) * chunk_bytes;
     const uint64_t rem = sp.len - off;
     const uint32_t len = rem < chunk_bytes ? uint32_t(rem) : chunk_bytes;
-    chunk_to_host(hd.host + hd.dst_off[s] + off, reinterpret_cast<const uint8_t*>(sp.ptr + off), len,
-                  lane);
+    uint8_t* dst = hd.host + hd.dst_off[s] + off;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(sp.ptr + off);
+    if (bulk && ((reinterpret_cast<uint64_t>(dst) | reinterpret_cast<uint64_t>(src) | len) & 15) == 0) {
+      if (lane == 0) chunk_to_host_bulk(dst, src, len, stage0, bar0, phase);
+      __syncwarp();
+    } else {
+      chunk_to_host(dst, src, len, lane);
+    }
   }
 }
 
@@ -472,22 +553,22 @@ __global__ void __launch_bounds__(kK1Threads, 1)
                  uint32_t* __restrict__ out, uint32_t* __restrict__ out_key, uint32_t k_full,
                  HashDrain hd) {
   extern __shared__ __align__(16) uint32_t s_tab[];
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(g_tab);
-    uint4* dst = reinterpret_cast<uint4*>(s_tab);
-    for (uint32_t i = threadIdx.x; i < kTabWords / 4; i += kK1Threads) dst[i] = src[i];
-  }
-  __syncthreads();
-
   const uint32_t lane = threadIdx.x & 31;
   // split drain: the writers are the LAST n_wr CTAs, so hashers (which never
   // wait) are dispatched first; a writer only spins once every hasher CTA
   // has been placed (crac_hash_drain_split checks they all fit at once)
   const uint32_t n_wr = kMode == 4 ? hd.n_writers : 0;
   if (kMode == 4 && blockIdx.x >= gridDim.x - n_wr) {
-    drain_writer(spans, chunk_first, n_spans, chunk_bytes, hd, (gridDim.x - n_wr) * kK1Warps, lane);
+    drain_writer(spans, chunk_first, n_spans, chunk_bytes, hd, (gridDim.x - n_wr) * kK1Warps, lane,
+                 hd.bulk_writers != 0, static_cast<uint32_t>(__cvta_generic_to_shared(s_tab)));
     return;
   }
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(g_tab);
+    uint4* dst = reinterpret_cast<uint4*>(s_tab);
+    for (uint32_t i = threadIdx.x; i < kTabWords / 4; i += kK1Threads) dst[i] = src[i];
+  }
+  __syncthreads();
   const LaneLut lut = make_lut(static_cast<uint32_t>(__cvta_generic_to_shared(s_tab)), lane);
   const uint64_t gw = blockIdx.x * uint64_t(kK1Warps) + (threadIdx.x >> 5);
   const uint64_t tw = (gridDim.x - n_wr) * uint64_t(kK1Warps);
@@ -674,27 +755,6 @@ __global__ void __launch_bounds__(kK1Threads, 1)
 // word costs one extra LDS.128 on the shared-memory pipe the lookups already
 // keep busy.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -1326,6 +1386,19 @@ int sm_count() {
   return n;
 }
 
+// The split drain's writers move 16-byte-aligned dirty chunks with
+// cp.async.bulk (TMA: HBM -> shared -> pinned image), unaligned ones with SM
+// stores.  C5 at 64 GiB: 1/5/25 % dirty 13.6 / 66.6 / 331.5 ms against 13.9 /
+// 68.8 / 342 ms with SM stores for all (profiles/r02/tma_writers.txt).
+// CRAC_WRITER_TMA=0 turns it off.
+bool bulk_writers_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CRAC_WRITER_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool getenv_flag(const char* name) {
   const char* e = std::getenv(name);
   return e && e[0] && e[0] != '0';
@@ -1512,7 +1585,7 @@ int crac_hash_drain_split(const crac_span_t* d_spans, const uint64_t* d_chunk_fi
       d_spans, d_chunk_first, n_spans, chunk_bytes, c_lo, c_hi, d_crc, d_key,
       k_full_for(chunk_bytes),
       HashDrain{d_crc_prev, d_key_prev, d_dst_off, host_image, d_counters, d_queue, d_counters + 2,
-                n_writers});
+                n_writers, bulk_writers_enabled() ? 1u : 0u});
   return int(cudaGetLastError());
 }
 

@@ -385,7 +385,8 @@ def test_forged_crc_collision_is_resent_with_keys(eng, split):
 
 
 @pytest.mark.parametrize("env", [{"CRAC_FORCE_FUSED": "1"}, {"CRAC_K1_PAIR": "0"},
-                                 {"CRAC_K1_PAIR": "8"}], ids=["fused", "one-chain", "pair8-key"])
+                                 {"CRAC_K1_PAIR": "8"}, {"CRAC_WRITER_TMA": "0"}],
+                         ids=["fused", "one-chain", "pair8-key", "sm-store-writers"])
 def test_alternative_kernel_selections_drain_the_same_bytes(env):
     """The fallbacks behind the defaults (the fused incremental drain the
     split one falls back to when its grid cannot be co-resident; the
