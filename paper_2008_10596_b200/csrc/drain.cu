@@ -1379,7 +1379,16 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   check_cuda(cudaStreamWaitEvent(E.s_hash, E.ev_ready[0], 0), "wait");
   check_cuda(cudaStreamWaitEvent(E.s_shadow, E.ev_ready[0], 0), "wait");
   // K1 on all but kPackSMs SMs: the pack kernels never queue behind it
-  const uint32_t k1_ctas = uint32_t(std::max(1, E.sm_count - DrainEngine::kPackSMs));
+  // CRAC_K1_WAVES=n: K1 on every SM in n waves of CTAs (the high-priority
+  // pack takes SMs as K1 CTAs retire) instead of all but kPackSMs SMs in one
+  // persistent wave.  4 waves: K1 in situ 0.93 of HBM against 0.82-0.85, but
+  // the drain 0.5 % slower (profiles/r02/k1_waves.txt): off by default
+  static const int k1_waves = [] {
+    const char* e = std::getenv("CRAC_K1_WAVES");
+    return e ? std::atoi(e) : 0;
+  }();
+  const uint32_t k1_ctas = k1_waves > 0 ? uint32_t(k1_waves * E.sm_count)
+                                        : uint32_t(std::max(1, E.sm_count - DrainEngine::kPackSMs));
   check_cuda(cudaEventRecord(E.ev_h0, E.s_hash), "event");
   if (fused) {
     const bool aligned = std::all_of(P.pay_rec_off.begin(), P.pay_rec_off.end(),

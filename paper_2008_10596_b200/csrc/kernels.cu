@@ -1470,7 +1470,9 @@ int crac_chunk_key_range(const crac_span_t* d_spans, const uint64_t* d_chunk_fir
   if (int rc = crac_gpu_init()) return rc;
   const uint64_t warps_needed = c_hi - c_lo;
   uint64_t blocks = (warps_needed + kK1Warps - 1) / kK1Warps;
-  const uint64_t cap = max_ctas ? std::min<uint64_t>(max_ctas, sm_count()) : sm_count();
+  // max_ctas may exceed the SM count: K1 then runs in waves of CTAs, so SMs
+  // free up for higher-priority streams (the drain's pack) as CTAs retire
+  const uint64_t cap = max_ctas ? max_ctas : sm_count();
   if (blocks > cap) blocks = cap;
   // prefetch depth: 16 rows in flight for 64 KiB chunks; 8 for 4 KiB pages
   // (one batch covers the page, so remote host-resident pages are read with
