@@ -1778,10 +1778,11 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       holder.reset();  // whatever failed is reported in order, after the parse
     }
   }
-  // ... and only into an arena that is mapped before they are queued: the
-  // premap's VMM calls wait for copies already queued
-  // (profiles/r02/lazy_premap.txt; C2 cold restart 17.9 ms with early
-  // windows ahead of the premap, r02j).  A cold arena is mapped right here,
+  // ... and only into an arena whose map is under way before the parse: the
+  // premap from the parsed log behind early windows was slow (C2 cold
+  // restart 17.9 ms, r02j; it mapped 16 k extents in many runs, and many
+  // small handles cost far more than one, profiles/r02/probe_vmm.txt).  A
+  // cold arena is mapped right here,
   // before the parse, up to the highest extent the LOG ever placed (a scan
   // of its records, no parse) when that is at most ~4x the stream; a sparser
   // one keeps the premap from the active set and goes without early windows.
@@ -1943,9 +1944,10 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   // extents touch, in address order (first fit hands out low addresses
   // again after frees, so id order is not address order), without
   // sorting the extents (C2: 16 k); one-block gaps are bridged.  Mapping in
-  // pieces interleaved with the windows' H2D was measured slower (C4 cold
-  // restart 2681 vs 2462 ms, profiles/r02/lazy_premap.txt): the VMM calls
-  // wait for the copies already queued.
+  // 1 GiB pieces interleaved with the windows' H2D was measured slower (C4
+  // cold restart 2681 vs 2462 ms, profiles/r02/lazy_premap.txt): 120 handles
+  // cost far more than one (profiles/r02/probe_vmm.txt), and the enqueue
+  // loop waited on them.
   {
     constexpr uint64_t kBlock = 2ull << 20;
     std::vector<uint8_t> need((cfg.arena_bytes + kBlock - 1) / kBlock, 0);
