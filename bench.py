@@ -18,7 +18,9 @@ e2e    = same bytes / sum over steps of (max over ranks of the CUDA-event
          interval around the step through the public C-ABI: host image
          buffers, session teardown and arena release included)
 The restart is cold: the closed session's arena is freed before each refill,
-as in a new process.  With N > 1 ranks every drain meets the other ranks at
+as in a new process (its VA at once; its physical memory is released on a
+thread beside the refill's first copies, and the refill's arena map waits for
+that release -- CRAC_SYNC_RELEASE=1 releases it before the refill instead).  With N > 1 ranks every drain meets the other ranks at
 the product's global-checkpoint barrier (crac_barrier, crac_engine.h).
 `--gpus N` outside torchrun spawns the N ranks itself; `--dry-run` runs the
 rank plumbing only (no GPU).
@@ -36,6 +38,8 @@ import sys
 import threading
 import time
 from pathlib import Path
+
+SYNC_RELEASE = os.environ.get("CRAC_SYNC_RELEASE") == "1"
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
@@ -871,7 +875,7 @@ def main() -> None:
         t0 = time.perf_counter()
         s.close()
         t1 = time.perf_counter()
-        engine.drop_arena_cache()
+        engine.drop_arena_cache(release_later=not SYNC_RELEASE)
         teardown.append(((t1 - t0) * 1e3, (time.perf_counter() - t1) * 1e3))
         s2, rf = engine.restart_from_address(addr, n)
         if gbar:
@@ -1057,7 +1061,10 @@ def main() -> None:
                        **cfg_extra, "parallelism": f"independent drains x{world}",
                        "global_barrier": "crac_barrier (shared memory) at quiesce-complete and "
                                          "image-complete of every drain" if world > 1 else None,
-                       "restart": "cold: the closed session's arena is freed before each refill",
+                       "restart": ("cold: the closed session's arena is freed before each refill"
+                                   + ("" if SYNC_RELEASE else
+                                      " (its physical release overlaps the refill's first copies;"
+                                      " the refill's arena map waits for it)")),
                        "l2": "inputs larger than L2" if live > 256 * MIB else "inputs may fit L2"},
             "per_gpu": {"checkpoint_GBps": round(live / (drain_ms * 1e-3) / 1e9, 3),
                         "restart_GBps": round(live / (refill_ms * 1e-3) / 1e9, 3),

@@ -251,6 +251,13 @@ int crac_peek_cuda_error(void);
  * then maps its physical memory afresh, as in a new process (a cold restart). */
 int crac_drop_arena_cache(int device);
 
+/* As crac_drop_arena_cache, but only the VA is freed before returning: the
+ * physical memory is released on a background thread, and a restart that
+ * needs it (its arena map) waits for that release, so the release overlaps
+ * the restart's first H2D copies.  crac_drop_arena_cache on the device waits
+ * for releases in flight. */
+int crac_drop_arena_cache_async(int device);
+
 /* Host CRC-32 the engine uses for host-resident pages and small sections
  * (zlib's crc32, bit-identical; PCLMUL folding).  No GPU needed. */
 uint32_t crac_crc32_host(const void* data, uint64_t n, uint32_t crc);

@@ -500,6 +500,14 @@ int crac_drop_arena_cache(int device) {
   });
 }
 
+int crac_drop_arena_cache_async(int device) {
+  return guard([&] {
+    int dev = device;
+    if (dev < 0) check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    drop_arena_cache(dev, /*release_later=*/true);
+  });
+}
+
 uint32_t crac_crc32_host(const void* data, uint64_t n, uint32_t crc) {
   return codec::crc32_fast(static_cast<const uint8_t*>(data), n, crc);
 }

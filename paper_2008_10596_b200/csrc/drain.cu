@@ -1769,6 +1769,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     host_pre_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_entry).count();
   };
+  constexpr uint64_t kColdHeadDefault = 8ull << 30;
   // (only without managed pages: the early windows would carry the host
   // runs the H2D otherwise skips, and a UVM refill is not link-bound)
   if (pk.ok && pk.len4 == 0 && !pk.pinned_big) {
@@ -1799,9 +1800,22 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
   const bool map_beside = map_beside_env >= 0 ? map_beside_env == 1 : pk.arena_hi <= (16ull << 30);
+  // A bigger cold arena is mapped as two handles: its first `head` bytes
+  // before the copies, the rest on a thread while the windows bound for the
+  // head stream in (the enqueue joins it before the first window whose
+  // destinations lie beyond; VMM calls do not wait for copies in flight,
+  // profiles/r02/probe_vmm.txt).  CRAC_COLD_HEAD_MIB sets the head (0: one
+  // handle, mapped before the copies).
+  static const uint64_t cold_head_env = [] {
+    const char* e = std::getenv("CRAC_COLD_HEAD_MIB");
+    return e ? uint64_t(std::strtoull(e, nullptr, 10)) << 20 : kColdHeadDefault;
+  }();
+  const uint64_t cold_head = (cold_head_env & ~((2ull << 20) - 1));
   std::thread map_thread;
   std::exception_ptr map_err;
   bool mapping = false;
+  bool deferred_map = false;  // the tail of the arena is being mapped by map_thread
+  uint64_t map_head = 0;      // bytes of the arena mapped before the copies when deferred
   if (holder && !holder->device().arena_premapped() && cold_fullmap && pk.arena_hi &&
       pk.arena_hi <= 4 * pk.stream_len + (1ull << 30)) {
     if (map_beside) {
@@ -1816,20 +1830,46 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       });
     } else {
       try {
-        holder->device().premap(kArenaBase, pk.arena_hi);
+        const bool split = cold_head && pk.arena_hi >= 2 * cold_head;
+        map_head = split ? cold_head : pk.arena_hi;
+        holder->device().premap(kArenaBase, map_head);
+        if (split) {
+          deferred_map = true;
+          map_thread = std::thread([&, dev = holder->drain_engine().device] {
+            try {
+              cudaSetDevice(dev);
+              holder->device().premap(kArenaBase + map_head, pk.arena_hi - map_head);
+            } catch (...) {
+              map_err = std::current_exception();
+            }
+          });
+        }
       } catch (const Error&) {
         holder.reset();  // reported in order after the parse, if at all
       }
     }
     tr.mark("fullmap");
   }
+  // joins the deferred tail map; the engine streams drain before an error
+  // unwinds the session (the arena they write into is unmapped with it)
+  auto join_tail_map = [&] {
+    if (!deferred_map) return;
+    map_thread.join();
+    deferred_map = false;
+    tr.mark("tail-map-join");
+    if (map_err) {
+      cudaStreamSynchronize(holder->drain_engine().s_copy);
+      cudaStreamSynchronize(holder->drain_engine().s_pack);
+      std::rethrow_exception(map_err);
+    }
+  };
   struct MapJoin {
     std::thread& t;
     ~MapJoin() {
       if (t.joinable()) t.join();
     }
   } map_join{map_thread};
-  if (holder && !mapping && !holder->device().arena_premapped()) {
+  if (holder && !mapping && !deferred_map && !holder->device().arena_premapped()) {
     // keep the session; no early windows
   } else if (holder) {
     DrainEngine& e = holder->drain_engine();
@@ -1855,7 +1895,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     if (holder) cudaStreamSynchronize(holder->drain_engine().s_copy);
     throw;
   }
-  if (map_thread.joinable()) {
+  if (map_thread.joinable() && !deferred_map) {
     map_thread.join();
     tr.mark("map-join");
     if (map_err) {  // reported in order below, if at all
@@ -1868,6 +1908,10 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   if (holder && (p.meta.seed != pk.seed || p.meta.arena_bytes != pk.arena_bytes ||
                  p.sec[2].payload_off != pk.s3)) {
     // (cannot happen for an image the parse accepts; kept as a guard)
+    if (deferred_map) {
+      map_thread.join();
+      deferred_map = false;
+    }
     cudaStreamSynchronize(holder->drain_engine().s_copy);
     holder.reset();
     n_spec = 0;
@@ -1986,6 +2030,10 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       const char* e = std::getenv("CRAC_PREMAP_SINGLE");
       return !(e && e[0] == '0');
     }();
+    // the deferred tail map covers every extent up to pk.arena_hi (the
+    // highest the log placed); anything beyond waits for it
+    if (deferred_map && !runs.empty() && runs.back().second * kBlock > pk.arena_hi) join_tail_map();
+    if (deferred_map) runs.clear();
     if (single && !ctx.arena_premapped() && runs.size() > 8 &&
         4 * touched >= 3 * (runs.back().second - runs.front().first))
       runs = {{runs.front().first, runs.back().second}};
@@ -2007,6 +2055,17 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     windows = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
     if (stats) E.ensure_window_events(windows);
     if (!n_spec) check_cuda(cudaEventRecord(E.ev_c0, E.s_copy), "event");
+    // while the tail map runs: the stream prefix whose records all land in
+    // the mapped head (the first record with arena bytes beyond it ends it)
+    uint64_t head_safe_end = ~0ull;
+    if (deferred_map) {
+      const uint64_t lo = kArenaBase, hi = kArenaBase + cfg.arena_bytes;
+      for (const crac_record_t& r : P.recs)
+        if (r.ptr >= lo && r.ptr < hi && r.ptr + std::max(r.len, r.ext) > kArenaBase + map_head) {
+          head_safe_end = r.out_off;
+          break;
+        }
+    }
     size_t spans_done = 0, run_i = 0, krun_i = 0, drun_i = 0, srec_i = 0;
     std::vector<std::pair<uint64_t, uint64_t>> kr;
     constexpr uint64_t kVerifyBatch = 32768;  // 2 GiB of 64 KiB chunks: big enough to keep
@@ -2018,6 +2077,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       const uint64_t off = w * DrainEngine::kWindow;
       const uint64_t len = std::min(DrainEngine::kWindow, P.stream_len - off);
       const uint64_t with_ahead = std::min(len + 16, P.stream_len - off);
+      if (deferred_map && off + with_ahead > head_safe_end) join_tail_map();
       if (w >= n_spec) {  // (the early windows are in their slots already)
         if (w >= uint64_t(DrainEngine::kSlots))
           check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_free[slot], 0), "wait");
@@ -2062,6 +2122,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       }
     }
     check_cuda(cudaEventRecord(E.ev_c1, E.s_copy), "event");
+    join_tail_map();  // (every record fit in the head)
     if (P.n_dev_pages) {
       if (stats) {
         E.ensure_verify_events(verifies + 1);
@@ -2117,6 +2178,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     std::rethrow_exception(replay_err);
   }
   tr.mark("replay");
+  join_tail_map();  // (when the data path had nothing to wait for it)
   if (ctx.live_stream_ids() != p.streams) {
     quiet();
     raise(Errc::ReplayDivergence, "live streams after replay do not match the snapshot");

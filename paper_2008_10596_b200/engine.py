@@ -126,6 +126,7 @@ _SIGS = {
     "crac_barrier_close": (None, [_P, C.c_int]),
     "crac_peek_cuda_error": (C.c_int, []),
     "crac_drop_arena_cache": (C.c_int, [C.c_int]),
+    "crac_drop_arena_cache_async": (C.c_int, [C.c_int]),
     "crac_stream_handle": (C.c_int, [_P, _U64, C.POINTER(_P)]),
     "crac_live_streams": (C.c_int, [_P, _U64, _PU64, _PU64]),
     "crac_gate_enter": (C.c_int, [_P]),
@@ -643,10 +644,16 @@ def read_file(path, threads: int = 0, chunk_bytes: int = 0, direct: bool = True,
     return _bytes_at(base, got.value), io.as_dict()
 
 
-def drop_arena_cache(device: int = -1) -> None:
+def drop_arena_cache(device: int = -1, release_later: bool = False) -> None:
     """Frees the arena a closed session left cached on `device`: the next
-    restart maps its memory afresh, as a restart in a new process does."""
-    _check(lib().crac_drop_arena_cache(device))
+    restart maps its memory afresh, as a restart in a new process does.
+    release_later: only the VA is freed now; the physical memory is released
+    on a thread and the next restart's arena map waits for it (the release
+    overlaps the restart's first copies)."""
+    if release_later:
+        _check(lib().crac_drop_arena_cache_async(device))
+    else:
+        _check(lib().crac_drop_arena_cache(device))
 
 
 def decode_check(image) -> None:

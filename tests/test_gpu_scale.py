@@ -142,3 +142,30 @@ def test_restart_checked_against_regenerated_content(eng):
     rs, _ = eng.restart(bytes(bad))
     assert rs.verify_synthetic(1)["bad_allocations"] == 1
     rs.close()
+
+
+def test_cold_restart_two_handle_map_after_async_release(eng):
+    """A cold restart of an arena bigger than half the GPU right after
+    drop_arena_cache(release_later=True): the refill maps its head before the
+    copies and the tail on a thread that must wait for the old arena's
+    release (the two cannot coexist in HBM).  The restarted state equals the
+    regenerated content, twice over, and a synchronous drop still works."""
+    import torch
+    free, total = torch.cuda.mem_get_info()
+    n = int(total * 0.55) >> 30  # 1 GiB regions: arena > half of HBM
+    s = eng.Session(seed=5, arena_bytes=(n << 30) + n * (4 << 20))
+    workloads.build_regions(s, n, lambda r: (1 << 30) - 4096 * (r % 3), seed=5)
+    image = eng.Image()
+    try:
+        for rep in range(2):
+            s.checkpoint_into(image)
+            s.close()
+            eng.drop_arena_cache(release_later=True)
+            addr, size = image.address()
+            s, st = eng.restart_from_address(addr, size)
+            v = s.verify_synthetic(5)
+            assert v["bad_allocations"] == 0 and v["bytes_checked"] > (n - 1) << 30, (rep, v)
+        s.close()
+        eng.drop_arena_cache()  # waits for nothing in flight; frees the cached arena
+    finally:
+        image.close()

@@ -2,6 +2,7 @@
 
 * HoleIndex (O(log n) first fit) vs the reference's linear first fit with
   two-sided coalescing (ref: src/device_core.cpp:45-103).
+* RegionMap vs the reference's region table (ref: src/shim.cpp:42-88).
 """
 import subprocess
 from pathlib import Path
@@ -15,6 +16,26 @@ def test_hole_index_matches_reference_first_fit(tmp_path):
                     str(ROOT / "tests" / "native" / "hole_index_test.cpp"), "-o", str(exe)],
                    check=True)
     out = subprocess.run([str(exe), "60"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.strip() == "ok"
+
+
+def test_region_map_matches_reference_table(tmp_path):
+    """RegionMap (csrc/shim.cpp) vs the reference's region table: its own
+    test_shim.cpp cases, then random register/classify sequences against a
+    restatement of ref src/shim.cpp:42-88 (same regions, Errc, classes)."""
+    from paper_2008_10596_b200 import engine
+    if not engine.LIB_PATH.exists():
+        from paper_2008_10596_b200 import build
+        build.build()
+    exe = tmp_path / "region_map_test"
+    lib_dir = engine.LIB_PATH.parent
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", str(ROOT / "include"),
+                    "-I", "/usr/local/cuda/include",
+                    str(ROOT / "tests" / "native" / "region_map_test.cpp"), "-o", str(exe),
+                    "-L", str(lib_dir), "-lcrac_b200", f"-Wl,-rpath,{lib_dir}"],
+                   check=True)
+    out = subprocess.run([str(exe), "300"], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.strip() == "ok"
 
