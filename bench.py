@@ -18,9 +18,10 @@ e2e    = same bytes / sum over steps of (max over ranks of the CUDA-event
          interval around the step through the public C-ABI: host image
          buffers, session teardown and arena release included)
 The restart is cold: the closed session's arena is freed before each refill,
-as in a new process (its VA at once; its physical memory is released on a
-thread beside the refill's first copies, and the refill's arena map waits for
-that release -- CRAC_SYNC_RELEASE=1 releases it before the refill instead).  With N > 1 ranks every drain meets the other ranks at
+as in a new process.  (CRAC_ASYNC_RELEASE=1 frees only its VA before the
+refill and releases its memory on a thread beside it: the driver serializes
+the refill's arena map behind that release, so C4 restarts ~80 ms slower;
+profiles/r02/async_release.txt.)  With N > 1 ranks every drain meets the other ranks at
 the product's global-checkpoint barrier (crac_barrier, crac_engine.h).
 `--gpus N` outside torchrun spawns the N ranks itself; `--dry-run` runs the
 rank plumbing only (no GPU).
@@ -39,7 +40,7 @@ import threading
 import time
 from pathlib import Path
 
-SYNC_RELEASE = os.environ.get("CRAC_SYNC_RELEASE") == "1"
+SYNC_RELEASE = os.environ.get("CRAC_ASYNC_RELEASE") != "1"
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))

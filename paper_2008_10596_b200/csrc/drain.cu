@@ -86,12 +86,27 @@ PhaseTrace::~PhaseTrace() {
 // ---------------------------------------------------------------------------
 // buffers
 // ---------------------------------------------------------------------------
+// cudaMalloc that, when the device is out of memory, first frees a closed
+// session's cached arena (and waits for arena releases in flight) and retries
+static cudaError_t engine_malloc(void** p, size_t n) {
+  cudaError_t e = cudaMalloc(p, n);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+      drop_arena_cache(dev);
+      e = cudaMalloc(p, n);
+    }
+  }
+  return e;
+}
+
 template <typename T>
 void DevArray<T>::ensure(size_t n) {
   if (n <= cap) return;
   release();
   const size_t c = std::max<size_t>(n + n / 2, 64);
-  check_cuda(cudaMalloc(reinterpret_cast<void**>(&ptr), c * sizeof(T)), "cudaMalloc engine array");
+  check_cuda(engine_malloc(reinterpret_cast<void**>(&ptr), c * sizeof(T)), "cudaMalloc engine array");
   cap = c;
 }
 template <typename T>
@@ -132,7 +147,7 @@ DrainEngine::DrainEngine(int dev) : device(dev) {
   for (cudaEvent_t* e : {&ev_t0, &ev_t1, &ev_h0, &ev_h1, &ev_c0, &ev_c1})
     check_cuda(cudaEventCreate(e), "event");
   check_cuda(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev), "sm count");
-  check_cuda(cudaMalloc(&d_ring, kSlots * (kWindow + 64)), "staging ring");
+  check_cuda(engine_malloc(reinterpret_cast<void**>(&d_ring), kSlots * (kWindow + 64)), "staging ring");
   if (int rc = crac_gpu_init()) check_cuda(cudaError_t(rc), "crac_gpu_init");
 }
 
