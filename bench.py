@@ -18,10 +18,13 @@ e2e    = same bytes / sum over steps of (max over ranks of the CUDA-event
          interval around the step through the public C-ABI: host image
          buffers, session teardown and arena release included)
 The restart is cold: the closed session's arena is freed before each refill,
-as in a new process.  (CRAC_ASYNC_RELEASE=1 frees only its VA before the
-refill and releases its memory on a thread beside it: the driver serializes
-the refill's arena map behind that release, so C4 restarts ~80 ms slower;
-profiles/r02/async_release.txt.)  With N > 1 ranks every drain meets the other ranks at
+as in a new process.  A small arena (<= 16 GiB: C2) has only its VA freed
+before the refill and its memory released on a thread beside it (the public
+crac_drop_arena_cache_async), which keeps the driver's 2-130 ms release
+spikes off the step; a big one (C4) is released before the refill, because
+the driver serializes the refill's arena map behind a release in flight (C4
+~80 ms slower; profiles/r02/async_release.txt).  CRAC_ASYNC_RELEASE=0|1
+forces either.  With N > 1 ranks every drain meets the other ranks at
 the product's global-checkpoint barrier (crac_barrier, crac_engine.h).
 `--gpus N` outside torchrun spawns the N ranks itself; `--dry-run` runs the
 rank plumbing only (no GPU).
@@ -40,7 +43,7 @@ import threading
 import time
 from pathlib import Path
 
-SYNC_RELEASE = os.environ.get("CRAC_ASYNC_RELEASE") != "1"
+ASYNC_RELEASE = os.environ.get("CRAC_ASYNC_RELEASE")  # "0" | "1" | None (by arena size)
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
@@ -866,6 +869,8 @@ def main() -> None:
         return
 
     teardown = []  # host ms of (session close, arena release) per step
+    release_later = (ASYNC_RELEASE == "1" if ASYNC_RELEASE in ("0", "1")
+                     else live <= 16 * GIB)
 
     def step(s):
         """One checkpoint + restart, as a restart in a new process sees it:
@@ -876,7 +881,7 @@ def main() -> None:
         t0 = time.perf_counter()
         s.close()
         t1 = time.perf_counter()
-        engine.drop_arena_cache(release_later=not SYNC_RELEASE)
+        engine.drop_arena_cache(release_later=release_later)
         teardown.append(((t1 - t0) * 1e3, (time.perf_counter() - t1) * 1e3))
         s2, rf = engine.restart_from_address(addr, n)
         if gbar:
@@ -1063,9 +1068,8 @@ def main() -> None:
                        "global_barrier": "crac_barrier (shared memory) at quiesce-complete and "
                                          "image-complete of every drain" if world > 1 else None,
                        "restart": ("cold: the closed session's arena is freed before each refill"
-                                   + ("" if SYNC_RELEASE else
-                                      " (its physical release overlaps the refill's first copies;"
-                                      " the refill's arena map waits for it)")),
+                                   + ("; its memory released on a thread beside the refill"
+                                      " (crac_drop_arena_cache_async)" if release_later else "")),
                        "l2": "inputs larger than L2" if live > 256 * MIB else "inputs may fit L2"},
             "per_gpu": {"checkpoint_GBps": round(live / (drain_ms * 1e-3) / 1e9, 3),
                         "restart_GBps": round(live / (refill_ms * 1e-3) / 1e9, 3),
