@@ -282,6 +282,81 @@ def cpu_baseline(sample_gib: float, region: int) -> dict:
             "phases_s": {k: round(v, 3) for k, v in ph.items()}}
 
 
+def _ref_round_trip(s, live: int, sample: str) -> dict:
+    """One reference checkpoint+encode / decode+restart of session `s`."""
+    state = {"session": s}
+    ref_sample_step(state)
+    ph = state["phases"]
+    total = ph["checkpoint_s"] + ph["encode_s"] + ph["decode_s"] + ph["restart_s"]
+    state["session"].close()
+    return {"value": round(2 * live / total / 1e9, 4), "unit": "GB/s", "cores": 1,
+            "kind": "reference", "sample": sample,
+            "phases_s": {k: round(v, 3) for k, v in ph.items()}}
+
+
+def cpu_baseline_c2(calls: int) -> dict:
+    """The unmodified reference on the whole C2 workload (same call sequence
+    shape, seed 1), single-threaded by construction."""
+    from oracle import ref
+    import workloads
+    s = ref.RefSession(seed=1, arena_bytes=2 * GIB)
+    workloads.build_churn(s, calls, 1)
+    live = sum(r[2] for r in s.live_records())  # (id, kind, size, address)
+    return _ref_round_trip(s, live, f"C2 at full size ({calls} calls, {live // MIB} MiB live): "
+                                    "checkpoint()+encode_image() then decode_image()+restart() "
+                                    "of the unmodified reference, single-threaded by construction")
+
+
+def cpu_baseline_c3(sample_gib: float) -> dict:
+    """The unmodified reference on C3 scaled (256 MiB managed regions,
+    alternating 1 MiB device/host runs), single-threaded by construction."""
+    from oracle import ref
+    import workloads
+    mregion = 256 * MIB
+    n = max(1, int(sample_gib * GIB) // mregion)
+    s = ref.RefSession(seed=1, arena_bytes=n * mregion + 64 * MIB)
+    for _ in range(n):
+        i, _ = s.alloc(workloads.MANAGED, mregion)
+        s.fill_synthetic(i, 1)
+        for off in range(MIB, mregion, 2 * MIB):
+            s.page_read(i, off, MIB, workloads.HOST_SIDE)
+    return _ref_round_trip(s, n * mregion,
+                           f"C3 scaled to {n * mregion // MIB} MiB ({n} x 256 MiB managed, "
+                           "alternating 1 MiB device/host runs): checkpoint()+encode_image() then "
+                           "decode_image()+restart() of the unmodified reference, single-threaded")
+
+
+def cpu_baseline_c5(sample_gib: float) -> dict:
+    """the chunk-hash step on every host core -- zlib's crc32
+    (the reference's crc32_of) per 64 KiB chunk over a bounded sample, each
+    thread on its own slice (zlib releases the GIL)."""
+    import zlib
+    from concurrent.futures import ThreadPoolExecutor
+    threads = max(1, os.cpu_count() or 1)
+    chunk = 65536
+    buf = bytearray(os.urandom(1 << 20)) * 256  # 256 MiB (> L3), random content
+    view = memoryview(buf)
+    reps = max(1, int(sample_gib * GIB) // len(buf))
+
+    def work(t):
+        h = 0
+        for _ in range(reps):
+            for off in range(t * chunk, len(buf), threads * chunk):
+                h ^= zlib.crc32(view[off:off + chunk])
+        return h
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(work, range(threads)))
+    dt = time.perf_counter() - t0
+    hashed = reps * len(buf)
+    return {"value": round(hashed / dt / 1e9, 3), "unit": "GB/s hashed", "cores": threads,
+            "kind": "port",
+            "sample": f"{hashed // GIB} GiB ({reps} passes over a 256 MiB buffer): zlib crc32 per "
+                      f"64 KiB chunk on {threads} threads -- the host chunk-hash step the "
+                      "incremental drain's hash-only pass replaces (SURVEY 8(d) item 2)"}
+
+
 def _ref_worker(t, per, region, steps, warmup, barrier, q):
     """One host core: its own reference session (a separate process, so the
     reference's large vector allocations do not contend on one address
@@ -623,6 +698,9 @@ def run_c5(args, engine, sess, image, live, group, rank, world, peaks) -> None:
         torch, sess, image, live + 16 * len(sess.live_records()) + 20, sync_ms, args)
     if stall is not None:
         stall["precopy"] = measure_precopy(sess, image, sync_ms, args, rank)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_c5(16.0)
     if rank == 0:
         r1 = rows["1pct"]
         print(json.dumps({
@@ -633,7 +711,8 @@ def run_c5(args, engine, sess, image, live, group, rank, world, peaks) -> None:
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": WORKLOAD_NAMES["c5"], "live_bytes_per_gpu": live,
                        "chunk_bytes": 65536},
-            "incremental": rows, "stall_reduced": stall, "verified": verified}), flush=True)
+            "incremental": rows, "stall_reduced": stall, "verified": verified,
+            "cpu_baseline": cpu}), flush=True)
 
 
 def dd_ceiling(path: Path, nbytes: int, streams: int = 8) -> dict:
@@ -1035,8 +1114,13 @@ def main() -> None:
 
     # reported CPU baseline (rank 0, N = 1 only)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c4":
-        cpu = cpu_baseline(args.cpu_sample_gib, args.region_mib * MIB)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if args.workload == "c4":
+            cpu = cpu_baseline(args.cpu_sample_gib, args.region_mib * MIB)
+        elif args.workload == "c2":
+            cpu = cpu_baseline_c2(args.c2_calls)
+        elif args.workload == "c3":
+            cpu = cpu_baseline_c3(1.0)
 
     if rank == 0:
         value = 2 * live * world * args.steps / (dev_ms_max * 1e-3) / 1e9
