@@ -1,0 +1,18 @@
+# round 2aw: validation of the two-handle cold map build: full GPU suite, smoke, every workload (CPU baselines on C2/C3/C5 too)
+mkdir -p gpurun_out/r02aw
+timeout 2400 python -m pytest tests -x -q -m gpu > gpurun_out/r02aw/gputests.log 2>&1; tail -3 gpurun_out/r02aw/gputests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r02aw/smoke.log 2>&1; tail -1 gpurun_out/r02aw/smoke.log
+OUT=gpurun_out/r02aw/all bash tools/bench_all.sh > /dev/null 2>&1
+for f in gpurun_out/r02aw/all/bench_*.json; do python - "$f" <<'PY'
+import json, sys
+f = sys.argv[1]
+try:
+    d = json.loads(open(f).read().strip().splitlines()[-1])
+except Exception as e:
+    print(f, "unreadable", e); raise SystemExit
+r = d.get("roofline") or {}
+cpu = d.get("cpu_baseline") or {}
+print(f.split("/")[-1], d.get("value"), (d.get("e2e") or {}).get("value"), r.get("frac"),
+      (d.get("per_gpu") or {}).get("restart_ms"), "cpu", cpu.get("value"), cpu.get("kind"))
+PY
+done
