@@ -152,6 +152,11 @@ class ClockSampler:
         self.lines: list[str] = []
         self.proc = None
         self.t = None
+        self.first = 0  # samples before this index precede the timed region
+
+    def mark(self):
+        """The timed region starts now: earlier samples are dropped."""
+        self.first = len(self.lines)
 
     def start(self):
         try:
@@ -180,7 +185,7 @@ class ClockSampler:
             self.t.join(timeout=5)
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
+        for line in self.lines[self.first:]:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 8:
                 continue
@@ -967,14 +972,25 @@ def main() -> None:
             s2.set_barrier(gbar)
         return s2, dr, rf
 
+    # the sampler starts before the warm-up steps: nvidia-smi's own start-up
+    # (NVML init on every GPU) stalls the driver's memory-mapping calls for
+    # up to ~0.4 s, which it did inside the first timed step when started
+    # there (profiles/r02/clock_sampler.txt); only the samples taken during
+    # the timed steps are kept
+    clocks = ClockSampler() if rank == 0 and not os.environ.get("CRAC_NO_CLOCKS") else None
+    early_clocks = os.environ.get("CRAC_CLOCKS_AT", "warmup") != "timed"
+    if clocks and early_clocks:
+        clocks.start()
     t_warm = time.perf_counter()
     for _ in range(args.warmup):
         sess, _, _ = step(sess)
     warm_s = time.perf_counter() - t_warm
 
-    clocks = ClockSampler() if rank == 0 and not os.environ.get("CRAC_NO_CLOCKS") else None
     if clocks:
-        clocks.start()
+        if early_clocks:
+            clocks.mark()
+        else:
+            clocks.start()
     drains, refills, e2e_steps = [], [], []
     wall0 = time.perf_counter()
     for _ in range(args.steps):
