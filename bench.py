@@ -972,11 +972,11 @@ def main() -> None:
             s2.set_barrier(gbar)
         return s2, dr, rf
 
-    # the sampler starts before the warm-up steps: nvidia-smi's own start-up
-    # (NVML init on every GPU) stalls the driver's memory-mapping calls for
-    # up to ~0.4 s, which it did inside the first timed step when started
-    # there (profiles/r02/clock_sampler.txt); only the samples taken during
-    # the timed steps are kept
+    # the sampler starts before the warm-up steps, so nvidia-smi's own
+    # start-up (NVML init on every GPU) falls outside the timed region; only
+    # the samples taken during the timed steps are kept (measured: the slow
+    # steps some boxes show occur with no sampler at all,
+    # profiles/r02/clock_sampler.txt)
     clocks = ClockSampler() if rank == 0 and not os.environ.get("CRAC_NO_CLOCKS") else None
     early_clocks = os.environ.get("CRAC_CLOCKS_AT", "warmup") != "timed"
     if clocks and early_clocks:
