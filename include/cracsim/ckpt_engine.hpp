@@ -116,7 +116,7 @@ class PinnedImage {
 struct DrainStats {
   double total_ms = 0;       // first to last event of the operation
   double hash_ms = 0;        // K1 span (all launches)
-  double pack_ms = 0;        // pack (drain) or scatter (refill) kernels, summed
+  double pack_ms = 0;        // pack (drain) or scatter (refill) device time per launch
   double copy_ms = 0;        // D2H (drain) or H2D (refill) span
   uint64_t hash_bytes = 0;   // bytes K1 read
   uint64_t hash_launches = 0;

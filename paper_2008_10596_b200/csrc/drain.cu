@@ -458,12 +458,12 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 
 // Median duration of the first n window kernels (robust to the windows that
 // ran beside K1 at the start of a drain).
-double median_window_ms(DrainEngine& E, size_t n) {
-  std::vector<float> v;
-  for (size_t i = 0; i < n; ++i) v.push_back(elapsed(E.ev_w0[i], E.ev_w1[i]));
-  if (v.empty()) return 0;
-  std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
-  return v[v.size() / 2];
+// device time of the ring windows' pack launches, per launch
+double mean_pack_launch_ms(DrainEngine& E, size_t windows, uint64_t launches) {
+  if (!launches) return 0;
+  double t = 0;
+  for (size_t i = 0; i < windows; ++i) t += elapsed(E.ev_w0[i], E.ev_w1[i]);
+  return t / double(launches);
 }
 
 // Bulk-stream plan shared by drain and refill.  `ptr` = device-visible
@@ -880,13 +880,15 @@ void plan_direct_runs(ImagePlan& P, uint64_t limit, bool drain, uint64_t from = 
     uint64_t a, len;  // the payload's content [a, a + len) in the stream
   };
   std::vector<Exact> exact;  // per direct run (refill)
-  // CRAC_DIRECT = 0 | drain | refill (default) | both.  Measured on C4
-  // (tools/ab_direct2.sh, 3 rounds): the refill gains with direct H2D (55.0
-  // against 54.3 GB/s through the ring), the drain loses with direct D2H (54.0
-  // against 55.0), so only the refill uses them by default.
+  // CRAC_DIRECT = 0 | drain | refill | both (default).  Measured on C4: the
+  // refill gains with direct H2D (55.0 against 54.3 GB/s through the ring,
+  // round 1); the drain's direct D2H runs at the ring's speed (checkpoint
+  // 2281-2287 ms either way, profiles/r02/direct_drain.txt; round 1 measured
+  // it 2 % slower) and halves the drain's HBM traffic (no pack read + write
+  // of the payloads), so both use them.
   static const int enabled = [] {
     const char* e = std::getenv("CRAC_DIRECT");
-    if (!e) return 2;
+    if (!e) return 3;
     if (!std::strcmp(e, "0")) return 0;
     if (!std::strcmp(e, "drain")) return 1;
     if (!std::strcmp(e, "refill")) return 2;
@@ -1434,6 +1436,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
                                              E.d_tile_rec.ptr + off / CRAC_TILE_BYTES, off, len,
                                              E.d_shadow + (off - head), E.s_shadow)),
                "pack shadow");
+    ++Q.launches;
   }
 
   check_cuda(cudaEventRecord(E.ev_c0, E.s_pack), "event");
@@ -1454,6 +1457,8 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
                                                buf + (g0 - off), E.s_pack)),
                  "pack");
       Q.packed += g1 - g0;
+      ++Q.launches;
+      ++Q.ring_launches;
     }
     if (stats) cudaEventRecord(E.ev_w1[w], E.s_pack);
     check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_pack), "event");
@@ -1542,9 +1547,9 @@ void drain_finish(Session& session, DrainStats* stats) {
       stats->copy_ms = elapsed(E.ev_c0, E.ev_c1);
       stats->hash_launches = (P.pay_first.back() ? 1 : 0) + (P.n_dev_pages ? 1 : 0);
       stats->hash_bytes = hashed_bytes(P);
-      stats->pack_launches = (P.stream_len + DrainEngine::kWindow - 1) / DrainEngine::kWindow;
+      stats->pack_launches = Q.launches;  // ring + shadow
       stats->pack_bytes = Q.packed + (P.stream_len - Q.head);  // ring windows + shadow
-      stats->pack_ms = Q.windows ? median_window_ms(E, Q.windows) : 0;  // per ring window
+      stats->pack_ms = mean_pack_launch_ms(E, Q.windows, Q.ring_launches);  // per ring launch
       stats->d2h_bytes = P.stream_len - host_run_bytes(P);
       stats->shadow_bytes = P.stream_len - Q.head;
     }
