@@ -1404,8 +1404,18 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
     const char* e = std::getenv("CRAC_K1_WAVES");
     return e ? std::atoi(e) : 0;
   }();
+  // When the direct D2H copies carry nearly all of the ring part, the pack
+  // only writes frames and payload edges: K1 leaves it kPackSMsDirect SMs
+  // (CRAC_K1_SPARE_SMS overrides either count).
+  static const int spare_env = [] {
+    const char* e = std::getenv("CRAC_K1_SPARE_SMS");
+    return e ? std::atoi(e) : -1;
+  }();
+  const bool mostly_direct = head && direct_run_bytes(P) >= head - head / 32;
+  const int spare = spare_env >= 0 ? spare_env
+                                   : (mostly_direct ? DrainEngine::kPackSMsDirect : DrainEngine::kPackSMs);
   const uint32_t k1_ctas = k1_waves > 0 ? uint32_t(k1_waves * E.sm_count)
-                                        : uint32_t(std::max(1, E.sm_count - DrainEngine::kPackSMs));
+                                        : uint32_t(std::max(1, E.sm_count - spare));
   check_cuda(cudaEventRecord(E.ev_h0, E.s_hash), "event");
   if (fused) {
     const bool aligned = std::all_of(P.pay_rec_off.begin(), P.pay_rec_off.end(),

@@ -148,6 +148,7 @@ struct DrainEngine {
   static constexpr uint32_t kChunk = 65536;         // payload hash chunk
   static constexpr uint32_t kPageChunk = 4096;      // managed hash chunk (= page)
   static constexpr int kPackSMs = 16;               // SMs K1 leaves to the pack during a drain
+  static constexpr int kPackSMsDirect = 4;          // ... when direct copies carry the payloads
 
   int device = 0;
   int sm_count = 148;
