@@ -789,7 +789,8 @@ def run_file(args, engine, sess, live, group, rank, world, cfg_extra, gbar=None)
             sess.set_barrier(gbar)
         rows.append({"ckpt_s": t1 - t0, "restart_s": t3 - t2, "drain_ms": drain["total_ms"],
                      "write_ms": wio["ms"], "read_ms": rio["ms"], "refill_ms": refill["total_ms"],
-                     "direct": wio["direct"] and rio["direct"], "bytes": wio["bytes"]})
+                     "direct": wio["direct"] and rio["direct"], "bytes": wio["bytes"],
+                     "streamed": wio.get("streamed", 0)})
     rows = rows[args.warmup:]
     ck = group.max(statistics.mean(r["ckpt_s"] for r in rows))
     rs = group.max(statistics.mean(r["restart_s"] for r in rows))
@@ -846,7 +847,8 @@ def run_file(args, engine, sess, live, group, rank, world, cfg_extra, gbar=None)
         "per_gpu": {"checkpoint_to_file_GBps": round(live / ck / 1e9, 3),
                     "restart_from_file_GBps": round(live / rs / 1e9, 3),
                     "checkpoint_to_file_s": round(ck, 3), "restart_from_file_s": round(rs, 3),
-                    "phases_ms": m, "o_direct": all(r["direct"] for r in rows)},
+                    "phases_ms": m, "o_direct": all(r["direct"] for r in rows),
+                    "streamed_bytes": rows[-1]["streamed"]},
         "roofline": roof, "cpu_baseline": cpu, "gpu_deflate": gpuz}), flush=True)
 
 

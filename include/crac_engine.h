@@ -174,6 +174,7 @@ typedef struct crac_io_stats {
   uint32_t threads;   /* I/O threads */
   int32_t direct;     /* 1 if O_DIRECT */
   uint64_t bounced;   /* bytes moved through an aligned bounce buffer */
+  uint64_t streamed;  /* checkpoint_to_file: bytes written while the drain still ran */
 } crac_io_stats_t;
 /* compress: 0 none; 1 the reference's CRACSIMZ bytes (zlib compress2 level 6,
  * host, image.cpp:419-430); 2 the GPU deflate (K5): a different, valid zlib

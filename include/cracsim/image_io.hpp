@@ -34,6 +34,7 @@ struct FileIoStats {
   uint32_t threads = 0;   // I/O threads used
   bool direct = false;    // O_DIRECT was in effect
   uint64_t bounced = 0;   // bytes that went through a bounce buffer
+  uint64_t streamed = 0;  // streamed writes: bytes written while the drain still ran
 };
 
 struct FileIoOptions {
@@ -57,5 +58,45 @@ uint64_t file_bytes(const std::filesystem::path& path);
 // and capacity >= size rounded up to 4 KiB.  Returns the file size.
 uint64_t read_file_parallel(const std::filesystem::path& path, uint8_t* dst, uint64_t capacity,
                             FileIoStats* stats = nullptr, const FileIoOptions& opt = {});
+
+// Producer side of a streamed image write: the drain reports the image
+// prefix that has landed in host memory while the D2H is still running, so
+// the file write starts under the drain (checkpoint_to_file).
+struct LandSink {
+  virtual ~LandSink() = default;
+  // the image is [base, base + n); called once, before any other call
+  virtual void start(const uint8_t* base, uint64_t n) = 0;
+  // bytes the producer completes only after the stream has landed (section
+  // headers, folded CRCs): written again once every byte is final
+  virtual void rewrite(uint64_t a, uint64_t b) = 0;
+  // bytes [0, end) hold their final values, except the rewrite ranges
+  virtual void landed(uint64_t end) = 0;
+};
+
+// A parallel positional writer (the layout and O_DIRECT rules of
+// write_file_parallel) that writes each piece as soon as the producer has
+// landed it.  finish() is called once the whole image is final: the pieces
+// still waiting are written, the rewrite ranges written again (whole 4 KiB
+// blocks), the file cut to size and fdatasync'd.  Destroying an unfinished
+// writer stops its threads (the file is then incomplete).
+class StreamWriter final : public LandSink {
+ public:
+  explicit StreamWriter(const std::filesystem::path& path, const FileIoOptions& opt = {});
+  ~StreamWriter() override;
+  StreamWriter(const StreamWriter&) = delete;
+  StreamWriter& operator=(const StreamWriter&) = delete;
+
+  void start(const uint8_t* base, uint64_t n) override;
+  void rewrite(uint64_t a, uint64_t b) override;
+  void landed(uint64_t end) override;
+  // `base`/`n` must match start()'s when it was called (else it starts here)
+  void finish(const uint8_t* base, uint64_t n, FileIoStats* stats = nullptr);
+  // bytes the pieces wrote before finish() was called (streamed under the drain)
+  uint64_t early_bytes() const;
+
+ private:
+  struct State;
+  State* st_;
+};
 
 }  // namespace cracsim

@@ -78,7 +78,7 @@ void to_c(const DrainStats& d, crac_stats_t* o) {
 
 void to_c(const FileIoStats& f, crac_io_stats_t* o) {
   if (!o) return;
-  *o = crac_io_stats_t{f.ms, f.bytes, f.threads, f.direct ? 1 : 0, f.bounced};
+  *o = crac_io_stats_t{f.ms, f.bytes, f.threads, f.direct ? 1 : 0, f.bounced, f.streamed};
 }
 
 template <typename T>

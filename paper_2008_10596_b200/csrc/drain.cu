@@ -52,10 +52,17 @@
 #include <string>
 
 #include "crc_math.hpp"
+#include "cracsim/image_io.hpp"
 #include "drain_engine.hpp"
 #include "image_codec.hpp"
 
 namespace cracsim {
+
+namespace {
+thread_local LandSink* t_land_sink = nullptr;
+}  // namespace
+
+void set_land_sink(LandSink* sink) { t_land_sink = sink; }
 
 // ---------------------------------------------------------------------------
 // tracing
@@ -1358,7 +1365,14 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   const uint64_t windows = (head + W - 1) / W;
   Q.windows = windows;
   if (stats) E.ensure_window_events(windows);
-  const bool land_events = !P.host_pages.empty();
+  // a streamed file write follows the windows as they land (the image is
+  // final there except for what the host writes after the stream: the
+  // leading sections, crc3 inside the stream, crc4 and the tail)
+  LandSink* const sink = (t_land_sink && head == P.stream_len && P.host_pages.empty() &&
+                          P.pinned_runs.empty() && windows)
+                             ? t_land_sink
+                             : nullptr;
+  const bool land_events = !P.host_pages.empty() || sink;
   if (land_events) E.ensure_land_events(windows);
   // host-resident pages: hashed (all) and copied by host threads from now
   // on, beside the plan upload, K1 and the window loop (long runs at once;
@@ -1383,6 +1397,36 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
       if (t.joinable()) t.join();
     }
   } join_host{host_pass, recorded};
+  std::atomic<bool> sink_stop{false};
+  std::thread sink_pass;
+  if (sink) {
+    sink->start(img, total);
+    sink->rewrite(0, s3);
+    sink->rewrite(s3 + P.len3, s3 + P.len3 + 4);
+    sink->rewrite(s3 + P.stream_len, total);
+    sink_pass = std::thread([&, sink, img, s3, head, windows] {
+      for (uint64_t w = 0; w < windows; ++w) {
+        while (recorded.load(std::memory_order_acquire) < int64_t(w)) {
+          if (sink_stop.load(std::memory_order_relaxed)) return;
+          std::this_thread::yield();
+        }
+        if (sink_stop.load(std::memory_order_relaxed) ||
+            cudaEventSynchronize(E.ev_land[w]) != cudaSuccess)
+          return;
+        sink->landed(s3 + std::min((w + 1) * W, head));
+      }
+    });
+  }
+  struct SinkJoiner {  // (declared after join_host: runs first on unwinding)
+    std::thread& t;
+    std::atomic<bool>& stop;
+    ~SinkJoiner() {
+      if (t.joinable()) {
+        stop.store(true);
+        t.join();
+      }
+    }
+  } join_sink{sink_pass, sink_stop};
 
   // With the whole stream in the shadow, K1 copies every payload chunk to
   // its stream position right after hashing it: one HBM read of the state
@@ -1482,6 +1526,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   }
   tr.mark("enqueue");
   if (host_pass.joinable()) host_pass.join();
+  if (sink_pass.joinable()) sink_pass.join();  // every window has landed
   if (host_err) std::rethrow_exception(host_err);
   log_side.join();
   if (log_err) std::rethrow_exception(log_err);

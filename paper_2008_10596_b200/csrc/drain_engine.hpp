@@ -23,6 +23,14 @@
 
 namespace cracsim {
 
+struct LandSink;  // cracsim/image_io.hpp
+// The streamed file write that follows the next full drain on this thread
+// (checkpoint_to_file); null = none.  The drain reports the landed image
+// prefix to it when the whole stream goes through the ring windows with no
+// host-written pages; otherwise it reports nothing and the writer writes the
+// finished image.
+void set_land_sink(LandSink* sink);
+
 // Phase tracing for diagnosis: CRAC_TRACE=1 prints host-side phase times of
 // every drain / refill to stderr.
 struct PhaseTrace {

@@ -11,9 +11,11 @@
 #include <atomic>
 #include <cerrno>
 #include <chrono>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -212,6 +214,168 @@ void write_file_parallel(const std::filesystem::path& path, std::span<const uint
   }
   f.fd = -1;
   if (stats) *stats = FileIoStats{now_ms() - t0, n, std::min<uint32_t>(threads, uint32_t(std::max<uint64_t>(pieces, 1))), direct, bounced.load()};
+}
+
+// ---------------------------------------------------------------------------
+// streamed write (checkpoint_to_file under the drain)
+// ---------------------------------------------------------------------------
+struct StreamWriter::State {
+  std::filesystem::path path;
+  FileIoOptions opt;
+  Fd f;
+  bool direct = false;
+  uint64_t chunk = 0;
+  uint32_t threads = 0;
+  const uint8_t* base = nullptr;
+  uint64_t n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  uint64_t landed = 0;   // [0, landed) final except the rewrite ranges
+  bool final_all = false, stop = false, started = false;
+  std::vector<std::pair<uint64_t, uint64_t>> rewrites;
+  std::vector<std::thread> pool;
+  std::atomic<int> err{0};
+  std::atomic<uint64_t> bounced{0}, early{0};
+  double t0 = 0;
+
+  int write_range(uint64_t off, uint64_t len, std::unique_ptr<AlignedBuf>& b) {
+    if (!direct) return full_pwrite(f.fd, base + off, len, off);
+    const uint64_t padded = round_block(len);
+    if (reinterpret_cast<uintptr_t>(base + off) % kBlock == 0 && padded == len)
+      return full_pwrite(f.fd, base + off, len, off);
+    if (!b) b = std::make_unique<AlignedBuf>(chunk);
+    if (!b->p) return ENOMEM;
+    std::memcpy(b->p, base + off, len);
+    std::memset(b->p + len, 0, padded - len);
+    bounced.fetch_add(len, std::memory_order_relaxed);
+    return full_pwrite(f.fd, b->p, padded, off);
+  }
+
+  // thread t: its contiguous run of pieces, each once the producer has landed it
+  void worker(uint32_t t) {
+    const uint64_t pieces = (n + chunk - 1) / chunk;
+    std::unique_ptr<AlignedBuf> b;
+    for (uint64_t k = pieces * t / threads; k < pieces * (t + 1) / threads; ++k) {
+      const uint64_t off = k * chunk, len = std::min(chunk, n - off);
+      bool early_piece;
+      {
+        std::unique_lock lk(mu);
+        cv.wait(lk, [&] { return stop || final_all || landed >= off + len; });
+        if (stop) return;
+        early_piece = !final_all;
+      }
+      if (err.load(std::memory_order_relaxed)) return;
+      if (const int e = write_range(off, len, b)) {
+        int expected = 0;
+        err.compare_exchange_strong(expected, e);
+        return;
+      }
+      if (early_piece) early.fetch_add(len, std::memory_order_relaxed);
+    }
+  }
+
+  void halt() {
+    {
+      std::lock_guard lk(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& th : pool)
+      if (th.joinable()) th.join();
+    pool.clear();
+  }
+};
+
+StreamWriter::StreamWriter(const std::filesystem::path& path, const FileIoOptions& opt)
+    : st_(new State) {
+  State& S = *st_;
+  S.path = path;
+  S.opt = opt;
+  S.t0 = now_ms();
+  S.chunk = io_chunk(opt);
+  S.threads = io_threads(opt);
+  // in place, as write_file_parallel (no O_TRUNC; cut to size at the end)
+  S.f.fd = open_maybe_direct(path, O_WRONLY | O_CREAT, opt.direct, &S.direct);
+  if (S.f.fd < 0) {
+    const std::string why = std::strerror(errno);
+    delete st_;
+    raise(Errc::InvalidArgument, "cannot write " + path.string() + ": " + why);
+  }
+}
+
+StreamWriter::~StreamWriter() {
+  st_->halt();
+  delete st_;
+}
+
+void StreamWriter::start(const uint8_t* base, uint64_t n) {
+  State& S = *st_;
+  if (S.started) return;
+  S.started = true;
+  S.base = base;
+  S.n = n;
+  const uint64_t pieces = (n + S.chunk - 1) / S.chunk;
+  S.threads = uint32_t(std::min<uint64_t>(S.threads, std::max<uint64_t>(pieces, 1)));
+  for (uint32_t t = 0; t < S.threads && pieces; ++t) S.pool.emplace_back([&S, t] { S.worker(t); });
+}
+
+void StreamWriter::rewrite(uint64_t a, uint64_t b) {
+  std::lock_guard lk(st_->mu);
+  if (b > a) st_->rewrites.emplace_back(a, b);
+}
+
+void StreamWriter::landed(uint64_t end) {
+  {
+    std::lock_guard lk(st_->mu);
+    if (end <= st_->landed) return;
+    st_->landed = end;
+  }
+  st_->cv.notify_all();
+}
+
+uint64_t StreamWriter::early_bytes() const { return st_->early.load(); }
+
+void StreamWriter::finish(const uint8_t* base, uint64_t n, FileIoStats* stats) {
+  State& S = *st_;
+  if (S.started && (base != S.base || n != S.n)) {
+    S.halt();  // the producer's buffer moved: nothing written so far counts
+    S.started = false;
+    S.rewrites.clear();
+    S.early = 0;
+    S.threads = io_threads(S.opt);
+  }
+  if (!S.started) start(base, n);
+  {
+    std::lock_guard lk(S.mu);
+    S.final_all = true;
+    S.landed = n;
+  }
+  S.cv.notify_all();
+  for (auto& th : S.pool) th.join();
+  S.pool.clear();
+  auto fail = [&](int e) { raise(Errc::InvalidArgument, "cannot write " + S.path.string() + ": " + std::strerror(e)); };
+  if (const int e = S.err.load()) fail(e);
+  // the ranges the producer completed after they streamed, as whole blocks
+  std::sort(S.rewrites.begin(), S.rewrites.end());
+  std::unique_ptr<AlignedBuf> b;
+  uint64_t done = 0;  // blocks below this are written again already
+  for (auto [a, e] : S.rewrites) {
+    a = std::max(a / kBlock * kBlock, done);
+    e = std::min(round_block(std::min(e, n)), round_block(n));
+    if (a >= e) continue;
+    for (uint64_t off = a; off < e; off += S.chunk) {
+      const uint64_t len = std::min({S.chunk, e - off, n - off});
+      if (const int er = S.write_range(off, len, b)) fail(er);
+    }
+    done = e;
+  }
+  if (::ftruncate(S.f.fd, static_cast<off_t>(n)) != 0) fail(errno);
+  if (S.opt.sync && ::fdatasync(S.f.fd) != 0 && errno != EINVAL) fail(errno);
+  const int fd = S.f.fd;
+  S.f.fd = -1;
+  if (::close(fd) != 0) fail(errno);
+  if (stats)
+    *stats = FileIoStats{now_ms() - S.t0, n, S.threads, S.direct, S.bounced.load()};
 }
 
 uint64_t file_bytes(const std::filesystem::path& path) {

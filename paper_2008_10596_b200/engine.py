@@ -50,7 +50,7 @@ class Stats(C.Structure):
 
 class IoStats(C.Structure):
     _fields_ = [("ms", C.c_double), ("bytes", C.c_uint64), ("threads", C.c_uint32),
-                ("direct", C.c_int32), ("bounced", C.c_uint64)]
+                ("direct", C.c_int32), ("bounced", C.c_uint64), ("streamed", C.c_uint64)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}

@@ -104,3 +104,28 @@ def test_checkpoint_to_unwritable_path(eng, tmp_path):
     assert e.value.errc == "InvalidArgument"
     # the session is untouched and still drains
     assert s.checkpoint()[0]
+
+
+def test_streamed_write_under_the_drain(eng, tmp_path, monkeypatch):
+    """CRAC_FILE_STREAM=1: checkpoint_to_file writes the file while the
+    drain's windows land (StreamWriter): 1 MiB pieces so most of the file streams under the D2H;
+    the leading sections, crc3 and the tail are written again once final.
+    Over a longer stale file (in place, cut to size); the same bytes as the
+    drain-then-write path, and the reference restarts from it."""
+    monkeypatch.setenv("CRAC_IO_CHUNK_MIB", "1")
+    monkeypatch.setenv("CRAC_FILE_STREAM", "1")
+    s = eng.Session(seed=11, arena_bytes=512 << 20)
+    workloads.build_regions(s, 5, lambda k: (64 << 20) + 4096 * k + 3 * k + 5, seed=11)
+    p = tmp_path / "streamed.img"
+    p.write_bytes(os.urandom(1 << 20) * 400)  # longer than the image, garbage
+    img = eng.Image()
+    drain, io = s.checkpoint_to_file(p, img)
+    want = img.tobytes()
+    assert p.read_bytes() == want
+    assert io["bytes"] == len(want) and io["streamed"] > 0, io
+    monkeypatch.delenv("CRAC_FILE_STREAM")
+    q = tmp_path / "plain.img"
+    _, io2 = s.checkpoint_to_file(q)
+    assert io2["streamed"] == 0 and q.read_bytes() == want
+    b, _ = ref.ref_restart_from_file(p)
+    assert b.checkpoint()[0] == want
