@@ -1383,6 +1383,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
   if (!P.host_pages.empty() || !P.pinned_runs.empty())
     host_pass = std::thread([&] {
       try {
+        cudaSetDevice(E.device);  // (its event waits must not touch device 0's context)
         copy_pinned_runs(E, P, img + s3, true);  // before the app resumes (join below)
         host_pages_drain(E, P, img + s3, head, recorded);
       } catch (...) {
@@ -1405,6 +1406,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
     sink->rewrite(s3 + P.len3, s3 + P.len3 + 4);
     sink->rewrite(s3 + P.stream_len, total);
     sink_pass = std::thread([&, sink, img, s3, head, windows] {
+      cudaSetDevice(E.device);
       for (uint64_t w = 0; w < windows; ++w) {
         while (recorded.load(std::memory_order_acquire) < int64_t(w)) {
           if (sink_stop.load(std::memory_order_relaxed)) return;
