@@ -1095,6 +1095,12 @@ def main() -> None:
             kern_rows[k]["regime"] = ("latency: each launch moves only the frames and payload edges "
                                       "around the direct copies of its window, beside the link's copy "
                                       "(off the critical path; 'isolated' gives its bandwidth)")
+        elif k == "k_scatter_records":
+            kern_rows[k]["regime"] = ("in situ: the first ring windows of a cold restart, scattered "
+                                      "while the arena's tail is mapped on a thread beside them and the "
+                                      "H2D runs (their event span includes those stalls; off the critical "
+                                      "path); ncu times the same launches at ~19 us serialised "
+                                      "(profiles/r02be/launch_summary.txt), 'isolated' gives its bandwidth")
 
     # cold restart is now the timed step itself; the warm-arena variant is
     # reported beside it for comparison (arena adopted from the closed session)
