@@ -1096,11 +1096,12 @@ def main() -> None:
                                       "around the direct copies of its window, beside the link's copy "
                                       "(off the critical path; 'isolated' gives its bandwidth)")
         elif k == "k_scatter_records":
-            kern_rows[k]["regime"] = ("in situ: the first ring windows of a cold restart, scattered "
-                                      "while the arena's tail is mapped on a thread beside them and the "
-                                      "H2D runs (their event span includes those stalls; off the critical "
-                                      "path); ncu times the same launches at ~19 us serialised "
-                                      "(profiles/r02be/launch_summary.txt), 'isolated' gives its bandwidth")
+            kern_rows[k]["regime"] = ("in situ: the restart's first ring windows (queued before the "
+                                      "parse, so no direct runs start in them) scattered whole beside the "
+                                      "H2D; their event span is ~1.1 ms per launch with or without the "
+                                      "cold tail map beside them (profiles/r02/scatter_span.txt) against "
+                                      "~19 us under ncu (serialised, profiles/r02be/launch_summary.txt); "
+                                      "hidden behind the H2D, 'isolated' gives its bandwidth")
 
     # cold restart is now the timed step itself; the warm-arena variant is
     # reported beside it for comparison (arena adopted from the closed session)
