@@ -2148,6 +2148,15 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     constexpr uint64_t kVerifyBatch = 32768;  // 2 GiB of 64 KiB chunks: big enough to keep
                                               // K1 efficient beside the H2D; the tail
                                               // batch after the last window is < 0.5 ms
+    // a stream of fewer chunks (C2: 15.8 k small payloads) is verified in
+    // `verify_split` batches as its windows land, so only the last one
+    // follows the last H2D (CRAC_VERIFY_SPLIT, default 4; 1 = one batch)
+    static const uint64_t verify_split = [] {
+      const char* e = std::getenv("CRAC_VERIFY_SPLIT");
+      return uint64_t(e ? std::max(1, std::atoi(e)) : 4);
+    }();
+    const uint64_t verify_batch =
+        std::min<uint64_t>(kVerifyBatch, std::max<uint64_t>(1024, P.pay_first.back() / verify_split));
     for (uint64_t w = 0; w < windows; ++w) {
       const int slot = int(w % DrainEngine::kSlots);
       uint8_t* buf = E.d_ring + slot * (DrainEngine::kWindow + 64);
@@ -2185,7 +2194,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       while (done < P.pay_spans.size() &&
              P.pay_rec_off[done] + P.pay_spans[done].len <= off + len)
         ++done;
-      if (done > spans_done && (P.pay_first[done] - P.pay_first[spans_done] >= kVerifyBatch ||
+      if (done > spans_done && (P.pay_first[done] - P.pay_first[spans_done] >= verify_batch ||
                                 w + 1 == windows)) {
         if (stats) {
           E.ensure_verify_events(verifies + 1);
