@@ -722,7 +722,7 @@ def run_c5(args, engine, sess, image, live, group, rank, world, peaks) -> None:
             "cpu_baseline": cpu}), flush=True)
 
 
-def dd_ceiling(path: Path, nbytes: int, streams: int = 8) -> dict:
+def dd_ceiling(path: Path, nbytes: int, streams: int = 8, unlink: bool = True) -> dict:
     """Storage ceiling measured with coreutils dd, independent of our writer:
     `streams` concurrent O_DIRECT dd processes over disjoint 64 MiB-block
     ranges of one file (write with fdatasync, then read)."""
@@ -748,10 +748,11 @@ def dd_ceiling(path: Path, nbytes: int, streams: int = 8) -> dict:
         ok = all(p.wait() == 0 for p in ps)
         dt = time.perf_counter() - t0
         out[f"{mode}_GBps"] = round(blocks * bs / dt / 1e9, 3) if ok else None
-    try:
-        path.unlink()
-    except OSError:
-        pass
+    if unlink:
+        try:
+            path.unlink()
+        except OSError:
+            pass
     out["how"] = f"{streams} concurrent dd O_DIRECT streams, 64 MiB blocks, {blocks * bs // MIB} MiB"
     return out
 
@@ -818,7 +819,22 @@ def run_file(args, engine, sess, live, group, rank, world, cfg_extra, gbar=None)
         zs.close()
         zero.close()
     img.close()
-    ceiling = dd_ceiling(path, min(nbytes, 16 * GIB)) if rank == 0 else None
+    # the storage ceiling: coreutils dd at 8 and at 16 concurrent streams (the
+    # writer's own thread count), the best of each direction; one dd pass is
+    # noisy on the box's virtio disk (a single 8-stream pass has read below
+    # what our writer then reached)
+    ceiling = None
+    if rank == 0:
+        for streams in (8, 16):
+            c = dd_ceiling(path, min(nbytes, 16 * GIB), streams, unlink=streams == 16)
+            if ceiling is None:
+                ceiling = c
+                continue
+            for k in ("write_GBps", "read_GBps"):
+                if (c.get(k) or 0) > (ceiling.get(k) or 0):
+                    ceiling[k] = c[k]
+        ceiling["how"] = ("best of 8 and 16 concurrent dd O_DIRECT streams per direction, "
+                          "64 MiB blocks, " + ceiling["how"].split(", ")[-1])
     try:
         path.unlink()
     except OSError:
