@@ -1016,8 +1016,9 @@ uint64_t host_run_bytes(const ImagePlan& P) {
 // Enqueues the copy of stream bytes [off, end) between a window buffer
 // (`buf` holds stream offset `off`) and the image stream, minus the host runs,
 // in pieces of at most kCopyChunk.  `run` walks P.host_runs across calls.
-void copy_window(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, uint8_t* buf,
-                 uint8_t* stream, bool d2h, cudaStream_t st) {
+uint64_t copy_window(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, uint8_t* buf,
+                     uint8_t* stream, bool d2h, cudaStream_t st, bool dry = false) {
+  uint64_t bytes = 0;
   const auto& R = P.skip_runs;
   // ring window pieces (CRAC_COPY_CHUNK_MIB, default DrainEngine::kCopyChunk)
   static const uint64_t piece = [] {
@@ -1039,7 +1040,8 @@ void copy_window(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, ui
     // H2D: 16 bytes past a gap that a skip run ends, for the scatter's
     // straddling last word (ring bytes under a skip run are never read else)
     const uint64_t bc = d2h ? b : std::min(end, b + 16);
-    for (uint64_t c = a; c < bc; c += piece) {
+    bytes += b - a;
+    for (uint64_t c = a; c < bc && !dry; c += piece) {
       const uint64_t n = std::min(piece, bc - c);
       void* dst = d2h ? static_cast<void*>(stream + c) : static_cast<void*>(buf + (c - off));
       const void* src = d2h ? static_cast<const void*>(buf + (c - off))
@@ -1048,6 +1050,7 @@ void copy_window(const ImagePlan& P, size_t& run, uint64_t off, uint64_t end, ui
     }
     a = b;
   }
+  return bytes;
 }
 
 // Host-resident managed pages of a drain.  Each host thread takes a block of
@@ -2121,7 +2124,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   }
   tr.mark("premap");
 
-  uint64_t windows = 0, verifies = 0, scattered = 0, scatter_launches = 0;
+  uint64_t windows = 0, verifies = 0, scattered = 0, scatter_launches = 0, ring_skipped = 0;
   // enqueues H2D windows -> scatter -> K1 verify (payloads as their regions
   // complete, then the device-resident pages); nothing here waits
   auto enqueue_data_path = [&] {
@@ -2144,7 +2147,12 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
         }
     }
     size_t spans_done = 0, run_i = 0, krun_i = 0, drun_i = 0, srec_i = 0;
-    std::vector<std::pair<uint64_t, uint64_t>> kr;
+    std::vector<std::pair<uint64_t, uint64_t>> kr, scatter_kr;
+    // CRAC_RING_SKIP=0: every window's ring part crosses the link, read or not
+    static const bool ring_skip = [] {
+      const char* e = std::getenv("CRAC_RING_SKIP");
+      return !(e && e[0] == '0');
+    }();
     constexpr uint64_t kVerifyBatch = 32768;  // 2 GiB of 64 KiB chunks: big enough to keep
                                               // K1 efficient beside the H2D; the tail
                                               // batch after the last window is < 0.5 ms
@@ -2164,20 +2172,30 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       const uint64_t len = std::min(DrainEngine::kWindow, P.stream_len - off);
       const uint64_t with_ahead = std::min(len + 16, P.stream_len - off);
       if (deferred_map && off + with_ahead > head_safe_end) join_tail_map();
+      // the window's kernel ranges, and which of them hold device-bound bytes
+      kernel_ranges(P, krun_i, off, off + len, kr);
+      scatter_kr.clear();
+      for (const auto& [g0, g1] : kr)
+        if (range_needs_scatter(P, srec_i, g0, g1)) scatter_kr.emplace_back(g0, g1);
       if (w >= n_spec) {  // (the early windows are in their slots already)
-        if (w >= uint64_t(DrainEngine::kSlots))
-          check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_free[slot], 0), "wait");
-        copy_window(P, run_i, off, off + with_ahead, buf, const_cast<uint8_t*>(raw.data() + s3),
-                    false, E.s_copy);
+        // a window no scatter reads (C4: only frames between direct runs)
+        // needs no ring copy, so the copy stream carries no slot wait there
+        // and its direct copies follow each other back to back
+        if (scatter_kr.empty() && ring_skip) {
+          ring_skipped += copy_window(P, run_i, off, off + len, buf, nullptr, false, E.s_copy, true);
+        } else {
+          if (w >= uint64_t(DrainEngine::kSlots))
+            check_cuda(cudaStreamWaitEvent(E.s_copy, E.ev_free[slot], 0), "wait");
+          copy_window(P, run_i, off, off + with_ahead, buf, const_cast<uint8_t*>(raw.data() + s3),
+                      false, E.s_copy);
+        }
         copy_direct(P, drun_i, off, off + len, const_cast<uint8_t*>(raw.data() + s3), false,
                     E.s_copy);
         check_cuda(cudaEventRecord(E.ev_ready[slot], E.s_copy), "event");
       }
       check_cuda(cudaStreamWaitEvent(E.s_pack, E.ev_ready[slot], 0), "wait");
       if (stats) cudaEventRecord(E.ev_w0[w], E.s_pack);
-      kernel_ranges(P, krun_i, off, off + len, kr);
-      for (const auto& [g0, g1] : kr) {
-        if (!range_needs_scatter(P, srec_i, g0, g1)) continue;
+      for (const auto& [g0, g1] : scatter_kr) {
         ++scatter_launches;
         check_cuda(cudaError_t(crac_scatter_records(E.d_recs.ptr, uint32_t(P.recs.size()),
                                                     E.d_tile_rec.ptr + g0 / CRAC_TILE_BYTES,
@@ -2368,7 +2386,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       uint64_t early_host = 0;
       for (const auto& [lo, hi] : P.host_runs)
         if (lo < n_spec * W) early_host += std::min(hi, n_spec * W) - lo;
-      stats->h2d_bytes = P.stream_len - host_run_bytes(P) + early_host;
+      stats->h2d_bytes = P.stream_len - host_run_bytes(P) + early_host - ring_skipped;
       stats->hash_bytes = hashed_bytes(P);
       stats->hash_launches = verifies;
       for (uint64_t v = 0; v < verifies; ++v) stats->hash_ms += elapsed(E.ev_v0[v], E.ev_v1[v]);
