@@ -403,6 +403,34 @@ def test_direct_runs_edges_match_reference(eng):
     assert rs.checkpoint()[0] == img
 
 
+def test_refill_skips_ring_windows_no_scatter_reads(eng):
+    """Big Device payloads only (the C4 shape at 10 x 64 MiB, plus one odd
+    size): past the early windows, a window holds only frames between exact
+    direct runs, so the refill skips its ring H2D (CRAC_RING_SKIP) -- fewer
+    H2D bytes than the stream -- and still restores every byte, cold and
+    warm."""
+    MIB = 1 << 20
+    sizes = [64 * MIB] * 9 + [64 * MIB + 4097]
+    s = eng.Session(seed=21, arena_bytes=704 * MIB)
+    r = ref.RefSession(seed=21, arena_bytes=704 * MIB)
+    for api in (s, r):
+        for k, size in enumerate(sizes):
+            i, _ = api.alloc(workloads.DEVICE, size)
+            api.fill_synthetic(i, 60 + k)
+    img, st = s.checkpoint()
+    assert img == r.checkpoint()[0]
+    want = _state(s)
+    s.close()
+    eng.drop_arena_cache()
+    rs, rst = eng.restart(img)  # cold
+    assert rst["h2d_bytes"] < st["d2h_bytes"], (rst["h2d_bytes"], st["d2h_bytes"])
+    assert _state(rs) == want
+    assert rs.checkpoint()[0] == img
+    rs.close()
+    rw, _ = eng.restart(img)  # warm (the arena of the closed session adopted)
+    assert _state(rw) == want and rw.checkpoint()[0] == img
+
+
 def test_c3_host_runs_skip_the_link_and_match_reference(eng):
     """Host-resident runs >= 256 KiB never cross PCIe (the window copies skip
     them; host threads write their frames and content).  Runs straddle the
