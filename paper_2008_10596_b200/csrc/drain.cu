@@ -1891,6 +1891,29 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
     return e ? uint64_t(std::strtoull(e, nullptr, 10)) << 20 : kColdHeadDefault;
   }();
   const uint64_t cold_head = (cold_head_env & ~((2ull << 20) - 1));
+  // the first ring windows' H2D, queued before the parse (they land in the
+  // engine's ring, not the arena, so they need no mapping)
+  auto enqueue_early = [&] {
+    DrainEngine& e = holder->drain_engine();
+    n_spec = std::min<uint64_t>(DrainEngine::kSlots, (pk.stream_len + W - 1) / W);
+    check_cuda(cudaEventRecord(e.ev_c0, e.s_copy), "event");
+    for (uint64_t w = 0; w < n_spec; ++w) {
+      const uint64_t off = w * W, n = std::min(W + 16, pk.stream_len - off);
+      uint8_t* buf = e.d_ring + w * (W + 64);
+      for (uint64_t c = 0; c < n; c += DrainEngine::kCopyChunk)
+        check_cuda(cudaMemcpyAsync(buf + c, raw.data() + pk.s3 + off + c,
+                                   std::min(DrainEngine::kCopyChunk, n - c), cudaMemcpyHostToDevice,
+                                   e.s_copy),
+                   "H2D (early)");
+      check_cuda(cudaEventRecord(e.ev_ready[w], e.s_copy), "event");
+    }
+  };
+  // CRAC_EARLY_FIRST=0: a big cold arena's head is mapped before the early
+  // windows are queued (the copy engine idles during that map)
+  static const bool early_first = [] {
+    const char* e = std::getenv("CRAC_EARLY_FIRST");
+    return !(e && e[0] == '0');
+  }();
   std::thread map_thread;
   std::exception_ptr map_err;
   bool mapping = false;
@@ -1912,6 +1935,7 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
       try {
         const bool split = cold_head && pk.arena_hi >= 2 * cold_head;
         map_head = split ? cold_head : pk.arena_hi;
+        if (early_first) enqueue_early();  // the link works while the head maps
         holder->device().premap(kArenaBase, map_head);
         if (split) {
           deferred_map = true;
@@ -1925,6 +1949,8 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
           });
         }
       } catch (const Error&) {
+        if (n_spec) cudaStreamSynchronize(holder->drain_engine().s_copy);  // early copies in flight
+        n_spec = 0;
         holder.reset();  // reported in order after the parse, if at all
       }
     }
@@ -1951,20 +1977,8 @@ Session restart_image(std::span<const uint8_t> image, const KernelCatalog& catal
   } map_join{map_thread};
   if (holder && !mapping && !deferred_map && !holder->device().arena_premapped()) {
     // keep the session; no early windows
-  } else if (holder) {
-    DrainEngine& e = holder->drain_engine();
-    n_spec = std::min<uint64_t>(DrainEngine::kSlots, (pk.stream_len + W - 1) / W);
-    check_cuda(cudaEventRecord(e.ev_c0, e.s_copy), "event");
-    for (uint64_t w = 0; w < n_spec; ++w) {
-      const uint64_t off = w * W, n = std::min(W + 16, pk.stream_len - off);
-      uint8_t* buf = e.d_ring + w * (W + 64);
-      for (uint64_t c = 0; c < n; c += DrainEngine::kCopyChunk)
-        check_cuda(cudaMemcpyAsync(buf + c, raw.data() + pk.s3 + off + c,
-                                   std::min(DrainEngine::kCopyChunk, n - c), cudaMemcpyHostToDevice,
-                                   e.s_copy),
-                   "H2D (early)");
-      check_cuda(cudaEventRecord(e.ev_ready[w], e.s_copy), "event");
-    }
+  } else if (holder && !n_spec) {
+    enqueue_early();
   }
   tr.mark("early");
   ParsedImage p;
