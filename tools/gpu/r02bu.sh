@@ -1,0 +1,17 @@
+# round 2bu: closing validation of round 2's last build: full GPU suite, smoke, default bench, C2, reference arm
+mkdir -p gpurun_out/r02bu
+timeout 2400 python -m pytest tests -x -q -m gpu > gpurun_out/r02bu/gputests.log 2>&1; tail -2 gpurun_out/r02bu/gputests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r02bu/smoke.log 2>&1; tail -1 gpurun_out/r02bu/smoke.log
+timeout 900 python bench.py > gpurun_out/r02bu/bench_c4.json 2> gpurun_out/r02bu/bench_c4.err
+timeout 600 python bench.py --workload c2 > gpurun_out/r02bu/bench_c2.json 2> gpurun_out/r02bu/bench_c2.err
+timeout 900 python bench.py --impl reference > gpurun_out/r02bu/bench_reference.json 2> gpurun_out/r02bu/bench_reference.err
+python - <<'PY'
+import json
+for w in ("c4", "c2"):
+    d = json.loads(open(f"gpurun_out/r02bu/bench_{w}.json").read().splitlines()[-1])
+    r = d["roofline"]; e = d["e2e"]
+    print(w, d["value"], e["value"], e["with_teardown"]["value"], r["frac"], d["per_gpu"]["checkpoint_ms"], d["per_gpu"]["restart_ms"],
+          r["d2h_peak_GBps"], r["h2d_peak_GBps"], "K1", r["kernels"]["k1_chunk_crc"]["frac"], "verified", d["verified"]["ok"], d["clocks"]["reasons"])
+ref = json.loads(open("gpurun_out/r02bu/bench_reference.json").read().splitlines()[-1])
+print("reference", ref.get("value"), ref.get("cpu_baseline", {}).get("cores"))
+PY
