@@ -262,6 +262,10 @@ int crac_drop_arena_cache_async(int device);
 /* Host CRC-32 the engine uses for host-resident pages and small sections
  * (zlib's crc32, bit-identical; PCLMUL folding).  No GPU needed. */
 uint32_t crac_crc32_host(const void* data, uint64_t n, uint32_t crc);
+/* The drain's host-page move: copies n bytes src -> dst (non-temporal stores
+ * when dst is 16-byte aligned) and returns crac_crc32_host(src, n, crc) from
+ * the same single read of src.  No GPU needed. */
+uint32_t crac_crc32_copy_host(void* dst, const void* src, uint64_t n, uint32_t crc);
 
 /* Kernel-level entry for parity tests: CRC of every 64 KiB (chunk_bytes)
  * chunk of a host buffer, computed by K1 on the GPU. */

@@ -512,6 +512,12 @@ uint32_t crac_crc32_host(const void* data, uint64_t n, uint32_t crc) {
   return codec::crc32_fast(static_cast<const uint8_t*>(data), n, crc);
 }
 
+uint32_t crac_crc32_copy_host(void* dst, const void* src, uint64_t n, uint32_t crc) {
+  const uint32_t r = codec::crc32_copy_stream(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), n, crc);
+  codec::stream_fence();
+  return r;
+}
+
 int crac_decode_check(const void* image, uint64_t size) {
   return guard([&] { (void)decode_image({static_cast<const uint8_t*>(image), size}); });
 }

@@ -61,6 +61,46 @@ CRAC_PCLMUL uint32_t fold_crc(uint32_t crc, const uint8_t* p, size_t len) {
   return uint32_t(_mm_extract_epi32(_mm_xor_si128(t, x0), 1));
 }
 
+// fold_crc that also copies the bytes it folds to `dst` (16-byte aligned)
+// with non-temporal stores: the destination lines are written without being
+// read first (no read-for-ownership), and the source is read once
+CRAC_PCLMUL uint32_t fold_crc_copy(uint32_t crc, const uint8_t* p, uint8_t* d, size_t len) {
+  const __m128i k1k2 = _mm_set_epi64x(0x1c6e41596LL, 0x154442bd4LL);
+  const __m128i k3k4 = _mm_set_epi64x(0x0ccaa009eLL, 0x1751997d0LL);
+  const __m128i k5 = _mm_set_epi64x(0, 0x163cd6124LL);
+  const __m128i poly = _mm_set_epi64x(0x1f7011641LL, 0x1db710641LL);
+  const __m128i mask32 = _mm_set_epi32(0, 0, 0, -1);
+  auto out = [&](size_t o, __m128i v) { _mm_stream_si128(reinterpret_cast<__m128i*>(d + o), v); };
+  __m128i y0 = load16(p), y1 = load16(p + 16), y2 = load16(p + 32), y3 = load16(p + 48);
+  out(0, y0), out(16, y1), out(32, y2), out(48, y3);
+  __m128i x0 = _mm_xor_si128(y0, _mm_cvtsi32_si128(int(crc))), x1 = y1, x2 = y2, x3 = y3;
+  p += 64;
+  d += 64;
+  len -= 64;
+  for (; len >= 64; len -= 64, p += 64, d += 64) {
+    y0 = load16(p), y1 = load16(p + 16), y2 = load16(p + 32), y3 = load16(p + 48);
+    out(0, y0), out(16, y1), out(32, y2), out(48, y3);
+    x0 = fold16(x0, k1k2, y0);
+    x1 = fold16(x1, k1k2, y1);
+    x2 = fold16(x2, k1k2, y2);
+    x3 = fold16(x3, k1k2, y3);
+  }
+  x0 = fold16(x0, k3k4, x1);
+  x0 = fold16(x0, k3k4, x2);
+  x0 = fold16(x0, k3k4, x3);
+  for (; len >= 16; len -= 16, p += 16, d += 16) {
+    y0 = load16(p);
+    out(0, y0);
+    x0 = fold16(x0, k3k4, y0);
+  }
+  x0 = _mm_xor_si128(_mm_clmulepi64_si128(x0, k3k4, 0x10), _mm_srli_si128(x0, 8));
+  x0 = _mm_xor_si128(_mm_clmulepi64_si128(_mm_and_si128(x0, mask32), k5, 0x00),
+                     _mm_srli_si128(x0, 4));
+  __m128i t = _mm_clmulepi64_si128(_mm_and_si128(x0, mask32), poly, 0x10);
+  t = _mm_clmulepi64_si128(_mm_and_si128(t, mask32), poly, 0x00);
+  return uint32_t(_mm_extract_epi32(_mm_xor_si128(t, x0), 1));
+}
+
 bool have_pclmul() {
   static const bool ok = __builtin_cpu_supports("pclmul") && __builtin_cpu_supports("sse4.1");
   return ok;
@@ -75,5 +115,21 @@ uint32_t crc32_fast(const uint8_t* p, size_t n, uint32_t crc) {
   if (n > body) crc = uint32_t(::crc32_z(crc, p + body, n - body));
   return crc;
 }
+
+uint32_t crc32_copy_stream(uint8_t* dst, const uint8_t* src, size_t n, uint32_t crc) {
+  if (n < 64 || !have_pclmul() || reinterpret_cast<uintptr_t>(dst) % 16) {
+    std::memcpy(dst, src, n);
+    return crc32_fast(src, n, crc);
+  }
+  const size_t body = n & ~size_t(15);
+  crc = ~fold_crc_copy(~crc, src, dst, body);
+  if (n > body) {
+    std::memcpy(dst + body, src + body, n - body);
+    crc = uint32_t(::crc32_z(crc, src + body, n - body));
+  }
+  return crc;
+}
+
+void stream_fence() { _mm_sfence(); }
 
 }  // namespace cracsim::codec

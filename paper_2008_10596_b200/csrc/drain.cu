@@ -815,14 +815,15 @@ void copy_pinned_runs(DrainEngine& E, const ImagePlan& P, uint8_t* stream, bool 
     const uint64_t o = pieces[i].second, n = std::min(kPiece, run.hi - run.lo - o);
     uint8_t* host = reinterpret_cast<uint8_t*>(run.host) + o;
     uint8_t* img = stream + run.lo + o;
-    if (drain) std::memcpy(img, host, n);
-    else std::memcpy(host, img, n);
+    if (!drain) std::memcpy(host, img, n);
     for (uint64_t c = 0; c < n; c += DrainEngine::kChunk) {
       const uint32_t len = uint32_t(std::min<uint64_t>(DrainEngine::kChunk, n - c));
       const uint64_t slot = run.pin0 + (o + c) / DrainEngine::kChunk;
-      E.h_pin_crc.ptr[slot] = crc32_fast(host + c, len);
+      // drain: each chunk read once, hashed and streamed into the image
+      E.h_pin_crc.ptr[slot] = drain ? crc32_copy_stream(img + c, host + c, len) : crc32_fast(host + c, len);
       if (drain) E.h_pin_key.ptr[slot] = chunk_key_host(host + c, len);
     }
+    if (drain) stream_fence();
   }, /*min_parallel=*/2);
 }
 
@@ -1082,6 +1083,11 @@ void host_pages_drain(DrainEngine& E, const ImagePlan& P, uint8_t* stream, uint6
   uint32_t* crc = E.h_host_crc.ptr;
   constexpr uint64_t W = DrainEngine::kWindow;
   const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  // CRAC_HOST_NT=0: host-run pages copied with memcpy after their CRC
+  static const bool nt_copy = [] {
+    const char* e = std::getenv("CRAC_HOST_NT");
+    return !(e && e[0] == '0');
+  }();
   std::atomic<uint64_t> next{0};
   std::atomic<int> failed{0};
   auto worker = [&] {
@@ -1090,12 +1096,15 @@ void host_pages_drain(DrainEngine& E, const ImagePlan& P, uint8_t* stream, uint6
       for (uint64_t i = b; i < std::min(n, b + 512); ++i) {
         const HostPage& h = P.host_pages[i];
         const auto* src = reinterpret_cast<const uint8_t*>(h.ptr);
-        crc[i] = crc32_fast(src, h.len);
         if (h.own_frame) {  // in a host run: no window copy touches these bytes
           std::memcpy(stream + h.stream_off - 16, P.recs[h.rec].frame, 16);
-          std::memcpy(stream + h.stream_off, src, h.len);
+          // one read of the page: hashed and streamed into the image (no
+          // read-for-ownership of the image lines)
+          crc[i] = nt_copy ? crc32_copy_stream(stream + h.stream_off, src, h.len)
+                           : (std::memcpy(stream + h.stream_off, src, h.len), crc32_fast(src, h.len));
           continue;
         }
+        crc[i] = crc32_fast(src, h.len);
         if (stash_of[i] != ~0ull) {
           std::memcpy(Q.stash.data() + stash_of[i], src, h.len);
           continue;
@@ -1110,6 +1119,7 @@ void host_pages_drain(DrainEngine& E, const ImagePlan& P, uint8_t* stream, uint6
         }
         std::memcpy(stream + h.stream_off, src, h.len);
       }
+    stream_fence();  // the streamed image bytes are visible before the join
   };
   std::vector<std::thread> pool;
   for (unsigned t = 1; t < hw; ++t) pool.emplace_back(worker);
@@ -1367,6 +1377,7 @@ void drain_locked(Session& session, PinnedImage& out, bool use_shadow, DrainStat
 
   const uint64_t windows = (head + W - 1) / W;
   Q.windows = windows;
+  Q.timed = stats != nullptr;
   if (stats) E.ensure_window_events(windows);
   // a streamed file write follows the windows as they land (the image is
   // final there except for what the host writes after the stream: the
@@ -1609,7 +1620,9 @@ void drain_finish(Session& session, DrainStats* stats) {
       stats->hash_bytes = hashed_bytes(P);
       stats->pack_launches = Q.launches;  // ring + shadow
       stats->pack_bytes = Q.packed + (P.stream_len - Q.head);  // ring windows + shadow
-      stats->pack_ms = mean_pack_launch_ms(E, Q.windows, Q.ring_launches);  // per ring launch
+      // per ring launch; a split drain begun without stats (checkpoint_begin)
+      // recorded no window events
+      stats->pack_ms = Q.timed ? mean_pack_launch_ms(E, Q.windows, Q.ring_launches) : 0.0;
       stats->d2h_bytes = P.stream_len - host_run_bytes(P);
       stats->shadow_bytes = P.stream_len - Q.head;
     }

@@ -209,6 +209,7 @@ struct DrainEngine {
     uint64_t windows = 0;    // ring windows (stats)
     uint64_t packed = 0;     // stream bytes the ring windows' pack kernels produced
     uint64_t launches = 0, ring_launches = 0;  // pack launches: all / of the ring windows
+    bool timed = false;      // the ring windows recorded ev_w0 / ev_w1 (drain_locked had stats)
     double stall_ms = 0;
     // host-resident pages of short runs in the shadow part, copied while the
     // app was stopped; written into the image after the shadow D2H lands

@@ -17,6 +17,11 @@ uint32_t crc32_host(const uint8_t* p, size_t n, uint32_t crc = 0);
 // zlib-identical CRC-32 by carry-less multiplication (crc_host.cpp), ~12 GB/s
 // per core against zlib's 2.6; zlib below 64 bytes or without PCLMUL.
 uint32_t crc32_fast(const uint8_t* p, size_t n, uint32_t crc = 0);
+// crc32_fast of src that also copies src to dst (non-temporal stores when dst
+// is 16-byte aligned: no read-for-ownership of the destination); the caller
+// runs stream_fence() before another agent may read dst
+uint32_t crc32_copy_stream(uint8_t* dst, const uint8_t* src, size_t n, uint32_t crc = 0);
+void stream_fence();
 
 std::vector<uint8_t> meta_bytes(const SnapshotMeta& m);
 std::vector<uint8_t> log_bytes(std::span<const CallLogEntry> log);

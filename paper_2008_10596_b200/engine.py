@@ -114,6 +114,7 @@ _SIGS = {
     "crac_checkpoint_precopy_finish": (C.c_int, [_P, C.POINTER(Stats)]),
     "crac_reserve_shadow_on": (C.c_int, [_P, _U64, C.c_int]),
     "crac_crc32_host": (C.c_uint32, [_P, _U64, _U32]),
+    "crac_crc32_copy_host": (C.c_uint32, [_P, _P, _U64, _U32]),
     "crac_session_set_barrier": (C.c_int, [_P, _P, _P]),
     "crac_compress_image_gpu": (C.c_int, [_P, _U64, C.POINTER(_P), _PU64, C.POINTER(C.c_double)]),
     "crac_probe_managed_populate": (C.c_int, [_U64, _U64, _U32, C.POINTER(C.c_double)]),

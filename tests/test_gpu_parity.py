@@ -972,3 +972,21 @@ def test_incremental_resends_a_crc_preserving_change(eng):
     assert st["incremental"]
     assert st["dirty_chunks"] == 2
     assert image.tobytes() == r.checkpoint()[0] == s.checkpoint()[0]
+
+
+def test_split_drain_first_in_a_fresh_process():
+    """A split drain begun without stats (checkpoint_begin) and finished with
+    them, as the first drain of a process: drain_finish once timed the ring
+    windows from events that only a drain with stats creates, so on a fresh
+    engine it read handles that were never made (segfault).  Run in its own
+    process so no earlier drain has sized the engine's event tables."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    for node in ("test_pinned_payloads_move_on_the_host_and_match_reference[all-shadow]",
+                 "test_async_drain_with_managed_runs_matches_reference[64]"):
+        out = subprocess.run([sys.executable, "-X", "faulthandler", "-m", "pytest", "-x", "-q", "-p",
+                              "no:cacheprovider", f"tests/test_gpu_parity.py::{node}"],
+                             cwd=root, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]

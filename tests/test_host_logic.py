@@ -92,3 +92,35 @@ def test_host_crc_is_zlib():
             for seed in (0, 0xDEADBEEF):
                 got = lib.crac_crc32_host(ctypes.c_void_p(base + off), n, seed)
                 assert got == zlib.crc32(buf[off:off + n], seed), (n, off, seed)
+
+
+def test_host_crc_copy_is_zlib_and_memcpy():
+    """crac_crc32_copy_host (the drain's host-page move: one read, PCLMUL
+    fold + non-temporal stores) returns zlib's CRC of the source and leaves an
+    exact copy, for every destination phase (16-byte aligned: streamed; else
+    memcpy) and lengths around the fold boundaries."""
+    import ctypes
+    import os
+    import zlib
+
+    from paper_2008_10596_b200 import engine
+    if not engine.LIB_PATH.exists():
+        from paper_2008_10596_b200 import build
+        build.build()
+    lib = engine.lib()
+    buf = os.urandom(1 << 16)
+    src = ctypes.create_string_buffer(buf, len(buf))
+    dst = ctypes.create_string_buffer(len(buf) + 64)
+    sbase, dbase = ctypes.addressof(src), ctypes.addressof(dst)
+    dpad = (-dbase) % 16  # dst + dpad is 16-byte aligned
+    for n in list(range(0, 200)) + [4095, 4096, 4097, 65536 - 64]:
+        for soff in (0, 3):
+            for doff in (dpad, dpad + 16, dpad + 1):
+                ctypes.memset(dbase, 0xA5, len(buf) + 64)
+                got = lib.crac_crc32_copy_host(ctypes.c_void_p(dbase + doff), ctypes.c_void_p(sbase + soff),
+                                               n, 7)
+                assert got == zlib.crc32(buf[soff:soff + n], 7), (n, soff, doff)
+                out = ctypes.string_at(dbase, len(buf) + 64)
+                assert out[doff:doff + n] == buf[soff:soff + n], (n, soff, doff)
+                assert out[doff + n:doff + n + 16] == b"\xa5" * len(out[doff + n:doff + n + 16])
+                assert out[:doff] == b"\xa5" * doff
