@@ -800,6 +800,18 @@ uint32_t chunk_key_host(const uint8_t* p, uint32_t len) {
 // (drain) or image -> allocation (refill), in 64 KiB-chunk-aligned 4 MiB
 // pieces, and hash what they moved: every chunk's CRC (and, draining, its
 // dirty key) into h_pin_crc / h_pin_key, so no SM reads host memory for them.
+// CRAC_HOST_NT=1: the drain's host threads hash and copy host-run pages and
+// pinned payloads in one read, streaming them into the image with
+// non-temporal stores (crc32_copy_stream).  Off by default: neutral on one
+// box, ~4 % slower C3 checkpoints on another (profiles/r02/host_nt.txt).
+bool host_nt_copy() {
+  static const bool on = [] {
+    const char* e = std::getenv("CRAC_HOST_NT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 void copy_pinned_runs(DrainEngine& E, const ImagePlan& P, uint8_t* stream, bool drain) {
   if (P.pinned_runs.empty()) return;
   constexpr uint64_t kPiece = 4ull << 20;  // a multiple of the 64 KiB chunk
@@ -815,15 +827,17 @@ void copy_pinned_runs(DrainEngine& E, const ImagePlan& P, uint8_t* stream, bool 
     const uint64_t o = pieces[i].second, n = std::min(kPiece, run.hi - run.lo - o);
     uint8_t* host = reinterpret_cast<uint8_t*>(run.host) + o;
     uint8_t* img = stream + run.lo + o;
+    const bool nt = drain && host_nt_copy();
+    if (drain && !nt) std::memcpy(img, host, n);
     if (!drain) std::memcpy(host, img, n);
     for (uint64_t c = 0; c < n; c += DrainEngine::kChunk) {
       const uint32_t len = uint32_t(std::min<uint64_t>(DrainEngine::kChunk, n - c));
       const uint64_t slot = run.pin0 + (o + c) / DrainEngine::kChunk;
-      // drain: each chunk read once, hashed and streamed into the image
-      E.h_pin_crc.ptr[slot] = drain ? crc32_copy_stream(img + c, host + c, len) : crc32_fast(host + c, len);
+      // (nt: each chunk read once, hashed and streamed into the image)
+      E.h_pin_crc.ptr[slot] = nt ? crc32_copy_stream(img + c, host + c, len) : crc32_fast(host + c, len);
       if (drain) E.h_pin_key.ptr[slot] = chunk_key_host(host + c, len);
     }
-    if (drain) stream_fence();
+    if (nt) stream_fence();
   }, /*min_parallel=*/2);
 }
 
@@ -1083,11 +1097,7 @@ void host_pages_drain(DrainEngine& E, const ImagePlan& P, uint8_t* stream, uint6
   uint32_t* crc = E.h_host_crc.ptr;
   constexpr uint64_t W = DrainEngine::kWindow;
   const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  // CRAC_HOST_NT=0: host-run pages copied with memcpy after their CRC
-  static const bool nt_copy = [] {
-    const char* e = std::getenv("CRAC_HOST_NT");
-    return !(e && e[0] == '0');
-  }();
+  const bool nt_copy = host_nt_copy();
   std::atomic<uint64_t> next{0};
   std::atomic<int> failed{0};
   auto worker = [&] {
@@ -1098,10 +1108,12 @@ void host_pages_drain(DrainEngine& E, const ImagePlan& P, uint8_t* stream, uint6
         const auto* src = reinterpret_cast<const uint8_t*>(h.ptr);
         if (h.own_frame) {  // in a host run: no window copy touches these bytes
           std::memcpy(stream + h.stream_off - 16, P.recs[h.rec].frame, 16);
-          // one read of the page: hashed and streamed into the image (no
-          // read-for-ownership of the image lines)
-          crc[i] = nt_copy ? crc32_copy_stream(stream + h.stream_off, src, h.len)
-                           : (std::memcpy(stream + h.stream_off, src, h.len), crc32_fast(src, h.len));
+          if (nt_copy) {  // one read of the page, streamed into the image
+            crc[i] = crc32_copy_stream(stream + h.stream_off, src, h.len);
+          } else {
+            crc[i] = crc32_fast(src, h.len);
+            std::memcpy(stream + h.stream_off, src, h.len);
+          }
           continue;
         }
         crc[i] = crc32_fast(src, h.len);
@@ -1119,7 +1131,7 @@ void host_pages_drain(DrainEngine& E, const ImagePlan& P, uint8_t* stream, uint6
         }
         std::memcpy(stream + h.stream_off, src, h.len);
       }
-    stream_fence();  // the streamed image bytes are visible before the join
+    if (nt_copy) stream_fence();  // the streamed image bytes are visible before the join
   };
   std::vector<std::thread> pool;
   for (unsigned t = 1; t < hw; ++t) pool.emplace_back(worker);
